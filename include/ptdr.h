@@ -1,0 +1,156 @@
+/*
+ * ptdr.h -- C ABI of libptdr.so, the B200 (sm_100a) Pauli-decomposition hot path.
+ *
+ * Operation (Sec. II-A): for A in C^{2^n x 2^n},
+ * compute every coefficient of A = sum_P alpha_P P over the 4^n Pauli strings
+ * P = sigma_{n-1} (x) ... (x) sigma_0 (l.178), alpha_P = Tr(P A) / 2^n (l.151)
+ * = tr(P^* A) / 2^n (P is Hermitian, l.128).
+ *
+ * Output order ("q order"): q = sum_l code(sigma_l) 4^l with code I=0, X=1, Y=2,
+ * Z=3, i.e. ascending text-lexicographic order of the string, leftmost letter
+ * (sigma_{n-1}) most significant -- the order of "alpha_II, alpha_IX, alpha_IY, ..."
+ * (l.143).  DESIGN.md reading R5.
+ *
+ * Memory: every pointer argument is a DEVICE pointer (cudaMalloc / torch CUDA
+ * tensor memory) unless the function name ends in _host.  The caller owns all
+ * memory; the library keeps no global mutable state except a thread-local error
+ * string and a per-device cache of launch parameters, allocates nothing persistent,
+ * and is reentrant given distinct workspaces.  Element type: ptdr_c128 =
+ * interleaved (re, im) binary64 (== cuDoubleComplex == torch.complex128), 16-byte
+ * aligned.  Streams are passed as `void*` holding a cudaStream_t (NULL = legacy
+ * default stream).
+ *
+ * Errors: functions return ptdr_status and never abort or throw across the ABI.
+ *   PTDR_EINVAL       bad n, structure, null / misaligned pointer, world/rank
+ *   PTDR_EUNSUPPORTED valid but not implemented combination (e.g. out aliases A)
+ *   PTDR_ENOMEM       workspace smaller than ptdr_workspace_bytes(), or a
+ *                     temporary allocation in ptdr_decompose / _host failed
+ *   PTDR_ECUDA        a CUDA API / launch error; detail in ptdr_last_error().
+ *                     Asynchronous faults surface at the caller's next stream sync.
+ */
+#ifndef PTDR_H_
+#define PTDR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+  double re, im;
+} ptdr_c128;
+
+/* Declared structure of A (trusted, not verified: SPEC.md l.202).
+ *  GENERAL        dense row-major A[i][j] at offset i*2^n + j                    (l.294)
+ *  HERMITIAN      dense storage; only the upper triangle and the real part of the
+ *                 diagonal are read; output has Im == 0 exactly (Theorem 2, l.123-136)
+ *  REAL_SYMMETRIC dense storage; only Re of the upper triangle + diagonal is read;
+ *                 output real, exact zeros where n_Y is odd
+ *  DIAGONAL       A = band array d[2^n] (d[i] = A[i][i]); output = the 2^n {I,Z}^n
+ *                 coefficients (l.369-389, Table I l.511), ascending z (see below)
+ *  TRIDIAGONAL    A = band array [3][2^n]: sub[i]=A[i][i-1] (sub[0] ignored),
+ *                 main[i]=A[i][i], sup[i]=A[i][i+1] (sup[2^n-1] ignored); output =
+ *                 the (n+1) blocks of 2^n coefficients that can be nonzero
+ *                 (Theorem l.404-406, Table I l.513): block b holds the X-mask
+ *                 x_b = 2^b - 1 (b = 0: the {I,Z}^n strings; b = n: the {X,Y}^n
+ *                 strings), and inside a block coefficients are in ascending
+ *                 Z-mask z, which is ascending q order restricted to that block.
+ * X-mask / Z-mask of a string: bit l of x is set iff sigma_l in {X,Y}; bit l of z
+ * is set iff sigma_l in {Y,Z}. */
+typedef enum {
+  PTDR_GENERAL = 0,
+  PTDR_HERMITIAN = 1,
+  PTDR_REAL_SYMMETRIC = 2,
+  PTDR_DIAGONAL = 3,
+  PTDR_TRIDIAGONAL = 4
+} ptdr_structure;
+
+typedef enum {
+  PTDR_OK = 0,
+  PTDR_EINVAL = 1,
+  PTDR_EUNSUPPORTED = 2,
+  PTDR_ENOMEM = 3,
+  PTDR_ECUDA = 4
+} ptdr_status;
+
+/* Supported n: dense structures 1 <= n <= 16; DIAGONAL / TRIDIAGONAL 1 <= n <= 28. */
+int ptdr_max_n(int structure);
+
+/* Number of ptdr_c128 elements of the input A: 4^n (dense), 2^n (DIAGONAL),
+ * 3*2^n (TRIDIAGONAL).  0 if (n, structure) is invalid. */
+size_t ptdr_input_count(int n, int structure);
+
+/* Number of ptdr_c128 output coefficients: 4^n, 2^n (DIAGONAL), (n+1)*2^n
+ * (TRIDIAGONAL).  0 if invalid. */
+size_t ptdr_output_count(int n, int structure);
+
+/* Device workspace bytes needed by ptdr_decompose_async for (n, structure) on one
+ * GPU (world = 1) or per rank of ptdr_decompose_xshard_async (world > 1).
+ * Deterministic in its arguments.  (size_t)-1 if invalid. */
+size_t ptdr_workspace_bytes(int n, int structure, int world);
+
+/* Synchronous convenience: allocates the workspace with cudaMallocAsync on the
+ * default stream, runs, synchronizes, frees.  A, out: device pointers. */
+ptdr_status ptdr_decompose(const ptdr_c128* A, int n, int structure, ptdr_c128* out);
+
+/* Asynchronous on `stream`.  A: device, ptdr_input_count(n,structure) elements.
+ * out: device, ptdr_output_count elements, must not overlap A.  workspace:
+ * device, >= ptdr_workspace_bytes(n, structure, 1) bytes, 256-byte aligned,
+ * contents ignored on entry and undefined on exit; it must not be used by
+ * another call until this call's work on `stream` has completed. */
+ptdr_status ptdr_decompose_async(const ptdr_c128* A, int n, int structure, ptdr_c128* out,
+                                 void* workspace, size_t ws_bytes, void* stream);
+
+/* End-to-end from HOST memory: copies A_host to the device, decomposes, copies the
+ * result to out_host, synchronizes.  Host buffers may be pageable or pinned
+ * (pinned is faster).  Allocates and frees its own device buffers. */
+ptdr_status ptdr_decompose_host(const ptdr_c128* A_host, int n, int structure,
+                                ptdr_c128* out_host);
+
+/* Multi-GPU, per rank, GENERAL only, after the caller's all-to-all (DESIGN.md
+ * "Multi-GPU").  world = 2^g GPUs, R = 2^n / world.  Rank `rank` owns the X-masks
+ * x with x >> (n-g) == rank.  A_local: device [2^n][R] row-major with
+ * A_local[i][c] = A[i][((i >> (n-g)) ^ rank) * R + c].  out_local: device
+ * 4^n / world coefficients: the q-ordered subsequence of rank's strings, i.e.
+ * out_local[zt * 4^(n-g) + (q mod 4^(n-g))] for the string (x, z) with
+ * zt = z >> (n-g).  Requires n - g >= 4. */
+ptdr_status ptdr_decompose_xshard_async(const ptdr_c128* A_local, int n, int rank, int world,
+                                        ptdr_c128* out_local, void* workspace, size_t ws_bytes,
+                                        void* stream);
+
+/* Seeded counter-based generator (the paper fixes no
+ * distribution, "a generic matrix", l.631).  Writes rows [row0, row0+nrows) of the
+ * dense variant (0 GENERAL, 1 HERMITIAN, 2 REAL_SYMMETRIC) into A (row-major,
+ * nrows x 2^n), entry = Philox4x32-10(counter = global element index) + Box-Muller.
+ * Bitwise independent of the row split (any sharding sees the same matrix). */
+ptdr_status ptdr_generate_dense_async(int n, uint64_t seed, int variant, uint64_t row0,
+                                      uint64_t nrows, ptdr_c128* A, void* stream);
+
+/* Same generator for the band inputs: variant 3 (DIAGONAL) writes d[2^n] into
+ * band; variant 4 (TRIDIAGONAL) writes the [3][2^n] sub/main/sup array. */
+ptdr_status ptdr_generate_band_async(int n, uint64_t seed, int variant, ptdr_c128* band,
+                                     void* stream);
+
+/* Same generator, but writes the column-block-major send layout used by the
+ * multi-GPU all-to-all: for rank `rank` of `world`, R = 2^n/world, block b of
+ * the output ([world][R][R]) holds rows rank*R.. of column block (rank ^ b),
+ * i.e. send[b][r][c] = A[rank*R + r][(rank ^ b)*R + c].  Then a plain equal-split
+ * all-to-all delivers exactly ptdr_decompose_xshard_async's A_local layout. */
+ptdr_status ptdr_generate_sendblocks_async(int n, uint64_t seed, int rank, int world,
+                                           ptdr_c128* send, void* stream);
+
+/* Number of kernel launches the last successful call on this host thread enqueued
+ * (used by bench.py's gpu_launches count). */
+int ptdr_last_launch_count(void);
+
+const char* ptdr_status_string(int status);
+const char* ptdr_last_error(void); /* thread-local detail of the last failure */
+int ptdr_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PTDR_H_ */

@@ -1,0 +1,272 @@
+"""Python binding of libptdr.so -- argument marshalling only.
+
+Every step of the decomposition runs in the CUDA kernels behind the C ABI
+(include/ptdr.h).  PyTorch is used only for device memory and streams.  There
+is no CPU fallback: if the shared library is missing or CUDA is unavailable the
+calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libptdr.so")
+
+STRUCTURES = {
+    "general": 0,
+    "hermitian": 1,
+    "real_symmetric": 2,
+    "diagonal": 3,
+    "tridiagonal": 4,
+}
+PTDR_OK, PTDR_EINVAL, PTDR_EUNSUPPORTED, PTDR_ENOMEM, PTDR_ECUDA = 0, 1, 2, 3, 4
+
+
+class PtdrError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{msg} (status {status})")
+        self.status = status
+
+
+_lib = None
+
+
+def lib():
+    """Load libptdr.so (fails loudly if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} not found: build it with `python paper_2403_11644_b200/build.py` "
+                "(or __graft_entry__.build()); there is no CPU fallback")
+        L = ctypes.CDLL(LIB_PATH)
+        i32, u64, sz, vp = ctypes.c_int, ctypes.c_uint64, ctypes.c_size_t, ctypes.c_void_p
+        L.ptdr_max_n.argtypes = [i32]
+        L.ptdr_input_count.argtypes = [i32, i32]
+        L.ptdr_input_count.restype = sz
+        L.ptdr_output_count.argtypes = [i32, i32]
+        L.ptdr_output_count.restype = sz
+        L.ptdr_workspace_bytes.argtypes = [i32, i32, i32]
+        L.ptdr_workspace_bytes.restype = sz
+        L.ptdr_decompose.argtypes = [vp, i32, i32, vp]
+        L.ptdr_decompose_async.argtypes = [vp, i32, i32, vp, vp, sz, vp]
+        L.ptdr_decompose_host.argtypes = [vp, i32, i32, vp]
+        L.ptdr_decompose_xshard_async.argtypes = [vp, i32, i32, i32, vp, vp, sz, vp]
+        L.ptdr_generate_dense_async.argtypes = [i32, u64, i32, u64, u64, vp, vp]
+        L.ptdr_generate_band_async.argtypes = [i32, u64, i32, vp, vp]
+        L.ptdr_generate_sendblocks_async.argtypes = [i32, u64, i32, i32, vp, vp]
+        L.ptdr_status_string.argtypes = [i32]
+        L.ptdr_status_string.restype = ctypes.c_char_p
+        L.ptdr_last_error.restype = ctypes.c_char_p
+        L.ptdr_last_launch_count.restype = i32
+        L.ptdr_version.restype = i32
+        for name in ("ptdr_decompose", "ptdr_decompose_async", "ptdr_decompose_host",
+                     "ptdr_decompose_xshard_async", "ptdr_generate_dense_async",
+                     "ptdr_generate_band_async", "ptdr_generate_sendblocks_async"):
+            getattr(L, name).restype = i32
+        _lib = L
+    return _lib
+
+
+def _check(status: int, what: str):
+    if status != PTDR_OK:
+        L = lib()
+        raise PtdrError(status, f"{what}: {L.ptdr_status_string(status).decode()}: "
+                                f"{L.ptdr_last_error().decode()}")
+
+
+def _structure(s) -> int:
+    return STRUCTURES[s] if isinstance(s, str) else int(s)
+
+
+def _stream_ptr(stream):
+    import torch
+
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def input_count(n: int, structure="general") -> int:
+    return int(lib().ptdr_input_count(n, _structure(structure)))
+
+
+def output_count(n: int, structure="general") -> int:
+    return int(lib().ptdr_output_count(n, _structure(structure)))
+
+
+def workspace_bytes(n: int, structure="general", world: int = 1) -> int:
+    v = int(lib().ptdr_workspace_bytes(n, _structure(structure), world))
+    if v == ctypes.c_size_t(-1).value:
+        raise PtdrError(PTDR_EINVAL, f"invalid (n={n}, structure={structure}, world={world})")
+    return v
+
+
+def last_launch_count() -> int:
+    return int(lib().ptdr_last_launch_count())
+
+
+def _require_cuda_c128(t, name):
+    import torch
+
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype != torch.complex128 or not t.is_contiguous():
+        raise TypeError(f"{name} must be contiguous complex128")
+
+
+def n_of(A, structure="general") -> int:
+    s = _structure(structure)
+    if s <= 2:
+        N = A.shape[-1]
+        if A.dim() != 2 or A.shape[0] != N:
+            raise ValueError("dense A must be 2^n x 2^n")
+    elif s == 3:
+        N = A.numel()
+    else:
+        N = A.numel() // 3
+    n = N.bit_length() - 1
+    if (1 << n) != N:
+        raise ValueError("size must be a power of two (the paper's zero padding is out of scope)")
+    return n
+
+
+def alloc_workspace(n: int, structure="general", world: int = 1, device=None):
+    import torch
+
+    nb = workspace_bytes(n, structure, world)
+    # torch's caching allocator returns >= 512-byte aligned blocks
+    return torch.empty(max(nb, 1), dtype=torch.uint8, device=device)
+
+
+def decompose(A, structure="general", out=None, workspace=None, stream=None):
+    """All Pauli coefficients of A (CUDA complex128) via ptdr_decompose_async.
+
+    Dense structures: A is [2^n, 2^n]; DIAGONAL: d[2^n]; TRIDIAGONAL: [3, 2^n]
+    (sub, main, sup).  Returns `out` (q order, see include/ptdr.h)."""
+    import torch
+
+    _require_cuda_c128(A, "A")
+    s = _structure(structure)
+    n = n_of(A, s)
+    if out is None:
+        out = torch.empty(output_count(n, s), dtype=torch.complex128, device=A.device)
+    _require_cuda_c128(out, "out")
+    if workspace is None:
+        workspace = alloc_workspace(n, s, 1, A.device)
+    st = lib().ptdr_decompose_async(ctypes.c_void_p(A.data_ptr()), n, s,
+                                    ctypes.c_void_p(out.data_ptr()),
+                                    ctypes.c_void_p(workspace.data_ptr()),
+                                    workspace.numel(), _stream_ptr(stream))
+    _check(st, "ptdr_decompose_async")
+    return out
+
+
+def decompose_host(A_host, structure="general", out_host=None):
+    """End-to-end from host memory (numpy or CPU torch tensor, complex128)."""
+    import numpy as np
+
+    s = _structure(structure)
+    a = A_host
+    if not isinstance(a, np.ndarray):
+        a = a.numpy()
+    if a.dtype != np.complex128 or not a.flags.c_contiguous:
+        raise TypeError("A_host must be C-contiguous complex128")
+    N = a.shape[-1] if s <= 2 else (a.size if s == 3 else a.size // 3)
+    n = N.bit_length() - 1
+    if out_host is None:
+        out_host = np.empty(output_count(n, s), dtype=np.complex128)
+    o = out_host if isinstance(out_host, np.ndarray) else out_host.numpy()
+    st = lib().ptdr_decompose_host(ctypes.c_void_p(a.ctypes.data), n, s,
+                                   ctypes.c_void_p(o.ctypes.data))
+    _check(st, "ptdr_decompose_host")
+    return out_host
+
+
+def decompose_xshard(A_local, n: int, rank: int, world: int, out=None, workspace=None,
+                     stream=None):
+    """Per-rank decomposition of the X-mask shard (after the all-to-all)."""
+    import torch
+
+    _require_cuda_c128(A_local, "A_local")
+    if out is None:
+        out = torch.empty((1 << (2 * n)) // world, dtype=torch.complex128, device=A_local.device)
+    if workspace is None:
+        workspace = alloc_workspace(n, "general", world, A_local.device)
+    st = lib().ptdr_decompose_xshard_async(ctypes.c_void_p(A_local.data_ptr()), n, rank, world,
+                                           ctypes.c_void_p(out.data_ptr()),
+                                           ctypes.c_void_p(workspace.data_ptr()),
+                                           workspace.numel(), _stream_ptr(stream))
+    _check(st, "ptdr_decompose_xshard_async")
+    return out
+
+
+_DENSE_VARIANTS = {"general": 0, "hermitian": 1, "real_symmetric": 2}
+
+
+def generate_dense(n: int, seed: int, variant="general", row0: int = 0, nrows=None, out=None,
+                   device=None, stream=None):
+    import torch
+
+    v = _DENSE_VARIANTS.get(variant, variant)
+    N = 1 << n
+    nrows = N - row0 if nrows is None else nrows
+    if out is None:
+        out = torch.empty((nrows, N), dtype=torch.complex128, device=device or "cuda")
+    _require_cuda_c128(out, "out")
+    st = lib().ptdr_generate_dense_async(n, seed, int(v), row0, nrows,
+                                         ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream))
+    _check(st, "ptdr_generate_dense_async")
+    return out
+
+
+def generate_band(n: int, seed: int, variant="tridiagonal", out=None, device=None, stream=None):
+    import torch
+
+    v = _structure(variant)
+    shape = (1 << n,) if v == 3 else (3, 1 << n)
+    if out is None:
+        out = torch.empty(shape, dtype=torch.complex128, device=device or "cuda")
+    _require_cuda_c128(out, "out")
+    st = lib().ptdr_generate_band_async(n, seed, v, ctypes.c_void_p(out.data_ptr()),
+                                        _stream_ptr(stream))
+    _check(st, "ptdr_generate_band_async")
+    return out
+
+
+def generate_sendblocks(n: int, seed: int, rank: int, world: int, out=None, device=None,
+                        stream=None):
+    import torch
+
+    N = 1 << n
+    R = N // world
+    if out is None:
+        out = torch.empty((world, R, R), dtype=torch.complex128, device=device or "cuda")
+    _require_cuda_c128(out, "out")
+    st = lib().ptdr_generate_sendblocks_async(n, seed, rank, world,
+                                              ctypes.c_void_p(out.data_ptr()),
+                                              _stream_ptr(stream))
+    _check(st, "ptdr_generate_sendblocks_async")
+    return out
+
+
+# ---- index helpers (host-side bookkeeping of the q order, include/ptdr.h) ----------
+def q_of(x: int, z: int, n: int) -> int:
+    """q index of the string with X-mask x and Z-mask z (code = 2 z_l + (x_l ^ z_l))."""
+    q = 0
+    for l in range(n):
+        xl, zl = (x >> l) & 1, (z >> l) & 1
+        q |= (2 * zl + (xl ^ zl)) << (2 * l)
+    return q
+
+
+def xz_of(q: int, n: int):
+    x = z = 0
+    for l in range(n):
+        c = (q >> (2 * l)) & 3
+        zl = c >> 1
+        xl = (c & 1) ^ zl
+        x |= xl << l
+        z |= zl << l
+    return x, z

@@ -1,0 +1,355 @@
+// abi.cu -- the C ABI of libptdr.so (include/ptdr.h): validation, workspace
+// layout and dispatch to the kernels.  No torch types, no exceptions across the ABI.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/ptdr.h"
+#include "dense_impl.cuh"
+#include "dense_plan.h"
+#include "internal.h"
+
+namespace ptdr {
+
+static thread_local std::string g_last_error;
+static thread_local int g_last_launches = 0;
+
+static int g_sm_count[64] = {0};
+
+int device_sm_count() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (g_sm_count[dev] == 0) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+      v = 148;
+    g_sm_count[dev] = v;
+  }
+  return g_sm_count[dev];
+}
+
+static ptdr_status fail(ptdr_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+static ptdr_status cuda_fail(cudaError_t e, const char* where) {
+  g_last_error = std::string(where) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+  return PTDR_ECUDA;
+}
+
+static bool is_dense(int s) { return s >= PTDR_GENERAL && s <= PTDR_REAL_SYMMETRIC; }
+static bool is_band(int s) { return s == PTDR_DIAGONAL || s == PTDR_TRIDIAGONAL; }
+static bool valid_n(int n, int s) {
+  if (is_dense(s)) return n >= 1 && n <= 16;
+  if (is_band(s)) return n >= 1 && n <= 28;
+  return false;
+}
+
+static uint64_t dense_chunks(int n) { return n >= 4 ? (1ull << n) / 16 : 1ull; }
+
+// Workspace of the dense path = max over the launches of one call.
+static size_t dense_ws(int n, int s, int world) {
+  if (s == PTDR_GENERAL) {
+    const uint64_t C = world > 1 ? ((1ull << n) / (uint64_t)world) / 16 : dense_chunks(n);
+    return make_dense_plan(n, C).ws_bytes();
+  }
+  if (n <= 8) return make_dense_plan(n, dense_chunks(n)).ws_bytes();
+  size_t a = make_dense_plan(n, 1).ws_bytes();
+  size_t b = make_dense_plan(n - 1, dense_chunks(n) - 1).ws_bytes();
+  return a > b ? a : b;
+}
+
+static ptdr_status launch_mode(int mode, const DenseArgs& a, const DensePlan& p, cudaStream_t st,
+                               int* nl) {
+  cudaError_t e;
+  switch (mode) {
+    case MODE_GENERAL: e = launch_dense_mode0(a, p, st, nl); break;
+    case MODE_HERM_MIRROR: e = launch_dense_mode1(a, p, st, nl); break;
+    case MODE_SYM_MIRROR: e = launch_dense_mode2(a, p, st, nl); break;
+    case MODE_HERM_HALF: e = launch_dense_mode3(a, p, st, nl); break;
+    default: e = launch_dense_mode4(a, p, st, nl); break;
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "dense kernel launch");
+  return PTDR_OK;
+}
+
+static DenseArgs base_args(const double2* A, double2* out, int n, void* ws) {
+  DenseArgs a{};
+  a.A = A;
+  a.out = out;
+  a.n = n;
+  a.ld = 1ull << n;
+  a.colmask = (1ull << n) - 1ull;
+  a.gshift = n;
+  a.scale = std::ldexp(1.0, -n);
+  a.ctr = reinterpret_cast<unsigned*>(ws);
+  return a;
+}
+
+static ptdr_status run_dense(const double2* A, int n, int s, double2* out, void* ws,
+                             cudaStream_t st, int* nl) {
+  const uint64_t C = dense_chunks(n);
+  if (s == PTDR_GENERAL || n <= 8) {
+    const int mode = s == PTDR_GENERAL ? MODE_GENERAL
+                     : s == PTDR_HERMITIAN ? MODE_HERM_MIRROR : MODE_SYM_MIRROR;
+    DensePlan p = make_dense_plan(n, C);
+    DenseArgs a = base_args(A, out, n, ws);
+    a.nv = n;
+    a.x_base = 0;
+    a.nchunks = C;
+    a.scratch = reinterpret_cast<double2*>(reinterpret_cast<char*>(ws) + p.ctr_bytes);
+    return launch_mode(mode, a, p, st, nl);
+  }
+  // HERMITIAN / REAL_SYMMETRIC, n >= 9: chunk 0 (x < 16) on full-length mirrored
+  // vectors, then chunks 1.. on half-length vectors.
+  {
+    DensePlan p = make_dense_plan(n, 1);
+    DenseArgs a = base_args(A, out, n, ws);
+    a.nv = n;
+    a.x_base = 0;
+    a.nchunks = 1;
+    a.scratch = reinterpret_cast<double2*>(reinterpret_cast<char*>(ws) + p.ctr_bytes);
+    ptdr_status r = launch_mode(s == PTDR_HERMITIAN ? MODE_HERM_MIRROR : MODE_SYM_MIRROR, a, p, st, nl);
+    if (r != PTDR_OK) return r;
+  }
+  {
+    DensePlan p = make_dense_plan(n - 1, C - 1);
+    DenseArgs a = base_args(A, out, n, ws);
+    a.nv = n - 1;
+    a.x_base = 16;
+    a.nchunks = C - 1;
+    a.scratch = reinterpret_cast<double2*>(reinterpret_cast<char*>(ws) + p.ctr_bytes);
+    return launch_mode(s == PTDR_HERMITIAN ? MODE_HERM_HALF : MODE_SYM_HALF, a, p, st, nl);
+  }
+}
+
+static bool overlaps(const void* a, size_t abytes, const void* b, size_t bbytes) {
+  const uintptr_t a0 = (uintptr_t)a, b0 = (uintptr_t)b;
+  return a0 < b0 + bbytes && b0 < a0 + abytes;
+}
+
+}  // namespace ptdr
+
+using namespace ptdr;
+
+extern "C" {
+
+int ptdr_version(void) { return 1; }
+
+int ptdr_max_n(int structure) {
+  if (is_dense(structure)) return 16;
+  if (is_band(structure)) return 28;
+  return 0;
+}
+
+size_t ptdr_input_count(int n, int s) {
+  if (!valid_n(n, s)) return 0;
+  const size_t N = (size_t)1 << n;
+  if (is_dense(s)) return N * N;
+  return s == PTDR_DIAGONAL ? N : 3 * N;
+}
+
+size_t ptdr_output_count(int n, int s) {
+  if (!valid_n(n, s)) return 0;
+  const size_t N = (size_t)1 << n;
+  if (is_dense(s)) return N * N;
+  return s == PTDR_DIAGONAL ? N : (size_t)(n + 1) * N;
+}
+
+size_t ptdr_workspace_bytes(int n, int s, int world) {
+  if (!valid_n(n, s) || world < 1 || (world & (world - 1))) return (size_t)-1;
+  if (world > 1) {
+    if (s != PTDR_GENERAL) return (size_t)-1;
+    const int g = __builtin_ctz((unsigned)world);
+    if (n - g < 4) return (size_t)-1;
+  }
+  if (is_dense(s)) return dense_ws(n, s, world);
+  return band_workspace_bytes(n, s);
+}
+
+const char* ptdr_status_string(int status) {
+  switch (status) {
+    case PTDR_OK: return "PTDR_OK";
+    case PTDR_EINVAL: return "PTDR_EINVAL";
+    case PTDR_EUNSUPPORTED: return "PTDR_EUNSUPPORTED";
+    case PTDR_ENOMEM: return "PTDR_ENOMEM";
+    case PTDR_ECUDA: return "PTDR_ECUDA";
+    default: return "PTDR_UNKNOWN";
+  }
+}
+
+const char* ptdr_last_error(void) { return g_last_error.c_str(); }
+
+int ptdr_last_launch_count(void) { return g_last_launches; }
+
+ptdr_status ptdr_decompose_async(const ptdr_c128* A, int n, int structure, ptdr_c128* out,
+                                 void* workspace, size_t ws_bytes, void* stream) {
+  g_last_launches = 0;
+  if (!valid_n(n, structure)) return fail(PTDR_EINVAL, "invalid n or structure");
+  if (!A || !out) return fail(PTDR_EINVAL, "null A or out");
+  if (((uintptr_t)A & 15) || ((uintptr_t)out & 15)) return fail(PTDR_EINVAL, "A/out not 16-byte aligned");
+  const size_t need = ptdr_workspace_bytes(n, structure, 1);
+  if (need > 0) {
+    if (!workspace) return fail(PTDR_ENOMEM, "workspace required");
+    if ((uintptr_t)workspace & 255) return fail(PTDR_EINVAL, "workspace not 256-byte aligned");
+  }
+  if (ws_bytes < need) return fail(PTDR_ENOMEM, "workspace too small");
+  const size_t inb = ptdr_input_count(n, structure) * 16, outb = ptdr_output_count(n, structure) * 16;
+  if (overlaps(A, inb, out, outb)) return fail(PTDR_EUNSUPPORTED, "out overlaps A");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int nl = 0;
+  ptdr_status r;
+  if (is_dense(structure)) {
+    r = run_dense(reinterpret_cast<const double2*>(A), n, structure, reinterpret_cast<double2*>(out),
+                  workspace, st, &nl);
+  } else {
+    cudaError_t e = launch_band(reinterpret_cast<const double2*>(A), reinterpret_cast<double2*>(out), n,
+                                structure, workspace, st, &nl);
+    r = e == cudaSuccess ? PTDR_OK : cuda_fail(e, "band kernel launch");
+  }
+  g_last_launches = nl;
+  return r;
+}
+
+ptdr_status ptdr_decompose_xshard_async(const ptdr_c128* A_local, int n, int rank, int world,
+                                        ptdr_c128* out_local, void* workspace, size_t ws_bytes,
+                                        void* stream) {
+  g_last_launches = 0;
+  if (world < 1 || (world & (world - 1))) return fail(PTDR_EINVAL, "world must be a power of two");
+  if (rank < 0 || rank >= world) return fail(PTDR_EINVAL, "rank out of range");
+  if (!valid_n(n, PTDR_GENERAL)) return fail(PTDR_EINVAL, "invalid n");
+  const int g = __builtin_ctz((unsigned)world);
+  if (n - g < 4) return fail(PTDR_EINVAL, "need n - log2(world) >= 4");
+  if (!A_local || !out_local) return fail(PTDR_EINVAL, "null pointer");
+  if (((uintptr_t)A_local & 15) || ((uintptr_t)out_local & 15)) return fail(PTDR_EINVAL, "misaligned");
+  const size_t need = ptdr_workspace_bytes(n, PTDR_GENERAL, world);
+  if (need > 0 && (!workspace || ((uintptr_t)workspace & 255)))
+    return fail(PTDR_EINVAL, "workspace missing or not 256-byte aligned");
+  if (ws_bytes < need) return fail(PTDR_ENOMEM, "workspace too small");
+  const uint64_t N = 1ull << n, R = N >> g;
+  if (overlaps(A_local, N * R * 16, out_local, N * R * 16)) return fail(PTDR_EUNSUPPORTED, "out overlaps A");
+  const uint64_t C = R / 16;
+  DensePlan p = make_dense_plan(n, C);
+  if (p.kind == 1) p.kind = 0;  // shards narrower than a single-phase tile: direct kernel
+  DenseArgs a = base_args(reinterpret_cast<const double2*>(A_local), reinterpret_cast<double2*>(out_local),
+                          n, workspace);
+  a.ld = R;
+  a.colmask = R - 1;
+  a.gshift = n - g;
+  a.nv = n;
+  a.x_base = (uint64_t)rank * R;
+  a.nchunks = C;
+  a.scratch = reinterpret_cast<double2*>(reinterpret_cast<char*>(workspace) + p.ctr_bytes);
+  int nl = 0;
+  ptdr_status r = launch_mode(MODE_GENERAL, a, p, reinterpret_cast<cudaStream_t>(stream), &nl);
+  g_last_launches = nl;
+  return r;
+}
+
+ptdr_status ptdr_decompose(const ptdr_c128* A, int n, int structure, ptdr_c128* out) {
+  if (!valid_n(n, structure)) return fail(PTDR_EINVAL, "invalid n or structure");
+  const size_t need = ptdr_workspace_bytes(n, structure, 1);
+  void* ws = nullptr;
+  cudaError_t e;
+  if (need > 0 && (e = cudaMalloc(&ws, need)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(PTDR_ENOMEM, std::string("cudaMalloc workspace: ") + cudaGetErrorString(e));
+  }
+  ptdr_status r = ptdr_decompose_async(A, n, structure, out, ws, need, nullptr);
+  const int nl = g_last_launches;
+  e = cudaDeviceSynchronize();
+  if (ws) cudaFree(ws);
+  g_last_launches = nl;
+  if (r != PTDR_OK) return r;
+  if (e != cudaSuccess) return cuda_fail(e, "ptdr_decompose sync");
+  return PTDR_OK;
+}
+
+ptdr_status ptdr_decompose_host(const ptdr_c128* A_host, int n, int structure,
+                                ptdr_c128* out_host) {
+  if (!valid_n(n, structure)) return fail(PTDR_EINVAL, "invalid n or structure");
+  if (!A_host || !out_host) return fail(PTDR_EINVAL, "null host pointer");
+  const size_t inb = ptdr_input_count(n, structure) * 16;
+  const size_t outb = ptdr_output_count(n, structure) * 16;
+  const size_t need = ptdr_workspace_bytes(n, structure, 1);
+  cudaStream_t st;
+  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
+  void *dA = nullptr, *dO = nullptr, *ws = nullptr;
+  ptdr_status r = PTDR_OK;
+  int nl = 0;
+  do {
+    if ((e = cudaMallocAsync(&dA, inb, st)) != cudaSuccess ||
+        (e = cudaMallocAsync(&dO, outb, st)) != cudaSuccess ||
+        (need > 0 && (e = cudaMallocAsync(&ws, need, st)) != cudaSuccess)) {
+      r = fail(PTDR_ENOMEM, std::string("device allocation: ") + cudaGetErrorString(e));
+      cudaGetLastError();
+      break;
+    }
+    if ((e = cudaMemcpyAsync(dA, A_host, inb, cudaMemcpyHostToDevice, st)) != cudaSuccess) {
+      r = cuda_fail(e, "H2D copy");
+      break;
+    }
+    r = ptdr_decompose_async(reinterpret_cast<const ptdr_c128*>(dA), n, structure,
+                             reinterpret_cast<ptdr_c128*>(dO), ws, need, st);
+    nl = g_last_launches;
+    if (r != PTDR_OK) break;
+    if ((e = cudaMemcpyAsync(out_host, dO, outb, cudaMemcpyDeviceToHost, st)) != cudaSuccess) {
+      r = cuda_fail(e, "D2H copy");
+      break;
+    }
+  } while (0);
+  if (dA) cudaFreeAsync(dA, st);
+  if (dO) cudaFreeAsync(dO, st);
+  if (ws) cudaFreeAsync(ws, st);
+  e = cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  g_last_launches = nl;
+  if (r == PTDR_OK && e != cudaSuccess) r = cuda_fail(e, "ptdr_decompose_host sync");
+  return r;
+}
+
+ptdr_status ptdr_generate_dense_async(int n, uint64_t seed, int variant, uint64_t row0,
+                                      uint64_t nrows, ptdr_c128* A, void* stream) {
+  g_last_launches = 0;
+  if (n < 1 || n > 16 || variant < 0 || variant > 2) return fail(PTDR_EINVAL, "invalid n or variant");
+  if (!A || ((uintptr_t)A & 15)) return fail(PTDR_EINVAL, "null or misaligned A");
+  if (row0 + nrows > (1ull << n)) return fail(PTDR_EINVAL, "rows out of range");
+  cudaError_t e = launch_generate_dense(n, seed, variant, row0, nrows, reinterpret_cast<double2*>(A),
+                                        reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "generator launch");
+  g_last_launches = nrows ? 1 : 0;
+  return PTDR_OK;
+}
+
+ptdr_status ptdr_generate_band_async(int n, uint64_t seed, int variant, ptdr_c128* band,
+                                     void* stream) {
+  g_last_launches = 0;
+  if (n < 1 || n > 28 || (variant != 3 && variant != 4)) return fail(PTDR_EINVAL, "invalid n or variant");
+  if (!band || ((uintptr_t)band & 15)) return fail(PTDR_EINVAL, "null or misaligned band");
+  cudaError_t e = launch_generate_band(n, seed, variant, reinterpret_cast<double2*>(band),
+                                       reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "generator launch");
+  g_last_launches = 1;
+  return PTDR_OK;
+}
+
+ptdr_status ptdr_generate_sendblocks_async(int n, uint64_t seed, int rank, int world,
+                                           ptdr_c128* send, void* stream) {
+  g_last_launches = 0;
+  if (n < 1 || n > 16 || world < 1 || (world & (world - 1)) || rank < 0 || rank >= world ||
+      (uint64_t)world > (1ull << n))
+    return fail(PTDR_EINVAL, "invalid n / rank / world");
+  if (!send || ((uintptr_t)send & 15)) return fail(PTDR_EINVAL, "null or misaligned send buffer");
+  cudaError_t e = launch_generate_sendblocks(n, seed, rank, world, reinterpret_cast<double2*>(send),
+                                             reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "generator launch");
+  g_last_launches = 1;
+  return PTDR_OK;
+}
+
+}  // extern "C"

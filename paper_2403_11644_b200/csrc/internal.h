@@ -1,0 +1,34 @@
+// internal.h -- declarations shared by the translation units of libptdr.so.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace ptdr {
+
+struct DenseArgs;
+struct DensePlan;
+
+int device_sm_count();  // SMs of the current device (cached per device)
+
+cudaError_t launch_dense_mode0(const DenseArgs& a, const DensePlan& p, cudaStream_t st, int* nl);
+cudaError_t launch_dense_mode1(const DenseArgs& a, const DensePlan& p, cudaStream_t st, int* nl);
+cudaError_t launch_dense_mode2(const DenseArgs& a, const DensePlan& p, cudaStream_t st, int* nl);
+cudaError_t launch_dense_mode3(const DenseArgs& a, const DensePlan& p, cudaStream_t st, int* nl);
+cudaError_t launch_dense_mode4(const DenseArgs& a, const DensePlan& p, cudaStream_t st, int* nl);
+
+// band paths (band.cu)
+size_t band_workspace_bytes(int n, int structure);
+cudaError_t launch_band(const double2* A, double2* out, int n, int structure, void* ws,
+                        cudaStream_t st, int* nl);
+
+// generators (generate.cu)
+cudaError_t launch_generate_dense(int n, uint64_t seed, int variant, uint64_t row0,
+                                  uint64_t nrows, double2* A, cudaStream_t st);
+cudaError_t launch_generate_band(int n, uint64_t seed, int variant, double2* band,
+                                 cudaStream_t st);
+cudaError_t launch_generate_sendblocks(int n, uint64_t seed, int rank, int world, double2* send,
+                                       cudaStream_t st);
+
+}  // namespace ptdr

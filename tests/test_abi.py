@@ -1,0 +1,96 @@
+"""CPU checks of the C-ABI library: it loads and exports every declared symbol,
+and its pure host functions (sizes, workspace, validation) behave as documented.
+No compute call is made here (no GPU)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2403_11644_b200 as ptdr
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    with open(os.path.join(ROOT, "include", "ptdr.h")) as f:
+        src = f.read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(ptdr_[a-z0-9_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2403_11644_b200 import build
+
+    build.build()
+    return ptdr.lib()
+
+
+def test_exports_every_declared_symbol(L):
+    syms = _declared_symbols()
+    assert len(syms) >= 15
+    for s in syms:
+        assert hasattr(L, s), s
+
+
+def test_counts(L):
+    assert ptdr.input_count(15) == 1 << 30
+    assert ptdr.output_count(15) == 1 << 30
+    assert ptdr.input_count(24, "diagonal") == 1 << 24
+    assert ptdr.input_count(24, "tridiagonal") == 3 << 24
+    assert ptdr.output_count(24, "tridiagonal") == 25 << 24
+    assert ptdr.output_count(0) == 0 and ptdr.output_count(17) == 0
+    assert L.ptdr_max_n(0) == 16 and L.ptdr_max_n(4) == 28
+
+
+def test_workspace_is_deterministic_and_small(L):
+    for n in range(1, 17):
+        for s in ("general", "hermitian", "real_symmetric"):
+            a = ptdr.workspace_bytes(n, s)
+            assert a == ptdr.workspace_bytes(n, s)
+            # the scratch ring stays a small fraction of the 126 MB L2 + counters
+            assert a <= 80 << 20, (n, s, a)
+    assert ptdr.workspace_bytes(24, "diagonal") == 0
+    assert ptdr.workspace_bytes(24, "tridiagonal") == 2 * (1 << 24) * 16
+    with pytest.raises(ptdr.PtdrError):
+        ptdr.workspace_bytes(15, "hermitian", 2)     # sharding is GENERAL only
+    with pytest.raises(ptdr.PtdrError):
+        ptdr.workspace_bytes(15, "general", 3)       # world must be a power of two
+    assert ptdr.workspace_bytes(15, "general", 8) > 0
+
+
+def test_validation_without_gpu(L):
+    # argument validation happens before any CUDA call
+    st = L.ptdr_decompose_async(None, 5, 0, None, None, 0, None)
+    assert st == ptdr.PTDR_EINVAL
+    st = L.ptdr_decompose_async(ctypes.c_void_p(16), 0, 0, ctypes.c_void_p(4096), None, 0, None)
+    assert st == ptdr.PTDR_EINVAL                   # n = 0 rejected
+    st = L.ptdr_decompose_async(ctypes.c_void_p(8), 3, 0, ctypes.c_void_p(4096), None, 0, None)
+    assert st == ptdr.PTDR_EINVAL                   # misaligned
+    st = L.ptdr_decompose_async(ctypes.c_void_p(4096), 3, 0, ctypes.c_void_p(4096 + 64), None, 0,
+                                None)
+    assert st == ptdr.PTDR_EUNSUPPORTED             # out overlaps A
+    st = L.ptdr_decompose_async(ctypes.c_void_p(1 << 20), 12, 0, ctypes.c_void_p(1 << 30), None, 0,
+                                None)
+    assert st == ptdr.PTDR_ENOMEM                   # workspace required
+    assert b"workspace" in L.ptdr_last_error()
+    st = L.ptdr_decompose_xshard_async(ctypes.c_void_p(4096), 10, 0, 3, ctypes.c_void_p(1 << 30),
+                                       None, 0, None)
+    assert st == ptdr.PTDR_EINVAL
+    assert L.ptdr_status_string(3) == b"PTDR_ENOMEM"
+
+
+def test_q_helpers_roundtrip():
+    import oracle
+
+    n = 4
+    for q in range(4 ** n):
+        x, z = ptdr.xz_of(q, n)
+        assert ptdr.q_of(x, z, n) == q
+        s = oracle.string_of(q, n)
+        # X-mask bit l set iff sigma_l in {X,Y}; Z-mask bit l set iff sigma_l in {Y,Z}
+        for l in range(n):
+            ch = s[n - 1 - l]
+            assert ((x >> l) & 1) == (ch in "XY")
+            assert ((z >> l) & 1) == (ch in "YZ")

@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -51,21 +52,48 @@ static bool valid_n(int n, int s) {
 
 static uint64_t dense_chunks(int n) { return n >= 4 ? (1ull << n) / 16 : 1ull; }
 
+static bool force_v1() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PTDR_DENSE_V1");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+// Plan for one launch; the workspace formula takes the max over both kernels so the
+// PTDR_DENSE_V1=1 debug switch never needs a bigger workspace.
+static DensePlan plan_for(int mode, int nv, uint64_t C) {
+  const bool v2_ok = (mode == MODE_GENERAL || mode == MODE_HERM_HALF || mode == MODE_SYM_HALF) &&
+                     !force_v1();
+  return make_dense_plan(nv, C, v2_ok);
+}
+static size_t plan_ws(int nv, uint64_t C) {
+  const size_t a = make_dense_plan(nv, C, false).ws_bytes();
+  const size_t b = make_dense_plan(nv, C, true).ws_bytes();
+  return a > b ? a : b;
+}
+
 // Workspace of the dense path = max over the launches of one call.
 static size_t dense_ws(int n, int s, int world) {
   if (s == PTDR_GENERAL) {
     const uint64_t C = world > 1 ? ((1ull << n) / (uint64_t)world) / 16 : dense_chunks(n);
-    return make_dense_plan(n, C).ws_bytes();
+    return plan_ws(n, C);
   }
-  if (n <= 8) return make_dense_plan(n, dense_chunks(n)).ws_bytes();
-  size_t a = make_dense_plan(n, 1).ws_bytes();
-  size_t b = make_dense_plan(n - 1, dense_chunks(n) - 1).ws_bytes();
+  if (n <= 8) return plan_ws(n, dense_chunks(n));
+  size_t a = plan_ws(n, 1);
+  size_t b = plan_ws(n - 1, dense_chunks(n) - 1);
   return a > b ? a : b;
 }
 
 static ptdr_status launch_mode(int mode, const DenseArgs& a, const DensePlan& p, cudaStream_t st,
                                int* nl) {
   cudaError_t e;
+  if (p.v2) {
+    e = launch_dense_v2(mode, a, p, st, nl);
+    if (e != cudaSuccess) return cuda_fail(e, "dense v2 kernel launch");
+    return PTDR_OK;
+  }
   switch (mode) {
     case MODE_GENERAL: e = launch_dense_mode0(a, p, st, nl); break;
     case MODE_HERM_MIRROR: e = launch_dense_mode1(a, p, st, nl); break;
@@ -96,7 +124,7 @@ static ptdr_status run_dense(const double2* A, int n, int s, double2* out, void*
   if (s == PTDR_GENERAL || n <= 8) {
     const int mode = s == PTDR_GENERAL ? MODE_GENERAL
                      : s == PTDR_HERMITIAN ? MODE_HERM_MIRROR : MODE_SYM_MIRROR;
-    DensePlan p = make_dense_plan(n, C);
+    DensePlan p = plan_for(mode, n, C);
     DenseArgs a = base_args(A, out, n, ws);
     a.nv = n;
     a.x_base = 0;
@@ -107,7 +135,7 @@ static ptdr_status run_dense(const double2* A, int n, int s, double2* out, void*
   // HERMITIAN / REAL_SYMMETRIC, n >= 9: chunk 0 (x < 16) on full-length mirrored
   // vectors, then chunks 1.. on half-length vectors.
   {
-    DensePlan p = make_dense_plan(n, 1);
+    DensePlan p = plan_for(MODE_HERM_MIRROR, n, 1);
     DenseArgs a = base_args(A, out, n, ws);
     a.nv = n;
     a.x_base = 0;
@@ -117,13 +145,14 @@ static ptdr_status run_dense(const double2* A, int n, int s, double2* out, void*
     if (r != PTDR_OK) return r;
   }
   {
-    DensePlan p = make_dense_plan(n - 1, C - 1);
+    const int hmode = s == PTDR_HERMITIAN ? MODE_HERM_HALF : MODE_SYM_HALF;
+    DensePlan p = plan_for(hmode, n - 1, C - 1);
     DenseArgs a = base_args(A, out, n, ws);
     a.nv = n - 1;
     a.x_base = 16;
     a.nchunks = C - 1;
     a.scratch = reinterpret_cast<double2*>(reinterpret_cast<char*>(ws) + p.ctr_bytes);
-    return launch_mode(s == PTDR_HERMITIAN ? MODE_HERM_HALF : MODE_SYM_HALF, a, p, st, nl);
+    return launch_mode(hmode, a, p, st, nl);
   }
 }
 
@@ -233,7 +262,7 @@ ptdr_status ptdr_decompose_xshard_async(const ptdr_c128* A_local, int n, int ran
   const uint64_t N = 1ull << n, R = N >> g;
   if (overlaps(A_local, N * R * 16, out_local, N * R * 16)) return fail(PTDR_EUNSUPPORTED, "out overlaps A");
   const uint64_t C = R / 16;
-  DensePlan p = make_dense_plan(n, C);
+  DensePlan p = plan_for(MODE_GENERAL, n, C);
   if (p.kind == 1) p.kind = 0;  // shards narrower than a single-phase tile: direct kernel
   DenseArgs a = base_args(reinterpret_cast<const double2*>(A_local), reinterpret_cast<double2*>(out_local),
                           n, workspace);

@@ -22,6 +22,7 @@ struct DensePlan {
   int NA = 0, NB = 0;  // tiles per chunk in phase A / B (two-phase)
   int L = 0;           // look-ahead (chunks of phase A issued ahead of phase B)
   int nslot = 0;       // scratch ring slots
+  bool v2 = false;     // warp-specialised TMA kernel (dense_v2.cu) instead of dense_impl.cuh
   uint64_t nchunks = 0;
   uint64_t slot_elems = 0;  // complex128 elements per scratch slot
   size_t ctr_bytes = 0;
@@ -29,9 +30,13 @@ struct DensePlan {
   size_t ws_bytes() const { return ctr_bytes + scratch_bytes; }
 };
 
-constexpr int kNominalResidentCtas = 296;  // 148 SMs x 2 CTAs; fixes L deterministically
+// Tiles resident at once on a B200 (fixes L deterministically, independent of the device):
+// v1 = 148 SMs x 2 CTAs; v2 = 148 SMs x 3 pipeline stages.
+constexpr int kNominalResidentCtas = 296;
+constexpr int kNominalResidentV2 = 444;
 
-inline DensePlan make_dense_plan(int nv, uint64_t nchunks) {
+// v2_ok: the caller's MODE can run on the TMA kernel (GENERAL or half-length modes).
+inline DensePlan make_dense_plan(int nv, uint64_t nchunks, bool v2_ok = false) {
   DensePlan p;
   p.nv = nv;
   p.nchunks = nchunks;
@@ -42,8 +47,10 @@ inline DensePlan make_dense_plan(int nv, uint64_t nchunks) {
   else { p.R = 8; p.M = nv - 8; }
   p.NA = 1 << (nv - 8);
   p.NB = 1 << (nv - 8);
+  p.v2 = v2_ok && p.R == 8;
+  const int resident = p.v2 ? kNominalResidentV2 : kNominalResidentCtas;
   int period = p.NA + p.NB;
-  int L = (3 * kNominalResidentCtas + 2 * period - 1) / (2 * period);  // ceil(1.5*ctas/period)
+  int L = (3 * resident + 2 * period - 1) / (2 * period);  // ceil(1.5*resident/period)
   if (L < 1) L = 1;
   if (L > 64) L = 64;
   p.L = L;

@@ -37,6 +37,7 @@ struct DenseArgs {
   int gshift;          // n - log2(world)
   int L;
   int nslot;
+  int discard;         // v2: discard consumed scratch lines from L2 (no write-back)
   double scale;        // 2^-n
 };
 

@@ -33,7 +33,8 @@ struct DensePlan {
 // Tiles resident at once on a B200 (fixes L deterministically, independent of the device):
 // v1 = 148 SMs x 2 CTAs; v2 = 148 SMs x 3 pipeline stages.
 constexpr int kNominalResidentCtas = 296;
-constexpr int kNominalResidentV2 = 444;
+constexpr int kNominalResidentV2 = 592;  // 148 SMs x (3 stages + 1 ticket claimed ahead)
+constexpr uint64_t kV2ScratchBudget = 2ull << 30;  // bytes of scratch slots for the v2 kernel
 
 // v2_ok: the caller's MODE can run on the TMA kernel (GENERAL or half-length modes).
 inline DensePlan make_dense_plan(int nv, uint64_t nchunks, bool v2_ok = false) {
@@ -54,7 +55,19 @@ inline DensePlan make_dense_plan(int nv, uint64_t nchunks, bool v2_ok = false) {
   if (L < 1) L = 1;
   if (L > 64) L = 64;
   p.L = L;
+  // Scratch slots.  A phase-A tile of chunk c waits until phase B of chunk c - nslot has
+  // drained the slot; with ~`resident` tickets in flight that wait is rare only if
+  // nslot >= L + 1 + resident/period.  v2 takes many more slots (capped by a byte budget):
+  // consumed slots are discarded from L2, so only the live ~L chunks occupy L2 and the
+  // extra slots cost HBM capacity, not bandwidth.
   uint64_t ns = (uint64_t)L + 2;
+  if (p.v2) {
+    const uint64_t slot_bytes = ((uint64_t)16 << nv) * 16;
+    uint64_t budget = kV2ScratchBudget / slot_bytes;
+    const uint64_t need = 2ull * (uint64_t)L + 2ull + (uint64_t)(resident / period);
+    if (budget < need) budget = need;
+    ns = budget;
+  }
   if (ns > nchunks) ns = nchunks;
   p.nslot = (int)ns;
   p.slot_elems = (uint64_t)16 << nv;

@@ -14,6 +14,7 @@
 //     (per-thread base + compile-time subset sums of per-bit deltas).
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "dense_impl.cuh"
@@ -117,22 +118,49 @@ __device__ __forceinline__ void emit_all(const DenseArgs& a, const EpiUnit<NB, (
   }
 }
 
+// Ticket order of dense_impl.cuh's decode_ticket, in 32-bit arithmetic with NA = NB = 2^M.
+__device__ __forceinline__ void decode_ticket32(uint32_t t, int M, uint32_t C, uint32_t L, int& phase,
+                                                uint32_t& chunk, uint32_t& tile) {
+  const uint32_t NA = 1u << M;
+  const uint32_t lp1 = (L + 1u < C) ? L + 1u : C;
+  const uint32_t pro = lp1 << M;
+  if (t < pro) {
+    phase = 0; chunk = t >> M; tile = t & (NA - 1u);
+    return;
+  }
+  t -= pro;
+  const uint32_t steady = C > L + 1u ? C - L - 1u : 0u;
+  if (t < (steady << (M + 1))) {
+    const uint32_t c = t >> (M + 1), o = t & (2u * NA - 1u);
+    if (o < NA) { phase = 1; chunk = c; tile = o; }
+    else { phase = 0; chunk = c + L + 1u; tile = o - NA; }
+    return;
+  }
+  t -= steady << (M + 1);
+  phase = 1; chunk = steady + (t >> M); tile = t & (NA - 1u);
+}
+
+// Scratch layout (per chunk slot): B-tile-major, Y[tileB][ih][f] with 4096 elements per
+// phase-B tile, so that a phase-B tile is one contiguous 64 KiB bulk copy.  The fiber
+// index phi = tileB * FB + f encodes (u, zl): bits [0,1]=u0,u1 [2,3]=zl0,zl1 [4,5]=u2,u3
+// [6..]=zl2.. (phi_u / phi_zl in dense_impl.cuh).
 template <int M, int MODE>
 __global__ void __launch_bounds__(kV2Threads, 1)
     dense_v2_kernel(const __grid_constant__ CUtensorMap tmap, DenseArgs a) {
   constexpr bool HALF = (MODE == MODE_HERM_HALF || MODE == MODE_SYM_HALF);
   constexpr int FB = kTileElems >> M;  // phase-B fibers per tile
+  constexpr int LFB = 12 - M;
   extern __shared__ __align__(1024) unsigned char smem[];
   double2* stage0 = reinterpret_cast<double2*>(smem);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kTileBytes);
   uint64_t* empty = full + kStages;
   TileMeta* meta = reinterpret_cast<TileMeta*>(empty + kStages);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int NA = 1 << M;  // tiles per chunk, each phase (nv = 8 + M)
-  const u64 C = a.nchunks;
+  const uint32_t C = (uint32_t)a.nchunks;
   unsigned* ticket = a.ctr;
   unsigned* doneA = a.ctr + 1;
   unsigned* doneB = a.ctr + 1 + C;
+  const uint32_t nslot = (uint32_t)a.nslot;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -148,39 +176,39 @@ __global__ void __launch_bounds__(kV2Threads, 1)
     if (lane == 0) {
       prefetch_tmap(&tmap);
       const uint64_t pol = policy_evict_first();
-      const u64 total = C * (u64)(2 * NA);
+      const uint32_t total = C << (M + 1);
       int tail = 0;
       // tickets are claimed one ahead so the atomic's round trip overlaps the current
       // tile's dependency wait and TMA issue (a claimed ticket is always processed next)
-      u64 next_tk = (u64)atomicAdd(ticket, 1u);
+      uint32_t next_tk = atomicAdd(ticket, 1u);
       for (int k = 0;; ++k) {
         const int s = k % kStages;
         if (k >= kStages) mbar_wait(&empty[s], (uint32_t)((k / kStages) - 1) & 1u);
-        const u64 tk = tail ? total : next_tk;
-        if (tk < total) next_tk = (u64)atomicAdd(ticket, 1u);
+        const uint32_t tk = tail ? total : next_tk;
+        if (tk < total) next_tk = atomicAdd(ticket, 1u);
         if (tk >= total) {
           meta[s].valid = 0;
           mbar_arrive(&full[s]);
           if (++tail == 2) break;
           continue;
         }
-        int phase, tile;
-        u64 chunk;
-        decode_ticket(tk, NA, NA, C, a.L, phase, chunk, tile);
+        int phase;
+        uint32_t chunk, tile;
+        decode_ticket32(tk, M, C, (uint32_t)a.L, phase, chunk, tile);
         if (phase == 0) {
-          if (chunk >= (u64)a.nslot) spin_until(&doneB[chunk - a.nslot], (unsigned)NA);
+          if (chunk >= nslot) spin_until(&doneB[chunk - nslot], 1u << M);
         } else {
-          spin_until(&doneA[chunk], (unsigned)NA);
+          spin_until(&doneA[chunk], 1u << M);
         }
         meta[s].valid = 1;
         meta[s].phase = phase;
-        meta[s].tile = tile;
+        meta[s].tile = (int)tile;
         meta[s].chunk = chunk;
+        double2* dst = stage0 + (size_t)s * kTileElems;
         if (phase == 0) {
           mbar_arrive_expect_tx(&full[s], (uint32_t)kTileBytes);
           const u64 x0 = a.x_base + 16ull * chunk;
           const int t = HALF ? 63 - __clzll(x0) : 0;
-          double2* dst = stage0 + (size_t)s * kTileElems;
 #pragma unroll 4
           for (int rb = 0; rb < 16; ++rb) {
             const u64 iv0 = ((u64)tile << 8) + (u64)rb * 16;
@@ -189,7 +217,11 @@ __global__ void __launch_bounds__(kV2Threads, 1)
             tma_load_2d(dst + rb * 256, &tmap, (int)(col0 * 2), (int)row0, &full[s], pol);
           }
         } else {
-          mbar_arrive(&full[s]);
+          // scratch written by other CTAs' generic stores, read by the async proxy
+          fence_proxy_async_global();
+          mbar_arrive_expect_tx(&full[s], (uint32_t)kTileBytes);
+          const double2* src = a.scratch + (size_t)(chunk % nslot) * a.slot_elems + ((size_t)tile << 12);
+          bulk_load(dst, src, (uint32_t)kTileBytes, &full[s], pol);
         }
       }
     }
@@ -199,20 +231,18 @@ __global__ void __launch_bounds__(kV2Threads, 1)
   // ------------------------------------------------------------------ consumers
   const int g = (warp - 1) / kGroupWarps;
   const int gtid = threadIdx.x - 32 - g * (32 * kGroupWarps);
-  const uint64_t pol_last = policy_evict_last();
   for (int k = g;; k += 2) {
     const int s = k % kStages;
     mbar_wait(&full[s], (uint32_t)(k / kStages) & 1u);
     const TileMeta m = meta[s];
     if (!m.valid) break;
     double2* S = stage0 + (size_t)s * kTileElems;
-    const u64 x0 = a.x_base + 16ull * m.chunk;
-    const int t = HALF ? 63 - __clzll(x0) : 0;
-    double2* Y = a.scratch + (m.chunk % (u64)a.nslot) * a.slot_elems;
+    const uint32_t chunk = (uint32_t)m.chunk;
+    double2* Y = a.scratch + (size_t)(chunk % nslot) * a.slot_elems;
+    double2 v[16];
     if (m.phase == 0) {
       // ---- phase A: v_x[i] for x = x0+u, i = tile*256 + jh*16 + kk (XOR transpose in SMEM)
       const int u = gtid & 15, jh = gtid >> 4;
-      double2 v[16];
 #pragma unroll
       for (int kk = 0; kk < 16; ++kk) {
         v[kk] = S[(jh * 16 + kk) * 16 + (kk ^ u)];
@@ -230,37 +260,45 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       wht_regs<4>(v);
-      double2* base = Y + ((((u64)m.tile << 8) + (u64)jl) << 4) + (u64)u;
+      // element (u, ih = tile, zl = j*16 + jl) -> Y[tileB][ih][f]
+      const uint32_t phi_lo = (uint32_t)((u & 3) | ((jl & 3) << 2) | ((u >> 2) << 4) | ((jl >> 2) << 6));
+      double2* base = Y + (((phi_lo >> LFB) << 12) | ((uint32_t)m.tile << LFB) | (phi_lo & (FB - 1)));
+      const uint64_t pol_last = policy_evict_last();
 #pragma unroll
-      for (int j = 0; j < 16; ++j) st_global_hint(base + (j << 8), v[j], pol_last);
+      for (int j = 0; j < 16; ++j) st_global_hint(base + ((size_t)j << (M - 4 + 12)), v[j], pol_last);
       named_bar_sync(1 + g, 32 * kGroupWarps);
       if (gtid == 0) {
         __threadfence();
-        atomicAdd(&doneA[m.chunk], 1u);
+        atomicAdd(&doneA[chunk], 1u);
       }
     } else {
-      // ---- phase B: WHT over ih for FB fibers (u, zl) + epilogue
-      double2 v[16];
-      {
-        const int f = gtid % FB, jh = gtid / FB;
-        const u64 phi = (u64)m.tile * FB + (u64)f;
-        const double2* src = Y + (phi_zl(phi) << 4) + (u64)phi_u(phi) + ((u64)jh << 16);
+      // ---- phase B: SMEM holds Y[tileB][ih][f] = [j][f]; WHT over j for FB fibers
+      const u64 x0 = a.x_base + 16ull * chunk;
+      const int t = HALF ? 63 - __clzll(x0) : 0;
+      const int f = gtid % FB, jh = gtid / FB;
 #pragma unroll
-        for (int kk = 0; kk < 16; ++kk) v[kk] = __ldcg(src + ((u64)kk << 12));
-        wht_regs<4>(v);
-        if constexpr (M == 4) {
-          if (lane == 0) mbar_arrive(&empty[s]);
-          EpiUnit<4, HALF> e;
-          e.init((uint32_t)x0 + (uint32_t)phi_u(phi), (uint32_t)phi_zl(phi), 8, t, a.gshift);
-          emit_all<MODE, 4>(a, e, v);
-        } else {
-#pragma unroll
-          for (int kk = 0; kk < 16; ++kk) S[(jh * 16 + kk) * FB + f] = v[kk];
-        }
+      for (int kk = 0; kk < 16; ++kk) v[kk] = S[(jh * 16 + kk) * FB + f];
+      if (a.discard) {
+        // the slot region of this tile is dead once in SMEM: drop it from L2 without
+        // write-back (the next writer of the slot waits for doneB of this chunk)
+        char* yb = reinterpret_cast<char*>(Y + ((size_t)m.tile << 12));
+        discard_l2(yb + (size_t)gtid * 256);
+        discard_l2(yb + (size_t)gtid * 256 + 128);
       }
-      if constexpr (M > 4) {
+      wht_regs<4>(v);
+      if constexpr (M == 4) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        const uint32_t phi = (uint32_t)m.tile * FB + (uint32_t)f;
+        EpiUnit<4, HALF> e;
+        e.init((uint32_t)x0 + (uint32_t)phi_u(phi), (uint32_t)phi_zl(phi), 8, t, a.gshift);
+        emit_all<MODE, 4>(a, e, v);
+      } else {
         constexpr int R2 = M - 4;
         constexpr int U2 = 1 << (8 - M);
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) S[(jh * 16 + kk) * FB + f] = v[kk];
         named_bar_sync(1 + g, 32 * kGroupWarps);
 #pragma unroll
         for (int p = 0; p < U2; ++p) {
@@ -276,7 +314,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
         for (int p = 0; p < U2; ++p) {
           const int uu = gtid + 256 * p;
           const int f2 = uu % FB, jl = uu / FB;
-          const u64 phi = (u64)m.tile * FB + (u64)f2;
+          const uint32_t phi = (uint32_t)m.tile * FB + (uint32_t)f2;
           wht_regs<R2>(&v[p * (1 << R2)]);
           EpiUnit<R2, HALF> e;
           e.init((uint32_t)x0 + (uint32_t)phi_u(phi), ((uint32_t)jl << 8) | (uint32_t)phi_zl(phi), 12,
@@ -287,7 +325,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
       named_bar_sync(1 + g, 32 * kGroupWarps);
       if (gtid == 0) {
         __threadfence();
-        atomicAdd(&doneB[m.chunk], 1u);
+        atomicAdd(&doneB[chunk], 1u);
       }
     }
   }
@@ -352,6 +390,10 @@ cudaError_t launch_dense_v2(int mode, const DenseArgs& a_in, const DensePlan& p,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  {
+    const char* nd = getenv("PTDR_NO_DISCARD");
+    a.discard = (nd && nd[0] == '1') ? 0 : 1;
+  }
   cudaError_t e = cudaMemsetAsync(a.ctr, 0, p.ctr_bytes, st);
   if (e != cudaSuccess) return e;
   *nlaunch += 1;

@@ -76,7 +76,7 @@ def test_large_configs_sampled(gpu, cfg):
     out = ptdr.decompose(A, variant)
     torch.cuda.synchronize()
     assert _parseval_gpu(A, out, n) < 1e-11
-    maxabs = torch.max(torch.abs(A)).item()
+    maxabs = max(torch.max(torch.abs(A[i:i + 1024])).item() for i in range(0, A.shape[0], 1024))
     del A
     qs = _sample_qs(n)
     got = out[torch.from_numpy(qs.astype(np.int64)).cuda()].cpu().numpy()

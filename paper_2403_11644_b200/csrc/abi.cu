@@ -52,26 +52,36 @@ static bool valid_n(int n, int s) {
 
 static uint64_t dense_chunks(int n) { return n >= 4 ? (1ull << n) / 16 : 1ull; }
 
-static bool force_v1() {
+// Dense-path kernel selection.  PTDR_DENSE_V1=1 forces the dense_impl.cuh kernels;
+// PTDR_PIPE_CFG=1|2|3 picks a dense_pipe.cu configuration (see dense_plan.h).
+static int pipe_choice() {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("PTDR_DENSE_V1");
-    v = (e && e[0] == '1') ? 1 : 0;
+    const char* e1 = getenv("PTDR_DENSE_V1");
+    const char* ec = getenv("PTDR_PIPE_CFG");
+    if (e1 && e1[0] == '1') v = kPipeNone;
+    else if (ec && ec[0] >= '1' && ec[0] <= '3') v = ec[0] - '0';
+    else v = kPipeCfg11x4;
   }
-  return v == 1;
+  return v;
 }
 
-// Plan for one launch; the workspace formula takes the max over both kernels so the
-// PTDR_DENSE_V1=1 debug switch never needs a bigger workspace.
 static DensePlan plan_for(int mode, int nv, uint64_t C) {
-  const bool v2_ok = (mode == MODE_GENERAL || mode == MODE_HERM_HALF || mode == MODE_SYM_HALF) &&
-                     !force_v1();
-  return make_dense_plan(nv, C, v2_ok);
+  const bool pipe_ok = mode == MODE_GENERAL || mode == MODE_HERM_HALF || mode == MODE_SYM_HALF;
+  int cfg = pipe_ok ? pipe_choice() : kPipeNone;
+  DensePlan p = make_dense_plan(nv, C, cfg);
+  if (pipe_ok && cfg != kPipeNone && p.pipe_cfg == kPipeNone)  // e.g. nv = 16 with LT = 11
+    p = make_dense_plan(nv, C, kPipeCfg12);
+  return p;
 }
+// The workspace is the max over every kernel choice so the env switches never need more.
 static size_t plan_ws(int nv, uint64_t C) {
-  const size_t a = make_dense_plan(nv, C, false).ws_bytes();
-  const size_t b = make_dense_plan(nv, C, true).ws_bytes();
-  return a > b ? a : b;
+  size_t m = 0;
+  for (int cfg = kPipeNone; cfg <= kPipeCfg11x3; ++cfg) {
+    const size_t b = make_dense_plan(nv, C, cfg).ws_bytes();
+    if (b > m) m = b;
+  }
+  return m;
 }
 
 // Workspace of the dense path = max over the launches of one call.
@@ -89,9 +99,9 @@ static size_t dense_ws(int n, int s, int world) {
 static ptdr_status launch_mode(int mode, const DenseArgs& a, const DensePlan& p, cudaStream_t st,
                                int* nl) {
   cudaError_t e;
-  if (p.v2) {
-    e = launch_dense_v2(mode, a, p, st, nl);
-    if (e != cudaSuccess) return cuda_fail(e, "dense v2 kernel launch");
+  if (p.pipe_cfg != kPipeNone) {
+    e = launch_dense_pipe(mode, a, p, st, nl);
+    if (e != cudaSuccess) return cuda_fail(e, "dense pipeline kernel launch");
     return PTDR_OK;
   }
   switch (mode) {

@@ -1,0 +1,480 @@
+// dense_pipe.cu -- warp-specialised TMA pipeline for the dense path (two-phase, nv >= 11).
+//
+// Same math as dense_impl.cuh (phase A: XOR-transpose gather + WHT over the low R index
+// bits into the scratch; phase B: WHT over the high M = nv - R bits + epilogue in q
+// order), organised for sm_100a:
+//   * one CTA per SM; warp 0 lane 0 = producer (tickets, inter-CTA dependency checks
+//     prefetched one tile ahead, TMA issue); NG consumer groups of GW warps take tiles
+//     round-robin from an NS-stage SMEM ring (mbarrier full/empty pipeline);
+//   * phase-A tiles (2^(R-4) row blocks of 16 x 16 complex128) arrive by 2-D TMA
+//     (cp.async.bulk.tensor), phase-B tiles (one contiguous 2^LT-element block of the
+//     B-tile-major scratch) by 1-D bulk copy;  HBM loads of later tiles overlap the
+//     arithmetic of earlier ones;
+//   * the XOR transpose happens in the SMEM read (conflict-free); the exchange between
+//     the two radix-16 register stages is done in place in the stage buffer;
+//   * consumed scratch lines are discarded from L2 (never written back to HBM);
+//   * completion counters are bumped per warp with release atomics (no CTA barrier).
+// Tile = 2^LT complex128 (LT = R + 4); a group has 2^(LT-4) threads holding 16 each.
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+#include <mutex>
+
+#include "dense_impl.cuh"
+#include "dense_plan.h"
+#include "internal.h"
+#include "sm100_ptx.cuh"
+
+namespace ptdr {
+
+struct TileMeta {
+  int valid, phase, tile, seq;
+  unsigned chunk, pad0, pad1, pad2;
+};
+
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// ---- 32-bit index arithmetic: n <= 16 so x, z < 2^16 and q < 2^32 ----------------------
+__device__ __forceinline__ uint32_t spread16(uint32_t v) {
+  v &= 0xFFFFu;
+  v = (v | (v << 8)) & 0x00FF00FFu;
+  v = (v | (v << 4)) & 0x0F0F0F0Fu;
+  v = (v | (v << 2)) & 0x33333333u;
+  v = (v | (v << 1)) & 0x55555555u;
+  return v;
+}
+__device__ __forceinline__ uint32_t q_offset32(uint32_t x, uint32_t z, int gshift) {
+  const uint32_t m = (gshift >= 32) ? 0xFFFFFFFFu : ((1u << gshift) - 1u);
+  const uint32_t top = (gshift >= 16) ? 0u : ((z >> gshift) << (2 * gshift));
+  return top | spread16((x ^ z) & m) | (spread16(z & m) << 1);
+}
+// q delta of setting z bit l (code_l = 2 z_l + (x_l ^ z_l); above gshift the z bit
+// indexes the rank-local block).
+__device__ __forceinline__ uint32_t q_delta32(uint32_t x, int l, int gshift) {
+  return (l < gshift) ? ((uint32_t)(3 - 2 * (int)((x >> l) & 1u)) << (2 * l)) : (1u << (l + gshift));
+}
+__device__ __forceinline__ uint32_t insert0_32(uint32_t v, int t) {
+  const uint32_t lo = v & ((1u << t) - 1u);
+  return ((v >> t) << (t + 1)) | lo;
+}
+
+// Epilogue of one thread-unit: q offset and phase of the unit's base (x, z) plus per-bit
+// deltas for the NB z bits that vary over the unit's registers (compile-time subsets).
+template <int NB, bool HALF>
+struct EpiUnit {
+  uint32_t q0, p0, Dt;
+  uint32_t D[NB];
+  uint32_t P[NB];
+  __device__ __forceinline__ void init(uint32_t x, uint32_t zu, int base_pos, int t, int gshift) {
+    const uint32_t zf = HALF ? insert0_32(zu, t) : zu;
+    q0 = q_offset32(x, zf, gshift);
+    p0 = __popc(x & zf);
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      int l = base_pos + b;
+      if (HALF) l += (l >= t) ? 1 : 0;
+      D[b] = q_delta32(x, l, gshift);
+      P[b] = (x >> l) & 1u;
+    }
+    Dt = HALF ? q_delta32(x, t, gshift) : 0u;
+  }
+};
+
+template <int MODE, int NB, int J>
+__device__ __forceinline__ void emit_reg(const DenseArgs& a, const EpiUnit<NB, (MODE >= 3)>& e,
+                                         double2 w) {
+  uint32_t q = e.q0, p = e.p0;
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    if (J & (1 << b)) {
+      q += e.D[b];
+      p += e.P[b];
+    }
+  }
+  if constexpr (MODE == MODE_GENERAL) {
+    const double2 c = rot_ipow(w, (int)p);
+    st_stream(a.out + q, make_double2(c.x * a.scale, c.y * a.scale));
+  } else {
+    // half-length modes: alpha = 2^{1-n} {Re, -Im, -Re, Im}[popcount(x&z) mod 4] (real)
+    const uint32_t p0 = p & 3u, p1 = (p + 1u) & 3u;
+    const double s = 2.0 * a.scale;
+    const double v0 = (p0 == 0) ? w.x : (p0 == 1) ? -w.y : (p0 == 2) ? -w.x : w.y;
+    const double v1 = (p1 == 0) ? w.x : (p1 == 1) ? -w.y : (p1 == 2) ? -w.x : w.y;
+    st_stream(a.out + q, make_double2(v0 * s, 0.0));
+    st_stream(a.out + (q + e.Dt), make_double2(v1 * s, 0.0));
+  }
+}
+
+template <int MODE, int NB, int J = 0>
+__device__ __forceinline__ void emit_all(const DenseArgs& a, const EpiUnit<NB, (MODE >= 3)>& e,
+                                         const double2* w) {
+  if constexpr (J < (1 << NB)) {
+    emit_reg<MODE, NB, J>(a, e, w[J]);
+    emit_all<MODE, NB, J + 1>(a, e, w);
+  }
+}
+
+// Ticket order of dense_impl.cuh's decode_ticket, 32-bit, NA = NB = 2^M.
+__device__ __forceinline__ void decode_ticket32(uint32_t t, int M, uint32_t C, uint32_t L, int& phase,
+                                                uint32_t& chunk, uint32_t& tile) {
+  const uint32_t NA = 1u << M;
+  const uint32_t lp1 = (L + 1u < C) ? L + 1u : C;
+  const uint32_t pro = lp1 << M;
+  if (t < pro) {
+    phase = 0; chunk = t >> M; tile = t & (NA - 1u);
+    return;
+  }
+  t -= pro;
+  const uint32_t steady = C > L + 1u ? C - L - 1u : 0u;
+  if (t < (steady << (M + 1))) {
+    const uint32_t c = t >> (M + 1), o = t & (2u * NA - 1u);
+    if (o < NA) { phase = 1; chunk = c; tile = o; }
+    else { phase = 0; chunk = c + L + 1u; tile = o - NA; }
+    return;
+  }
+  t -= steady << (M + 1);
+  phase = 1; chunk = steady + (t >> M); tile = t & (NA - 1u);
+}
+
+// Producer-side view of one claimed ticket.
+struct Claim {
+  uint32_t tk, chunk, tile, dep_target;
+  int phase;
+  const unsigned* dep;  // nullptr: no dependency
+  unsigned dep_val;
+};
+
+template <int LT, int GW, int NG, int NS>
+struct PipeCfg {
+  static constexpr int TE = 1 << LT;          // tile elements
+  static constexpr int TB = TE * 16;          // tile bytes
+  static constexpr int R = LT - 4;            // phase-A index bits
+  static constexpr int GT = GW * 32;          // threads per group (= TE / 16)
+  static constexpr int THREADS = 32 * (1 + NG * GW);
+  static constexpr int SMEM = NS * TB + 1024;
+  static_assert(GT * 16 == TE, "16 elements per consumer thread");
+};
+
+// Scratch layout (per chunk slot): B-tile-major Y[tileB][ih][f], 2^LT elements per phase-B
+// tile, so a phase-B tile is one contiguous bulk copy.  Fiber phi = tileB * FB + f encodes
+// (u, zl): bits [0,1]=u0,u1 [2,3]=zl0,zl1 [4,5]=u2,u3 [6..]=zl2.. (phi_u / phi_zl).
+template <int LT, int GW, int NG, int NS, int M, int MODE>
+__global__ void __launch_bounds__(PipeCfg<LT, GW, NG, NS>::THREADS, 1)
+    dense_pipe_kernel(const __grid_constant__ CUtensorMap tmap, DenseArgs a) {
+  using Cfg = PipeCfg<LT, GW, NG, NS>;
+  constexpr int R = Cfg::R, TE = Cfg::TE, GT = Cfg::GT;
+  constexpr bool HALF = (MODE == MODE_HERM_HALF || MODE == MODE_SYM_HALF);
+  constexpr int FB = TE >> M;  // phase-B fibers per tile
+  constexpr int LFB = LT - M;
+  static_assert(M >= 4 && M <= 8 && LFB <= 8, "phase-B fibre length 2^4..2^8");
+  extern __shared__ __align__(1024) unsigned char smem[];
+  double2* stage0 = reinterpret_cast<double2*>(smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * Cfg::TB);
+  uint64_t* empty = full + NS;
+  TileMeta* meta = reinterpret_cast<TileMeta*>(empty + NS);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t C = (uint32_t)a.nchunks;
+  unsigned* ticket = a.ctr;
+  unsigned* doneA = a.ctr + 1;
+  unsigned* doneB = a.ctr + 1 + C;
+  const uint32_t nslot = (uint32_t)a.nslot;
+  const unsigned per_tile = (unsigned)GW;  // per-warp completion signals per tile
+  const unsigned done_target = (1u << M) * per_tile;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], GW);
+      meta[s].seq = -1;
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  // ------------------------------------------------------------------ producer
+  if (warp == 0) {
+    if (lane == 0) {
+      prefetch_tmap(&tmap);
+      const uint64_t pol = policy_evict_first();
+      const uint32_t total = C << (M + 1);
+      auto claim = [&](uint32_t tk) {
+        Claim c;
+        c.tk = tk;
+        c.dep = nullptr;
+        c.dep_val = 0;
+        c.dep_target = done_target;
+        c.phase = 0; c.chunk = 0; c.tile = 0;
+        if (tk < total) {
+          decode_ticket32(tk, M, C, (uint32_t)a.L, c.phase, c.chunk, c.tile);
+          if (c.phase == 1) c.dep = &doneA[c.chunk];
+          else if (c.chunk >= nslot) c.dep = &doneB[c.chunk - nslot];
+          if (c.dep) c.dep_val = ld_acquire(c.dep);  // issued early; consumed one tile later
+        }
+        return c;
+      };
+      // Two tickets in hand: the current one and the next (already decoded, dependency
+      // counter already requested), plus the atomic for the one after that in flight.
+      Claim cur = claim(atomicAdd(ticket, 1u));
+      uint32_t tk_next = atomicAdd(ticket, 1u);
+      Claim nxt;
+      bool have_nxt = false;
+      int ends = 0;
+      for (int k = 0;; ++k) {
+        const int s = k % NS;
+        if (k >= NS) mbar_wait(&empty[s], (uint32_t)((k / NS) - 1) & 1u);
+        if (!have_nxt && cur.tk < total) {
+          nxt = claim(tk_next);
+          have_nxt = true;
+          tk_next = (nxt.tk < total) ? atomicAdd(ticket, 1u) : total;
+        }
+        if (cur.tk >= total) {
+          // one invalid tile per group ends the consumers
+          meta[s].valid = 0;
+          meta[s].seq = k;
+          mbar_arrive(&full[s]);
+          if (++ends == NG) break;
+          continue;
+        }
+        if (cur.dep) {
+          unsigned v = cur.dep_val;
+          while (v < cur.dep_target) {
+            __nanosleep(64);
+            v = ld_acquire(cur.dep);
+          }
+        }
+        double2* dst = stage0 + (size_t)s * TE;
+        meta[s].valid = 1;
+        meta[s].phase = cur.phase;
+        meta[s].tile = (int)cur.tile;
+        meta[s].chunk = cur.chunk;
+        meta[s].seq = k;
+        if (cur.phase == 0) {
+          mbar_arrive_expect_tx(&full[s], (uint32_t)Cfg::TB);
+          const u64 x0 = a.x_base + 16ull * cur.chunk;
+          const int t = HALF ? 63 - __clzll(x0) : 0;
+#pragma unroll
+          for (int rb = 0; rb < (1 << (R - 4)); ++rb) {
+            const u64 iv0 = ((u64)cur.tile << R) + (u64)rb * 16;
+            const u64 row0 = HALF ? insert0(iv0, t) : iv0;
+            const u64 col0 = ((row0 ^ x0) & a.colmask) & ~15ull;
+            tma_load_2d(dst + rb * 256, &tmap, (int)(col0 * 2), (int)row0, &full[s], pol);
+          }
+        } else {
+          // scratch written by other CTAs' generic stores, read by the async proxy
+          fence_proxy_async_global();
+          mbar_arrive_expect_tx(&full[s], (uint32_t)Cfg::TB);
+          const double2* src = a.scratch + (size_t)(cur.chunk % nslot) * a.slot_elems +
+                               ((size_t)cur.tile << LT);
+          bulk_load(dst, src, (uint32_t)Cfg::TB, &full[s], pol);
+        }
+        cur = nxt;
+        have_nxt = false;
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------ consumers
+  const int g = (warp - 1) / GW;
+  const int gtid = threadIdx.x - 32 - g * GT;
+  const int bar_id = 1 + g;
+  for (int k = g;; k += NG) {
+    const int s = k % NS;
+    // stages are shared round-robin by the groups, so a parity wait alone could match an
+    // older phase: first wait until the producer has published tile k in this stage
+    while (*reinterpret_cast<volatile int*>(&meta[s].seq) != k) __nanosleep(20);
+    mbar_wait(&full[s], (uint32_t)(k / NS) & 1u);
+    const TileMeta m = meta[s];
+    if (!m.valid) break;
+    double2* S = stage0 + (size_t)s * TE;
+    const uint32_t chunk = m.chunk;
+    double2* Y = a.scratch + (size_t)(chunk % nslot) * a.slot_elems;
+    double2 v[16];
+    if (m.phase == 0) {
+      // ---- phase A: v_x[i] for x = x0+u, i = tile*2^R + jh*16 + kk (XOR transpose in SMEM)
+      {
+        const int u = gtid & 15, jh = gtid >> 4;
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) {
+          v[kk] = S[(jh * 16 + kk) * 16 + (kk ^ u)];
+          if (MODE == MODE_SYM_HALF) v[kk].y = 0.0;
+        }
+        wht_regs<4>(v);
+        __syncwarp();
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) S[(jh * 16 + kk) * 16 + u] = v[kk];
+      }
+      named_bar_sync(bar_id, GT);
+      constexpr int R2 = R - 4;
+      constexpr int UA = 256 / GT;  // (u, jl) units per thread, each 2^R2 registers
+#pragma unroll
+      for (int p = 0; p < UA; ++p) {
+        const int uu = gtid + GT * p;
+        const int u = uu & 15, jl = uu >> 4;
+#pragma unroll
+        for (int j = 0; j < (1 << R2); ++j) v[p * (1 << R2) + j] = S[(j * 16 + jl) * 16 + u];
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      const uint64_t pol_last = policy_evict_last();
+#pragma unroll
+      for (int p = 0; p < UA; ++p) {
+        const int uu = gtid + GT * p;
+        const int u = uu & 15, jl = uu >> 4;
+        wht_regs<R2>(&v[p * (1 << R2)]);
+        // element (u, ih = tile, zl = j*16 + jl) -> Y[tileB][ih][f]
+        const uint32_t phi_lo =
+            (uint32_t)((u & 3) | ((jl & 3) << 2) | ((u >> 2) << 4) | ((jl >> 2) << 6));
+        double2* base = Y + (((phi_lo >> LFB) << LT) | ((uint32_t)m.tile << LFB) | (phi_lo & (FB - 1)));
+#pragma unroll
+        for (int j = 0; j < (1 << R2); ++j)
+          st_global_hint(base + ((size_t)j << (8 - LFB + LT)), v[p * (1 << R2) + j], pol_last);
+      }
+      __syncwarp();
+      if (lane == 0) red_release_add(&doneA[chunk], 1u);
+    } else {
+      // ---- phase B: SMEM holds Y[tileB][ih][f] = [j][f]; WHT over j for FB fibers
+      const u64 x0 = a.x_base + 16ull * chunk;
+      const int t = HALF ? 63 - __clzll(x0) : 0;
+      const int f = gtid % FB, jh = gtid / FB;
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) v[kk] = S[(jh * 16 + kk) * FB + f];
+      if (a.discard) {
+        // this tile's scratch is dead once in SMEM: drop it from L2 without write-back
+        // (the next writer of the slot waits for doneB of this chunk)
+        char* yb = reinterpret_cast<char*>(Y + ((size_t)m.tile << LT));
+#pragma unroll
+        for (int d = 0; d < Cfg::TB / 128 / GT; ++d) discard_l2(yb + ((size_t)(gtid + GT * d) << 7));
+      }
+      wht_regs<4>(v);
+      if constexpr (M == 4) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        const uint32_t phi = (uint32_t)m.tile * FB + (uint32_t)f;
+        EpiUnit<4, HALF> e;
+        e.init((uint32_t)x0 + (uint32_t)phi_u(phi), (uint32_t)phi_zl(phi), R, t, a.gshift);
+        emit_all<MODE, 4>(a, e, v);
+      } else {
+        constexpr int R2 = M - 4;
+        constexpr int UB = (FB * 16) / GT;  // (f, jl) units per thread, 2^R2 registers each
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) S[(jh * 16 + kk) * FB + f] = v[kk];
+        named_bar_sync(bar_id, GT);
+#pragma unroll
+        for (int p = 0; p < UB; ++p) {
+          const int uu = gtid + GT * p;
+          const int f2 = uu % FB, jl = uu / FB;
+#pragma unroll
+          for (int j = 0; j < (1 << R2); ++j) v[p * (1 << R2) + j] = S[(j * 16 + jl) * FB + f2];
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+#pragma unroll
+        for (int p = 0; p < UB; ++p) {
+          const int uu = gtid + GT * p;
+          const int f2 = uu % FB, jl = uu / FB;
+          const uint32_t phi = (uint32_t)m.tile * FB + (uint32_t)f2;
+          wht_regs<R2>(&v[p * (1 << R2)]);
+          EpiUnit<R2, HALF> e;
+          e.init((uint32_t)x0 + (uint32_t)phi_u(phi), ((uint32_t)jl << R) | (uint32_t)phi_zl(phi),
+                 R + 4, t, a.gshift);
+          emit_all<MODE, R2>(a, e, &v[p * (1 << R2)]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) red_release_add(&doneB[chunk], 1u);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static std::once_flag once;
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  std::call_once(once, []() {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+template <int LT, int GW, int NG, int NS, int M, int MODE>
+static cudaError_t launch_pipe_impl(const CUtensorMap& map, const DenseArgs& a, cudaStream_t st) {
+  using Cfg = PipeCfg<LT, GW, NG, NS>;
+  constexpr auto kern = dense_pipe_kernel<LT, GW, NG, NS, M, MODE>;
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [&]() {
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+  });
+  if (err != cudaSuccess) return err;
+  kern<<<device_sm_count(), Cfg::THREADS, Cfg::SMEM, st>>>(map, a);
+  return cudaGetLastError();
+}
+
+template <int LT, int GW, int NG, int NS, int MODE>
+static cudaError_t launch_pipe_m(const CUtensorMap& map, const DenseArgs& a, int M, cudaStream_t st) {
+  switch (M) {
+    case 4: return launch_pipe_impl<LT, GW, NG, NS, 4, MODE>(map, a, st);
+    case 5: return launch_pipe_impl<LT, GW, NG, NS, 5, MODE>(map, a, st);
+    case 6: return launch_pipe_impl<LT, GW, NG, NS, 6, MODE>(map, a, st);
+    case 7: return launch_pipe_impl<LT, GW, NG, NS, 7, MODE>(map, a, st);
+    case 8: return launch_pipe_impl<LT, GW, NG, NS, 8, MODE>(map, a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int LT, int GW, int NG, int NS>
+static cudaError_t launch_pipe_cfg(int mode, const CUtensorMap& map, const DenseArgs& a, int M,
+                                   cudaStream_t st) {
+  switch (mode) {
+    case MODE_GENERAL: return launch_pipe_m<LT, GW, NG, NS, MODE_GENERAL>(map, a, M, st);
+    case MODE_HERM_HALF: return launch_pipe_m<LT, GW, NG, NS, MODE_HERM_HALF>(map, a, M, st);
+    case MODE_SYM_HALF: return launch_pipe_m<LT, GW, NG, NS, MODE_SYM_HALF>(map, a, M, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_dense_pipe(int mode, const DenseArgs& a_in, const DensePlan& p, cudaStream_t st,
+                              int* nlaunch) {
+  if (p.kind != 2 || p.pipe_cfg == 0) return cudaErrorInvalidValue;
+  DenseArgs a = a_in;
+  a.L = p.L;
+  a.nslot = p.nslot;
+  a.slot_elems = p.slot_elems;
+  PFN_cuTensorMapEncodeTiled_v12000 enc = encode_fn();
+  if (!enc) return cudaErrorNotSupported;
+  CUtensorMap map;
+  const cuuint64_t ncols = a.colmask + 1, nrows = 1ull << a.n;
+  cuuint64_t gdim[2] = {2 * ncols, nrows};
+  cuuint64_t gstride[1] = {a.ld * 16};
+  cuuint32_t box[2] = {32, 16};  // 16 complex128 x 16 rows
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double2*>(a.A), gdim, gstride,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  {
+    const char* nd = getenv("PTDR_NO_DISCARD");
+    a.discard = (nd && nd[0] == '1') ? 0 : 1;
+  }
+  cudaError_t e = cudaMemsetAsync(a.ctr, 0, p.ctr_bytes, st);
+  if (e != cudaSuccess) return e;
+  *nlaunch += 1;
+  switch (p.pipe_cfg) {
+    case kPipeCfg12: return launch_pipe_cfg<12, 8, 2, 3>(mode, map, a, p.M, st);
+    case kPipeCfg11x4: return launch_pipe_cfg<11, 4, 4, 6>(mode, map, a, p.M, st);
+    case kPipeCfg11x3: return launch_pipe_cfg<11, 4, 3, 6>(mode, map, a, p.M, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace ptdr

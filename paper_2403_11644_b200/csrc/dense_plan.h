@@ -22,7 +22,7 @@ struct DensePlan {
   int NA = 0, NB = 0;  // tiles per chunk in phase A / B (two-phase)
   int L = 0;           // look-ahead (chunks of phase A issued ahead of phase B)
   int nslot = 0;       // scratch ring slots
-  bool v2 = false;     // warp-specialised TMA kernel (dense_v2.cu) instead of dense_impl.cuh
+  int pipe_cfg = 0;    // 0: dense_impl.cuh kernels; else a dense_pipe.cu configuration
   uint64_t nchunks = 0;
   uint64_t slot_elems = 0;  // complex128 elements per scratch slot
   size_t ctr_bytes = 0;
@@ -30,40 +30,57 @@ struct DensePlan {
   size_t ws_bytes() const { return ctr_bytes + scratch_bytes; }
 };
 
-// Tiles resident at once on a B200 (fixes L deterministically, independent of the device):
-// v1 = 148 SMs x 2 CTAs; v2 = 148 SMs x 3 pipeline stages.
-constexpr int kNominalResidentCtas = 296;
-constexpr int kNominalResidentV2 = 592;  // 148 SMs x (3 stages + 1 ticket claimed ahead)
-constexpr uint64_t kV2ScratchBudget = 2ull << 30;  // bytes of scratch slots for the v2 kernel
+// dense_pipe.cu configurations: tile 2^LT elements, GW warps per group, NG groups, NS stages.
+enum { kPipeNone = 0, kPipeCfg12 = 1 /* 12,8,2,3 */, kPipeCfg11x4 = 2 /* 11,4,4,6 */,
+       kPipeCfg11x3 = 3 /* 11,4,3,6 */ };
+inline int pipe_lt(int cfg) { return cfg == kPipeCfg12 ? 12 : 11; }
+inline int pipe_stages(int cfg) { return cfg == kPipeCfg12 ? 3 : 6; }
 
-// v2_ok: the caller's MODE can run on the TMA kernel (GENERAL or half-length modes).
-inline DensePlan make_dense_plan(int nv, uint64_t nchunks, bool v2_ok = false) {
+// Tiles resident at once on a B200 (fixes L deterministically, independent of the device).
+constexpr int kNominalSMs = 148;
+constexpr int kNominalResidentCtas = 296;          // v1: 148 SMs x 2 CTAs
+constexpr uint64_t kPipeScratchBudget = 2ull << 30;  // bytes of scratch slots for the pipeline
+
+// pipe_cfg: requested dense_pipe.cu configuration (0 = v1 kernels).  Falls back to v1 when
+// the phase split does not fit the configuration (M = nv - (LT-4) must be in [4, 8]).
+inline DensePlan make_dense_plan(int nv, uint64_t nchunks, int pipe_cfg = kPipeNone) {
   DensePlan p;
   p.nv = nv;
   p.nchunks = nchunks;
   if (nv <= 5) { p.kind = 0; return p; }
   if (nv <= 7) { p.kind = 1; p.R = nv; p.M = 0; return p; }
   p.kind = 2;
-  if (nv <= 11) { p.R = nv - 4; p.M = 4; }
-  else { p.R = 8; p.M = nv - 8; }
-  p.NA = 1 << (nv - 8);
-  p.NB = 1 << (nv - 8);
-  p.v2 = v2_ok && p.R == 8;
-  const int resident = p.v2 ? kNominalResidentV2 : kNominalResidentCtas;
-  int period = p.NA + p.NB;
+  if (pipe_cfg != kPipeNone) {
+    const int R = pipe_lt(pipe_cfg) - 4;
+    if (nv - R < 4 || nv - R > 8) pipe_cfg = kPipeNone;
+  }
+  p.pipe_cfg = pipe_cfg;
+  int resident;
+  if (pipe_cfg != kPipeNone) {
+    p.R = pipe_lt(pipe_cfg) - 4;
+    p.M = nv - p.R;
+    resident = kNominalSMs * (pipe_stages(pipe_cfg) + 2);
+  } else {
+    if (nv <= 11) { p.R = nv - 4; p.M = 4; }
+    else { p.R = 8; p.M = nv - 8; }
+    resident = kNominalResidentCtas;
+  }
+  p.NA = 1 << p.M;
+  p.NB = 1 << p.M;
+  const int period = p.NA + p.NB;
   int L = (3 * resident + 2 * period - 1) / (2 * period);  // ceil(1.5*resident/period)
   if (L < 1) L = 1;
   if (L > 64) L = 64;
   p.L = L;
   // Scratch slots.  A phase-A tile of chunk c waits until phase B of chunk c - nslot has
   // drained the slot; with ~`resident` tickets in flight that wait is rare only if
-  // nslot >= L + 1 + resident/period.  v2 takes many more slots (capped by a byte budget):
-  // consumed slots are discarded from L2, so only the live ~L chunks occupy L2 and the
-  // extra slots cost HBM capacity, not bandwidth.
+  // nslot >= L + 1 + resident/period.  The pipeline takes many more slots (capped by a
+  // byte budget): consumed slots are discarded from L2, so only the live ~L chunks occupy
+  // L2 and the extra slots cost HBM capacity, not bandwidth.
   uint64_t ns = (uint64_t)L + 2;
-  if (p.v2) {
+  if (pipe_cfg != kPipeNone) {
     const uint64_t slot_bytes = ((uint64_t)16 << nv) * 16;
-    uint64_t budget = kV2ScratchBudget / slot_bytes;
+    uint64_t budget = kPipeScratchBudget / slot_bytes;
     const uint64_t need = 2ull * (uint64_t)L + 2ull + (uint64_t)(resident / period);
     if (budget < need) budget = need;
     ns = budget;

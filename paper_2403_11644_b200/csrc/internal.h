@@ -18,8 +18,8 @@ cudaError_t launch_dense_mode2(const DenseArgs& a, const DensePlan& p, cudaStrea
 cudaError_t launch_dense_mode3(const DenseArgs& a, const DensePlan& p, cudaStream_t st, int* nl);
 cudaError_t launch_dense_mode4(const DenseArgs& a, const DensePlan& p, cudaStream_t st, int* nl);
 
-cudaError_t launch_dense_v2(int mode, const DenseArgs& a, const DensePlan& p, cudaStream_t st,
-                            int* nl);
+cudaError_t launch_dense_pipe(int mode, const DenseArgs& a, const DensePlan& p, cudaStream_t st,
+                              int* nl);
 
 // band paths (band.cu)
 size_t band_workspace_bytes(int n, int structure);

@@ -152,8 +152,9 @@ struct PipeCfg {
   static constexpr int TB = TE * 16;          // tile bytes
   static constexpr int R = LT - 4;            // phase-A index bits
   static constexpr int GT = GW * 32;          // threads per group (= TE / 16)
-  static constexpr int THREADS = 32 * (1 + NG * GW);
-  static constexpr int SMEM = NS * TB + 1024;
+  static constexpr int SIGD = 4;               // completion-signal slots per group
+  static constexpr int THREADS = 32 * (2 + NG * GW);  // warp 0 producer, warp 1 signaler
+  static constexpr int SMEM = NS * TB + 2048;
   static_assert(GT * 16 == TE, "16 elements per consumer thread");
 };
 
@@ -174,20 +175,27 @@ __global__ void __launch_bounds__(PipeCfg<LT, GW, NG, NS>::THREADS, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * Cfg::TB);
   uint64_t* empty = full + NS;
   TileMeta* meta = reinterpret_cast<TileMeta*>(empty + NS);
+  constexpr int SIGD = Cfg::SIGD;
+  uint64_t* sigbar = reinterpret_cast<uint64_t*>(meta + NS);  // [NG][SIGD], count GW
+  uint64_t* sigfree = sigbar + NG * SIGD;                       // [NG][SIGD], count 1
+  unsigned** sigptr = reinterpret_cast<unsigned**>(sigfree + NG * SIGD);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t C = (uint32_t)a.nchunks;
   unsigned* ticket = a.ctr;
   unsigned* doneA = a.ctr + 1;
   unsigned* doneB = a.ctr + 1 + C;
   const uint32_t nslot = (uint32_t)a.nslot;
-  const unsigned per_tile = (unsigned)GW;  // per-warp completion signals per tile
-  const unsigned done_target = (1u << M) * per_tile;
+  const unsigned done_target = 1u << M;  // one completion signal per tile
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], GW);
       meta[s].seq = -1;
+    }
+    for (int i = 0; i < NG * SIGD; ++i) {
+      mbar_init(&sigbar[i], GW);
+      mbar_init(&sigfree[i], 1);
     }
     fence_mbar_init();
   }
@@ -276,18 +284,69 @@ __global__ void __launch_bounds__(PipeCfg<LT, GW, NG, NS>::THREADS, 1)
     return;
   }
 
+  // ------------------------------------------------------------------ signaler
+  // Consumers arrive (per warp, non-blocking) on sigbar after their global stores; this
+  // thread turns each completed tile into one release increment of the tile's counter
+  // (cumulative over the stores observed through the mbarrier, as a CTA barrier followed
+  // by one thread's release would be), so no consumer warp ever waits on a memory fence.
+  if (warp == 1) {
+    if (lane == 0) {
+      int jg[NG];
+#pragma unroll
+      for (int gg = 0; gg < NG; ++gg) jg[gg] = 0;
+      int ended = 0;
+      while (ended < NG) {
+        bool progress = false;
+#pragma unroll
+        for (int gg = 0; gg < NG; ++gg) {
+          if (jg[gg] < 0) continue;
+          const int d = jg[gg] % SIGD;
+          if (mbar_try_wait(&sigbar[gg * SIGD + d], (uint32_t)(jg[gg] / SIGD) & 1u)) {
+            unsigned* p = sigptr[gg * SIGD + d];
+            if (p == nullptr) {
+              jg[gg] = -1;
+              ++ended;
+            } else {
+              red_release_add(p, 1u);
+              ++jg[gg];
+            }
+            mbar_arrive(&sigfree[gg * SIGD + d]);
+            progress = true;
+          }
+        }
+        if (!progress) __nanosleep(32);
+      }
+    }
+    return;
+  }
+
   // ------------------------------------------------------------------ consumers
-  const int g = (warp - 1) / GW;
-  const int gtid = threadIdx.x - 32 - g * GT;
+  const int g = (warp - 2) / GW;
+  const int gtid = threadIdx.x - 64 - g * GT;
+  const int wig = gtid >> 5;  // warp index within the group
+  // per-warp completion signal of the group's j-th tile (see the signaler)
+  auto signal = [&](int j, unsigned* counter) {
+    __syncwarp();
+    if (lane == 0) {
+      const int d = j % SIGD;
+      if (j >= SIGD) mbar_wait(&sigfree[g * SIGD + d], (uint32_t)((j / SIGD) - 1) & 1u);
+      if (wig == 0) sigptr[g * SIGD + d] = counter;
+      mbar_arrive(&sigbar[g * SIGD + d]);
+    }
+  };
   const int bar_id = 1 + g;
-  for (int k = g;; k += NG) {
+  int j = 0;
+  for (int k = g;; k += NG, ++j) {
     const int s = k % NS;
     // stages are shared round-robin by the groups, so a parity wait alone could match an
     // older phase: first wait until the producer has published tile k in this stage
     while (*reinterpret_cast<volatile int*>(&meta[s].seq) != k) __nanosleep(20);
     mbar_wait(&full[s], (uint32_t)(k / NS) & 1u);
     const TileMeta m = meta[s];
-    if (!m.valid) break;
+    if (!m.valid) {
+      signal(j, nullptr);  // end marker for the signaler
+      break;
+    }
     double2* S = stage0 + (size_t)s * TE;
     const uint32_t chunk = m.chunk;
     double2* Y = a.scratch + (size_t)(chunk % nslot) * a.slot_elems;
@@ -333,8 +392,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, GW, NG, NS>::THREADS, 1)
         for (int j = 0; j < (1 << R2); ++j)
           st_global_hint(base + ((size_t)j << (8 - LFB + LT)), v[p * (1 << R2) + j], pol_last);
       }
-      __syncwarp();
-      if (lane == 0) red_release_add(&doneA[chunk], 1u);
+      signal(j, &doneA[chunk]);
     } else {
       // ---- phase B: SMEM holds Y[tileB][ih][f] = [j][f]; WHT over j for FB fibers
       const u64 x0 = a.x_base + 16ull * chunk;
@@ -386,8 +444,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, GW, NG, NS>::THREADS, 1)
           emit_all<MODE, R2>(a, e, &v[p * (1 << R2)]);
         }
       }
-      __syncwarp();
-      if (lane == 0) red_release_add(&doneB[chunk], 1u);
+      signal(j, &doneB[chunk]);
     }
   }
 }

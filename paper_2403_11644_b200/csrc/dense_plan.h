@@ -59,7 +59,7 @@ inline DensePlan make_dense_plan(int nv, uint64_t nchunks, int pipe_cfg = kPipeN
   if (pipe_cfg != kPipeNone) {
     p.R = pipe_lt(pipe_cfg) - 4;
     p.M = nv - p.R;
-    resident = kNominalSMs * (pipe_stages(pipe_cfg) + 2);
+    resident = kNominalSMs * pipe_stages(pipe_cfg);
   } else {
     if (nv <= 11) { p.R = nv - 4; p.M = 4; }
     else { p.R = 8; p.M = nv - 8; }

@@ -32,6 +32,16 @@ struct TileMeta {
   unsigned chunk, pad0, pad1, pad2;
 };
 
+// Relaxed GPU-scope load of a completion counter.  No L1 invalidation (an acquire load
+// would emit CCTL.IVALL and stall the producer for a full L2 round trip per tile).  The
+// data the producer then reads is fetched by the TMA from L2 (the point of coherence)
+// in an instruction control-dependent on this value, after fence.proxy.async.global.
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -218,7 +228,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, GW, NG, NS>::THREADS, 1)
           decode_ticket32(tk, M, C, (uint32_t)a.L, c.phase, c.chunk, c.tile);
           if (c.phase == 1) c.dep = &doneA[c.chunk];
           else if (c.chunk >= nslot) c.dep = &doneB[c.chunk - nslot];
-          if (c.dep) c.dep_val = ld_acquire(c.dep);  // issued early; consumed one tile later
+          if (c.dep) c.dep_val = ld_relaxed(c.dep);  // issued early; consumed one tile later
         }
         return c;
       };
@@ -249,7 +259,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, GW, NG, NS>::THREADS, 1)
           unsigned v = cur.dep_val;
           while (v < cur.dep_target) {
             __nanosleep(64);
-            v = ld_acquire(cur.dep);
+            v = ld_relaxed(cur.dep);
           }
         }
         double2* dst = stage0 + (size_t)s * TE;

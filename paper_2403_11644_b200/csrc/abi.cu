@@ -10,6 +10,7 @@
 #include <string>
 
 #include "../../include/ptdr.h"
+#include "../../include/ptdr_debug.h"
 #include "dense_impl.cuh"
 #include "dense_plan.h"
 #include "internal.h"
@@ -178,6 +179,8 @@ using namespace ptdr;
 extern "C" {
 
 int ptdr_version(void) { return 1; }
+
+int ptdr_debug_trace_copy(void* host, size_t bytes) { return debug_trace_copy(host, bytes); }
 
 int ptdr_max_n(int structure) {
   if (is_dense(structure)) return 16;

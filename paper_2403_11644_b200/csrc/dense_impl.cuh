@@ -37,7 +37,8 @@ struct DenseArgs {
   int gshift;          // n - log2(world)
   int L;
   int nslot;
-  int discard;         // v2: discard consumed scratch lines from L2 (no write-back)
+  int discard;         // pipeline: discard consumed scratch lines from L2 (no write-back)
+  unsigned long long* trace;  // pipeline debug timeline (nullptr unless PTDR_TRACE=1)
   double scale;        // 2^-n
 };
 

@@ -42,6 +42,13 @@ __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
   return v;
 }
 
+// Debug timeline (PTDR_TRACE=1): CTA 0 records clock64 stamps of its first kTraceTiles
+// tiles into a.trace[tile * 16 + field].
+constexpr int kTraceTiles = 512;
+__device__ __forceinline__ void trace_stamp(unsigned long long* tr, int k, int field) {
+  if (tr != nullptr && blockIdx.x == 0 && k < kTraceTiles) tr[k * 16 + field] = clock64();
+}
+
 __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -241,7 +248,9 @@ __global__ void __launch_bounds__(PipeCfg<LT, GW, NG, NS>::THREADS, 1)
       int ends = 0;
       for (int k = 0;; ++k) {
         const int s = k % NS;
+        trace_stamp(a.trace, k, 0);
         if (k >= NS) mbar_wait(&empty[s], (uint32_t)((k / NS) - 1) & 1u);
+        trace_stamp(a.trace, k, 1);
         if (!have_nxt && cur.tk < total) {
           nxt = claim(tk_next);
           have_nxt = true;
@@ -262,6 +271,8 @@ __global__ void __launch_bounds__(PipeCfg<LT, GW, NG, NS>::THREADS, 1)
             v = ld_relaxed(cur.dep);
           }
         }
+        trace_stamp(a.trace, k, 2);
+        if (a.trace && blockIdx.x == 0 && k < kTraceTiles) a.trace[k * 16 + 8] = cur.phase;
         double2* dst = stage0 + (size_t)s * TE;
         meta[s].valid = 1;
         meta[s].phase = cur.phase;
@@ -287,6 +298,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, GW, NG, NS>::THREADS, 1)
                                ((size_t)cur.tile << LT);
           bulk_load(dst, src, (uint32_t)Cfg::TB, &full[s], pol);
         }
+        trace_stamp(a.trace, k, 3);
         cur = nxt;
         have_nxt = false;
       }
@@ -350,8 +362,10 @@ __global__ void __launch_bounds__(PipeCfg<LT, GW, NG, NS>::THREADS, 1)
     const int s = k % NS;
     // stages are shared round-robin by the groups, so a parity wait alone could match an
     // older phase: first wait until the producer has published tile k in this stage
+    if (gtid == 0) trace_stamp(a.trace, k, 4);
     while (*reinterpret_cast<volatile int*>(&meta[s].seq) != k) __nanosleep(20);
     mbar_wait(&full[s], (uint32_t)(k / NS) & 1u);
+    if (gtid == 0) trace_stamp(a.trace, k, 5);
     const TileMeta m = meta[s];
     if (!m.valid) {
       signal(j, nullptr);  // end marker for the signaler
@@ -388,6 +402,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, GW, NG, NS>::THREADS, 1)
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+      if (gtid == 0) trace_stamp(a.trace, k, 6);
       const uint64_t pol_last = policy_evict_last();
 #pragma unroll
       for (int p = 0; p < UA; ++p) {
@@ -403,6 +418,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, GW, NG, NS>::THREADS, 1)
           st_global_hint(base + ((size_t)j << (8 - LFB + LT)), v[p * (1 << R2) + j], pol_last);
       }
       signal(j, &doneA[chunk]);
+      if (gtid == 0) trace_stamp(a.trace, k, 7);
     } else {
       // ---- phase B: SMEM holds Y[tileB][ih][f] = [j][f]; WHT over j for FB fibers
       const u64 x0 = a.x_base + 16ull * chunk;
@@ -442,6 +458,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, GW, NG, NS>::THREADS, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
+        if (gtid == 0) trace_stamp(a.trace, k, 6);
 #pragma unroll
         for (int p = 0; p < UB; ++p) {
           const int uu = gtid + GT * p;
@@ -455,11 +472,28 @@ __global__ void __launch_bounds__(PipeCfg<LT, GW, NG, NS>::THREADS, 1)
         }
       }
       signal(j, &doneB[chunk]);
+      if (gtid == 0) trace_stamp(a.trace, k, 7);
     }
   }
 }
 
 // ------------------------------------------------------------------ host side
+static unsigned long long* g_trace = nullptr;
+static unsigned long long* debug_trace_buffer() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("PTDR_TRACE");
+    on = (e && e[0] == '1') ? 1 : 0;
+    if (on && cudaMalloc(&g_trace, (size_t)kTraceTiles * 16 * 8) != cudaSuccess) g_trace = nullptr;
+  }
+  return g_trace;
+}
+int debug_trace_copy(void* host, size_t bytes) {
+  if (!g_trace) return -1;
+  const size_t n = bytes < (size_t)kTraceTiles * 16 * 8 ? bytes : (size_t)kTraceTiles * 16 * 8;
+  if (cudaDeviceSynchronize() != cudaSuccess) return -2;
+  return cudaMemcpy(host, g_trace, n, cudaMemcpyDeviceToHost) == cudaSuccess ? (int)n : -3;
+}
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static std::once_flag once;
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -535,6 +569,11 @@ cudaError_t launch_dense_pipe(int mode, const DenseArgs& a_in, const DensePlan& 
   }
   cudaError_t e = cudaMemsetAsync(a.ctr, 0, p.ctr_bytes, st);
   if (e != cudaSuccess) return e;
+  a.trace = debug_trace_buffer();
+  if (a.trace) {
+    e = cudaMemsetAsync(a.trace, 0, (size_t)kTraceTiles * 16 * 8, st);
+    if (e != cudaSuccess) return e;
+  }
   *nlaunch += 1;
   switch (p.pipe_cfg) {
     case kPipeCfg12: return launch_pipe_cfg<12, 8, 2, 3>(mode, map, a, p.M, st);

@@ -21,6 +21,8 @@ cudaError_t launch_dense_mode4(const DenseArgs& a, const DensePlan& p, cudaStrea
 cudaError_t launch_dense_pipe(int mode, const DenseArgs& a, const DensePlan& p, cudaStream_t st,
                               int* nl);
 
+int debug_trace_copy(void* host, size_t bytes);
+
 // band paths (band.cu)
 size_t band_workspace_bytes(int n, int structure);
 cudaError_t launch_band(const double2* A, double2* out, int n, int structure, void* ws,

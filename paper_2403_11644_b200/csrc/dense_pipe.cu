@@ -239,10 +239,17 @@ __global__ void __launch_bounds__(PipeCfg<LT, GW, NG, NS>::THREADS, 1)
         }
         return c;
       };
-      // Two tickets in hand: the current one and the next (already decoded, dependency
-      // counter already requested), plus the atomic for the one after that in flight.
-      Claim cur = claim(atomicAdd(ticket, 1u));
-      uint32_t tk_next = atomicAdd(ticket, 1u);
+      // Tickets are claimed three atomics ahead of their decode (the single ticket
+      // counter is contended; its round trip is ~1 us under load), and a decoded ticket's
+      // dependency counter is requested one tile before it is needed.  A claimed ticket
+      // is always processed, in claim order, so holding several is deadlock-free.
+      uint32_t q0 = atomicAdd(ticket, 1u);
+      uint32_t q1 = atomicAdd(ticket, 1u);
+      uint32_t q2 = atomicAdd(ticket, 1u);
+      Claim cur = claim(q0);
+      q0 = q1;
+      q1 = q2;
+      q2 = atomicAdd(ticket, 1u);
       Claim nxt;
       bool have_nxt = false;
       int ends = 0;
@@ -252,9 +259,11 @@ __global__ void __launch_bounds__(PipeCfg<LT, GW, NG, NS>::THREADS, 1)
         if (k >= NS) mbar_wait(&empty[s], (uint32_t)((k / NS) - 1) & 1u);
         trace_stamp(a.trace, k, 1);
         if (!have_nxt && cur.tk < total) {
-          nxt = claim(tk_next);
+          nxt = claim(q0);
           have_nxt = true;
-          tk_next = (nxt.tk < total) ? atomicAdd(ticket, 1u) : total;
+          q0 = q1;
+          q1 = q2;
+          q2 = (q1 < total) ? atomicAdd(ticket, 1u) : total;
         }
         if (cur.tk >= total) {
           // one invalid tile per group ends the consumers
@@ -281,14 +290,15 @@ __global__ void __launch_bounds__(PipeCfg<LT, GW, NG, NS>::THREADS, 1)
         meta[s].seq = k;
         if (cur.phase == 0) {
           mbar_arrive_expect_tx(&full[s], (uint32_t)Cfg::TB);
-          const u64 x0 = a.x_base + 16ull * cur.chunk;
-          const int t = HALF ? 63 - __clzll(x0) : 0;
+          const uint32_t x0 = (uint32_t)a.x_base + 16u * cur.chunk;
+          const int t = HALF ? 31 - __clz(x0) : 0;
+          const uint32_t cm = (uint32_t)a.colmask & ~15u;
 #pragma unroll
           for (int rb = 0; rb < (1 << (R - 4)); ++rb) {
-            const u64 iv0 = ((u64)cur.tile << R) + (u64)rb * 16;
-            const u64 row0 = HALF ? insert0(iv0, t) : iv0;
-            const u64 col0 = ((row0 ^ x0) & a.colmask) & ~15ull;
-            tma_load_2d(dst + rb * 256, &tmap, (int)(col0 * 2), (int)row0, &full[s], pol);
+            const uint32_t iv0 = (cur.tile << R) + (uint32_t)rb * 16u;
+            const uint32_t row0 = HALF ? insert0_32(iv0, t) : iv0;
+            const uint32_t col0 = (row0 ^ x0) & cm;
+            tma_load_2d(dst + rb * 256, &tmap, (int)(col0 * 2u), (int)row0, &full[s], pol);
           }
         } else {
           // scratch written by other CTAs' generic stores, read by the async proxy

@@ -155,14 +155,6 @@ __device__ __forceinline__ void decode_ticket32(uint32_t t, int M, uint32_t C, u
   phase = 1; chunk = steady + (t >> M); tile = t & (NA - 1u);
 }
 
-// Producer-side view of one claimed ticket.
-struct Claim {
-  uint32_t tk, chunk, tile, dep_target;
-  int phase;
-  const unsigned* dep;  // nullptr: no dependency
-  unsigned dep_val;
-};
-
 template <int LT, int GW, int NG, int NS>
 struct PipeCfg {
   static constexpr int TE = 1 << LT;          // tile elements
@@ -224,78 +216,62 @@ __global__ void __launch_bounds__(PipeCfg<LT, GW, NG, NS>::THREADS, 1)
       prefetch_tmap(&tmap);
       const uint64_t pol = policy_evict_first();
       const uint32_t total = C << (M + 1);
-      auto claim = [&](uint32_t tk) {
-        Claim c;
-        c.tk = tk;
-        c.dep = nullptr;
-        c.dep_val = 0;
-        c.dep_target = done_target;
-        c.phase = 0; c.chunk = 0; c.tile = 0;
+      // Decoded ticket: (tk, phase, chunk, tile) and its dependency counter, whose value is
+      // requested (dv) one tile before it is checked.
+      auto decode_into = [&](uint32_t tk, uint32_t& tkX, int& phX, uint32_t& chX, uint32_t& tlX,
+                             const unsigned*& depX, unsigned& dvX) {
+        tkX = tk;
+        phX = 0; chX = 0; tlX = 0;
+        depX = nullptr;
+        dvX = 0;
         if (tk < total) {
-          decode_ticket32(tk, M, C, (uint32_t)a.L, c.phase, c.chunk, c.tile);
-          if (c.phase == 1) c.dep = &doneA[c.chunk];
-          else if (c.chunk >= nslot) c.dep = &doneB[c.chunk - nslot];
-          if (c.dep) c.dep_val = ld_relaxed(c.dep);  // issued early; consumed one tile later
+          decode_ticket32(tk, M, C, (uint32_t)a.L, phX, chX, tlX);
+          if (phX == 1) depX = &doneA[chX];
+          else if (chX >= nslot) depX = &doneB[chX - nslot];
+          if (depX) dvX = ld_relaxed(depX);
         }
-        return c;
       };
-      // Tickets are claimed three atomics ahead of their decode (the single ticket
-      // counter is contended; its round trip is ~1 us under load), and a decoded ticket's
-      // dependency counter is requested one tile before it is needed.  A claimed ticket
-      // is always processed, in claim order, so holding several is deadlock-free.
-      uint32_t q0 = atomicAdd(ticket, 1u);
-      uint32_t q1 = atomicAdd(ticket, 1u);
-      uint32_t q2 = atomicAdd(ticket, 1u);
-      Claim cur = claim(q0);
-      q0 = q1;
-      q1 = q2;
-      q2 = atomicAdd(ticket, 1u);
-      Claim nxt;
-      bool have_nxt = false;
-      int ends = 0;
-      for (int k = 0;; ++k) {
+      int k = 0, ends = 0;
+      // Publish one tile (or an end marker) into stage k % NS.  Returns true when all
+      // groups have received their end marker.
+      auto process = [&](const uint32_t& tkX, const int& phX, const uint32_t& chX,
+                         const uint32_t& tlX, const unsigned* const& depX,
+                         const unsigned& dvX) -> bool {
         const int s = k % NS;
         trace_stamp(a.trace, k, 0);
         if (k >= NS) mbar_wait(&empty[s], (uint32_t)((k / NS) - 1) & 1u);
         trace_stamp(a.trace, k, 1);
-        if (!have_nxt && cur.tk < total) {
-          nxt = claim(q0);
-          have_nxt = true;
-          q0 = q1;
-          q1 = q2;
-          q2 = (q1 < total) ? atomicAdd(ticket, 1u) : total;
-        }
-        if (cur.tk >= total) {
+        if (tkX >= total) {
           // one invalid tile per group ends the consumers
           meta[s].valid = 0;
           meta[s].seq = k;
           mbar_arrive(&full[s]);
-          if (++ends == NG) break;
-          continue;
+          ++k;
+          return ++ends == NG;
         }
-        if (cur.dep) {
-          unsigned v = cur.dep_val;
-          while (v < cur.dep_target) {
+        if (depX) {
+          unsigned v = dvX;
+          while (v < done_target) {
             __nanosleep(64);
-            v = ld_relaxed(cur.dep);
+            v = ld_relaxed(depX);
           }
         }
         trace_stamp(a.trace, k, 2);
-        if (a.trace && blockIdx.x == 0 && k < kTraceTiles) a.trace[k * 16 + 8] = cur.phase;
+        if (a.trace && blockIdx.x == 0 && k < kTraceTiles) a.trace[k * 16 + 8] = phX;
         double2* dst = stage0 + (size_t)s * TE;
         meta[s].valid = 1;
-        meta[s].phase = cur.phase;
-        meta[s].tile = (int)cur.tile;
-        meta[s].chunk = cur.chunk;
+        meta[s].phase = phX;
+        meta[s].tile = (int)tlX;
+        meta[s].chunk = chX;
         meta[s].seq = k;
-        if (cur.phase == 0) {
+        if (phX == 0) {
           mbar_arrive_expect_tx(&full[s], (uint32_t)Cfg::TB);
-          const uint32_t x0 = (uint32_t)a.x_base + 16u * cur.chunk;
+          const uint32_t x0 = (uint32_t)a.x_base + 16u * chX;
           const int t = HALF ? 31 - __clz(x0) : 0;
           const uint32_t cm = (uint32_t)a.colmask & ~15u;
 #pragma unroll
           for (int rb = 0; rb < (1 << (R - 4)); ++rb) {
-            const uint32_t iv0 = (cur.tile << R) + (uint32_t)rb * 16u;
+            const uint32_t iv0 = (tlX << R) + (uint32_t)rb * 16u;
             const uint32_t row0 = HALF ? insert0_32(iv0, t) : iv0;
             const uint32_t col0 = (row0 ^ x0) & cm;
             tma_load_2d(dst + rb * 256, &tmap, (int)(col0 * 2u), (int)row0, &full[s], pol);
@@ -304,13 +280,31 @@ __global__ void __launch_bounds__(PipeCfg<LT, GW, NG, NS>::THREADS, 1)
           // scratch written by other CTAs' generic stores, read by the async proxy
           fence_proxy_async_global();
           mbar_arrive_expect_tx(&full[s], (uint32_t)Cfg::TB);
-          const double2* src = a.scratch + (size_t)(cur.chunk % nslot) * a.slot_elems +
-                               ((size_t)cur.tile << LT);
+          const double2* src = a.scratch + (size_t)(chX % nslot) * a.slot_elems + ((size_t)tlX << LT);
           bulk_load(dst, src, (uint32_t)Cfg::TB, &full[s], pol);
         }
         trace_stamp(a.trace, k, 3);
-        cur = nxt;
-        have_nxt = false;
+        ++k;
+        return false;
+      };
+      // Tickets come in pairs (one atomic per two tiles, one pair ahead), and the two
+      // decoded tickets live in fixed register sets P and Q that alternate: no register
+      // holding an in-flight load result is ever copied (a copy would stall on it).
+      // A claimed ticket is always processed, in claim order, so this is deadlock-free.
+      uint32_t tkP, chP, tlP, tkQ, chQ, tlQ;
+      int phP, phQ;
+      const unsigned *depP, *depQ;
+      unsigned dvP, dvQ;
+      const uint32_t b0 = atomicAdd(ticket, 2u);
+      decode_into(b0, tkP, phP, chP, tlP, depP, dvP);
+      decode_into(b0 + 1, tkQ, phQ, chQ, tlQ, depQ, dvQ);
+      uint32_t nb = (b0 + 1 < total) ? atomicAdd(ticket, 2u) : total;
+      for (;;) {
+        if (process(tkP, phP, chP, tlP, depP, dvP)) break;
+        decode_into(nb, tkP, phP, chP, tlP, depP, dvP);
+        if (process(tkQ, phQ, chQ, tlQ, depQ, dvQ)) break;
+        decode_into(nb + 1, tkQ, phQ, chQ, tlQ, depQ, dvQ);
+        nb = (nb + 1 < total) ? atomicAdd(ticket, 2u) : total;
       }
     }
     return;

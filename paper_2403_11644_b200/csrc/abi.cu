@@ -51,50 +51,58 @@ static bool valid_n(int n, int s) {
   return false;
 }
 
-static uint64_t dense_chunks(int n) { return n >= 4 ? (1ull << n) / 16 : 1ull; }
 
 // Dense-path kernel selection.  PTDR_DENSE_V1=1 forces the dense_impl.cuh kernels;
-// PTDR_PIPE_CFG=1|2|3 picks a dense_pipe.cu configuration (see dense_plan.h).
+// PTDR_PIPE_CFG=<k> picks a dense_pipe configuration (see dense_plan.h).
 static int pipe_choice() {
   static int v = -1;
   if (v < 0) {
     const char* e1 = getenv("PTDR_DENSE_V1");
     const char* ec = getenv("PTDR_PIPE_CFG");
     if (e1 && e1[0] == '1') v = kPipeNone;
-    else if (ec && ec[0] >= '1' && ec[0] <= '3') v = ec[0] - '0';
-    else v = kPipeCfg11x4;
+    else if (ec && ec[0] >= '1' && ec[0] <= '0' + kPipeCfgCount) v = ec[0] - '0';
+    else v = kPipeDefault;
   }
   return v;
 }
 
-static DensePlan plan_for(int mode, int nv, uint64_t C) {
-  const bool pipe_ok = mode == MODE_GENERAL || mode == MODE_HERM_HALF || mode == MODE_SYM_HALF;
-  int cfg = pipe_ok ? pipe_choice() : kPipeNone;
-  DensePlan p = make_dense_plan(nv, C, cfg);
-  if (pipe_ok && cfg != kPipeNone && p.pipe_cfg == kPipeNone)  // e.g. nv = 16 with LT = 11
-    p = make_dense_plan(nv, C, kPipeCfg12);
-  return p;
+static bool pipe_mode(int mode) {
+  return mode == MODE_GENERAL || mode == MODE_HERM_HALF || mode == MODE_SYM_HALF;
+}
+
+static DensePlan plan_for(int mode, int nv, uint64_t x_count) {
+  return make_dense_plan(nv, x_count, pipe_mode(mode) ? pipe_choice() : kPipeNone);
 }
 // The workspace is the max over every kernel choice so the env switches never need more.
-static size_t plan_ws(int nv, uint64_t C) {
+static size_t plan_ws(int nv, uint64_t x_count) {
   size_t m = 0;
-  for (int cfg = kPipeNone; cfg <= kPipeCfg11x3; ++cfg) {
-    const size_t b = make_dense_plan(nv, C, cfg).ws_bytes();
+  for (int cfg = kPipeNone; cfg <= kPipeCfgCount; ++cfg) {
+    const size_t b = make_dense_plan(nv, x_count, cfg).ws_bytes();
     if (b > m) m = b;
   }
   return m;
 }
 
+// X-masks handled by the mirrored launch of HERMITIAN / REAL_SYMMETRIC (n >= 9): the first
+// chunk of the half-length launch must start at a power of two >= its chunk width.
+static uint64_t herm_mirror_width(int n, int hmode) {
+  const uint64_t N = 1ull << n;
+  const DensePlan hp = plan_for(hmode, n - 1, N - 32);
+  return hp.W;
+}
+
 // Workspace of the dense path = max over the launches of one call.
 static size_t dense_ws(int n, int s, int world) {
-  if (s == PTDR_GENERAL) {
-    const uint64_t C = world > 1 ? ((1ull << n) / (uint64_t)world) / 16 : dense_chunks(n);
-    return plan_ws(n, C);
+  const uint64_t N = 1ull << n;
+  if (s == PTDR_GENERAL) return plan_ws(n, world > 1 ? N / (uint64_t)world : N);
+  if (n <= 8) return plan_ws(n, N);
+  size_t m = 0;
+  for (uint64_t w : {16ull, 32ull}) {
+    const size_t a = plan_ws(n, w), b = plan_ws(n - 1, N - w);
+    if (a > m) m = a;
+    if (b > m) m = b;
   }
-  if (n <= 8) return plan_ws(n, dense_chunks(n));
-  size_t a = plan_ws(n, 1);
-  size_t b = plan_ws(n - 1, dense_chunks(n) - 1);
-  return a > b ? a : b;
+  return m;
 }
 
 static ptdr_status launch_mode(int mode, const DenseArgs& a, const DensePlan& p, cudaStream_t st,
@@ -131,37 +139,38 @@ static DenseArgs base_args(const double2* A, double2* out, int n, void* ws) {
 
 static ptdr_status run_dense(const double2* A, int n, int s, double2* out, void* ws,
                              cudaStream_t st, int* nl) {
-  const uint64_t C = dense_chunks(n);
+  const uint64_t N = 1ull << n;
   if (s == PTDR_GENERAL || n <= 8) {
     const int mode = s == PTDR_GENERAL ? MODE_GENERAL
                      : s == PTDR_HERMITIAN ? MODE_HERM_MIRROR : MODE_SYM_MIRROR;
-    DensePlan p = plan_for(mode, n, C);
+    DensePlan p = plan_for(mode, n, N);
     DenseArgs a = base_args(A, out, n, ws);
     a.nv = n;
     a.x_base = 0;
-    a.nchunks = C;
+    a.nchunks = p.nchunks;
     a.scratch = reinterpret_cast<double2*>(reinterpret_cast<char*>(ws) + p.ctr_bytes);
     return launch_mode(mode, a, p, st, nl);
   }
-  // HERMITIAN / REAL_SYMMETRIC, n >= 9: chunk 0 (x < 16) on full-length mirrored
-  // vectors, then chunks 1.. on half-length vectors.
+  // HERMITIAN / REAL_SYMMETRIC, n >= 9: X-masks below the half-length launch's chunk width
+  // on full-length mirrored vectors, the rest on half-length vectors.
+  const int hmode = s == PTDR_HERMITIAN ? MODE_HERM_HALF : MODE_SYM_HALF;
+  const uint64_t w = herm_mirror_width(n, hmode);
   {
-    DensePlan p = plan_for(MODE_HERM_MIRROR, n, 1);
+    DensePlan p = plan_for(MODE_HERM_MIRROR, n, w);
     DenseArgs a = base_args(A, out, n, ws);
     a.nv = n;
     a.x_base = 0;
-    a.nchunks = 1;
+    a.nchunks = p.nchunks;
     a.scratch = reinterpret_cast<double2*>(reinterpret_cast<char*>(ws) + p.ctr_bytes);
     ptdr_status r = launch_mode(s == PTDR_HERMITIAN ? MODE_HERM_MIRROR : MODE_SYM_MIRROR, a, p, st, nl);
     if (r != PTDR_OK) return r;
   }
   {
-    const int hmode = s == PTDR_HERMITIAN ? MODE_HERM_HALF : MODE_SYM_HALF;
-    DensePlan p = plan_for(hmode, n - 1, C - 1);
+    DensePlan p = plan_for(hmode, n - 1, N - w);
     DenseArgs a = base_args(A, out, n, ws);
     a.nv = n - 1;
-    a.x_base = 16;
-    a.nchunks = C - 1;
+    a.x_base = w;
+    a.nchunks = p.nchunks;
     a.scratch = reinterpret_cast<double2*>(reinterpret_cast<char*>(ws) + p.ctr_bytes);
     return launch_mode(hmode, a, p, st, nl);
   }
@@ -274,9 +283,8 @@ ptdr_status ptdr_decompose_xshard_async(const ptdr_c128* A_local, int n, int ran
   if (ws_bytes < need) return fail(PTDR_ENOMEM, "workspace too small");
   const uint64_t N = 1ull << n, R = N >> g;
   if (overlaps(A_local, N * R * 16, out_local, N * R * 16)) return fail(PTDR_EUNSUPPORTED, "out overlaps A");
-  const uint64_t C = R / 16;
-  DensePlan p = plan_for(MODE_GENERAL, n, C);
-  if (p.kind == 1) p.kind = 0;  // shards narrower than a single-phase tile: direct kernel
+  DensePlan p = plan_for(MODE_GENERAL, n, R);
+  if (p.kind == 1) { p.kind = 0; p.nchunks = R / 16; }  // narrow shards: direct kernel
   DenseArgs a = base_args(reinterpret_cast<const double2*>(A_local), reinterpret_cast<double2*>(out_local),
                           n, workspace);
   a.ld = R;
@@ -284,7 +292,7 @@ ptdr_status ptdr_decompose_xshard_async(const ptdr_c128* A_local, int n, int ran
   a.gshift = n - g;
   a.nv = n;
   a.x_base = (uint64_t)rank * R;
-  a.nchunks = C;
+  a.nchunks = p.nchunks;
   a.scratch = reinterpret_cast<double2*>(reinterpret_cast<char*>(workspace) + p.ctr_bytes);
   int nl = 0;
   ptdr_status r = launch_mode(MODE_GENERAL, a, p, reinterpret_cast<cudaStream_t>(stream), &nl);

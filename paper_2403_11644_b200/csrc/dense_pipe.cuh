@@ -1,0 +1,546 @@
+// dense_pipe.cuh -- warp-specialised TMA pipeline for the dense path (two-phase, nv >= 11).
+//
+// Same math as dense_impl.cuh (phase A: XOR-transpose gather + WHT over the low R index
+// bits into the scratch; phase B: WHT over the high M = nv - R bits + epilogue in q
+// order), organised for sm_100a:
+//   * one CTA per SM; warp 0 lane 0 = producer (tickets, inter-CTA dependency checks
+//     prefetched one tile ahead, TMA issue); NG consumer groups of GW warps take tiles
+//     round-robin from an NS-stage SMEM ring (mbarrier full/empty pipeline);
+//   * phase-A tiles (2^(R-4) row blocks of 16 x 16 complex128) arrive by 2-D TMA
+//     (cp.async.bulk.tensor), phase-B tiles (one contiguous 2^LT-element block of the
+//     B-tile-major scratch) by 1-D bulk copy;  HBM loads of later tiles overlap the
+//     arithmetic of earlier ones;
+//   * the XOR transpose happens in the SMEM read (conflict-free); the exchange between
+//     the two radix-16 register stages is done in place in the stage buffer;
+//   * consumed scratch lines are discarded from L2 (never written back to HBM);
+//   * completion counters are bumped per warp with release atomics (no CTA barrier).
+// Tile = 2^LT complex128 (LT = R + 4); a group has 2^(LT-4) threads holding 16 each.
+#pragma once
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+#include <mutex>
+
+#include "dense_impl.cuh"
+#include "dense_plan.h"
+#include "internal.h"
+#include "sm100_ptx.cuh"
+
+namespace ptdr {
+
+struct TileMeta {
+  int valid, phase, tile, seq;
+  unsigned chunk, pad0, pad1, pad2;
+};
+
+// Relaxed GPU-scope load of a completion counter.  No L1 invalidation (an acquire load
+// would emit CCTL.IVALL and stall the producer for a full L2 round trip per tile).  The
+// data the producer then reads is fetched by the TMA from L2 (the point of coherence)
+// in an instruction control-dependent on this value, after fence.proxy.async.global.
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Debug timeline (PTDR_TRACE=1): CTA 0 records clock64 stamps of its first kTraceTiles
+// tiles into a.trace[tile * 16 + field].
+constexpr int kTraceTiles = 512;
+__device__ __forceinline__ void trace_stamp(unsigned long long* tr, int k, int field) {
+  if (tr != nullptr && blockIdx.x == 0 && k < kTraceTiles) tr[k * 16 + field] = clock64();
+}
+
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// ---- 32-bit index arithmetic: n <= 16 so x, z < 2^16 and q < 2^32 ----------------------
+__device__ __forceinline__ uint32_t spread16(uint32_t v) {
+  v &= 0xFFFFu;
+  v = (v | (v << 8)) & 0x00FF00FFu;
+  v = (v | (v << 4)) & 0x0F0F0F0Fu;
+  v = (v | (v << 2)) & 0x33333333u;
+  v = (v | (v << 1)) & 0x55555555u;
+  return v;
+}
+__device__ __forceinline__ uint32_t q_offset32(uint32_t x, uint32_t z, int gshift) {
+  const uint32_t m = (gshift >= 32) ? 0xFFFFFFFFu : ((1u << gshift) - 1u);
+  const uint32_t top = (gshift >= 16) ? 0u : ((z >> gshift) << (2 * gshift));
+  return top | spread16((x ^ z) & m) | (spread16(z & m) << 1);
+}
+// q delta of setting z bit l (code_l = 2 z_l + (x_l ^ z_l); above gshift the z bit
+// indexes the rank-local block).
+__device__ __forceinline__ uint32_t q_delta32(uint32_t x, int l, int gshift) {
+  return (l < gshift) ? ((uint32_t)(3 - 2 * (int)((x >> l) & 1u)) << (2 * l)) : (1u << (l + gshift));
+}
+__device__ __forceinline__ uint32_t insert0_32(uint32_t v, int t) {
+  const uint32_t lo = v & ((1u << t) - 1u);
+  return ((v >> t) << (t + 1)) | lo;
+}
+
+// Epilogue of one thread-unit: q offset and phase of the unit's base (x, z) plus per-bit
+// deltas for the NB z bits that vary over the unit's registers (compile-time subsets).
+template <int NB, bool HALF>
+struct EpiUnit {
+  uint32_t q0, p0, Dt;
+  uint32_t D[NB];
+  uint32_t P[NB];
+  __device__ __forceinline__ void init(uint32_t x, uint32_t zu, int base_pos, int t, int gshift) {
+    const uint32_t zf = HALF ? insert0_32(zu, t) : zu;
+    q0 = q_offset32(x, zf, gshift);
+    p0 = __popc(x & zf);
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      int l = base_pos + b;
+      if (HALF) l += (l >= t) ? 1 : 0;
+      D[b] = q_delta32(x, l, gshift);
+      P[b] = (x >> l) & 1u;
+    }
+    Dt = HALF ? q_delta32(x, t, gshift) : 0u;
+  }
+};
+
+template <int MODE, int NB, int J>
+__device__ __forceinline__ void emit_reg(const DenseArgs& a, const EpiUnit<NB, (MODE >= 3)>& e,
+                                         double2 w) {
+  uint32_t q = e.q0, p = e.p0;
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    if (J & (1 << b)) {
+      q += e.D[b];
+      p += e.P[b];
+    }
+  }
+  if constexpr (MODE == MODE_GENERAL) {
+    const double2 c = rot_ipow(w, (int)p);
+    st_stream(a.out + q, make_double2(c.x * a.scale, c.y * a.scale));
+  } else {
+    // half-length modes: alpha = 2^{1-n} {Re, -Im, -Re, Im}[popcount(x&z) mod 4] (real)
+    const uint32_t p0 = p & 3u, p1 = (p + 1u) & 3u;
+    const double s = 2.0 * a.scale;
+    const double v0 = (p0 == 0) ? w.x : (p0 == 1) ? -w.y : (p0 == 2) ? -w.x : w.y;
+    const double v1 = (p1 == 0) ? w.x : (p1 == 1) ? -w.y : (p1 == 2) ? -w.x : w.y;
+    st_stream(a.out + q, make_double2(v0 * s, 0.0));
+    st_stream(a.out + (q + e.Dt), make_double2(v1 * s, 0.0));
+  }
+}
+
+template <int MODE, int NB, int J = 0>
+__device__ __forceinline__ void emit_all(const DenseArgs& a, const EpiUnit<NB, (MODE >= 3)>& e,
+                                         const double2* w) {
+  if constexpr (J < (1 << NB)) {
+    emit_reg<MODE, NB, J>(a, e, w[J]);
+    emit_all<MODE, NB, J + 1>(a, e, w);
+  }
+}
+
+// Ticket order of dense_impl.cuh's decode_ticket, 32-bit, NA = NB = 2^M.
+__device__ __forceinline__ void decode_ticket32(uint32_t t, int M, uint32_t C, uint32_t L, int& phase,
+                                                uint32_t& chunk, uint32_t& tile) {
+  const uint32_t NA = 1u << M;
+  const uint32_t lp1 = (L + 1u < C) ? L + 1u : C;
+  const uint32_t pro = lp1 << M;
+  if (t < pro) {
+    phase = 0; chunk = t >> M; tile = t & (NA - 1u);
+    return;
+  }
+  t -= pro;
+  const uint32_t steady = C > L + 1u ? C - L - 1u : 0u;
+  if (t < (steady << (M + 1))) {
+    const uint32_t c = t >> (M + 1), o = t & (2u * NA - 1u);
+    if (o < NA) { phase = 1; chunk = c; tile = o; }
+    else { phase = 0; chunk = c + L + 1u; tile = o - NA; }
+    return;
+  }
+  t -= steady << (M + 1);
+  phase = 1; chunk = steady + (t >> M); tile = t & (NA - 1u);
+}
+
+template <int LT, int XB, int GW, int NG, int NS>
+struct PipeCfg {
+  static constexpr int TE = 1 << LT;          // tile elements
+  static constexpr int TB = TE * 16;          // tile bytes
+  static constexpr int W = 1 << XB;           // X-masks per chunk (TMA box = W rows x W cols)
+  static constexpr int R = LT - XB;           // phase-A index bits (rows per phase-A tile = 2^R)
+  static constexpr int GT = GW * 32;          // threads per group (= TE / 16)
+  static constexpr int SIGD = 4;               // completion-signal slots per group
+  static constexpr int THREADS = 32 * (2 + NG * GW);  // warp 0 producer, warp 1 signaler
+  static constexpr int SMEM = NS * TB + 2048;
+  static_assert(GT * 16 == TE, "16 elements per consumer thread");
+};
+
+// Fiber index of the phase-B tiles: phi encodes (u, zl) with bits [0,1]=u0,u1 [2,3]=zl0,zl1
+// [4, XB+2)=u2.. [XB+2, ..)=zl2.., so 2^k consecutive fibers form a (u, zl) square of
+// 4^(k/2) consecutive q (coalesced epilogue stores).
+template <int XB>
+__device__ __forceinline__ uint32_t phi_of(uint32_t u, uint32_t zl) {
+  return (u & 3u) | ((zl & 3u) << 2) | ((u >> 2) << 4) | ((zl >> 2) << (XB + 2));
+}
+template <int XB>
+__device__ __forceinline__ uint32_t phi_u_of(uint32_t phi) {
+  return (phi & 3u) | (((phi >> 4) & ((1u << (XB - 2)) - 1u)) << 2);
+}
+template <int XB>
+__device__ __forceinline__ uint32_t phi_zl_of(uint32_t phi) {
+  return ((phi >> 2) & 3u) | ((phi >> (XB + 2)) << 2);
+}
+
+// Scratch layout (per chunk slot): B-tile-major Y[tileB][ih][f], 2^LT elements per phase-B
+// tile, so a phase-B tile is one contiguous bulk copy (fiber phi = tileB * FB + f).
+template <int LT, int XB, int GW, int NG, int NS, int M, int MODE>
+__global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS>::THREADS, 1)
+    dense_pipe_kernel(const __grid_constant__ CUtensorMap tmap, DenseArgs a) {
+  using Cfg = PipeCfg<LT, XB, GW, NG, NS>;
+  constexpr int R = Cfg::R, TE = Cfg::TE, GT = Cfg::GT, W = Cfg::W;
+  constexpr bool HALF = (MODE == MODE_HERM_HALF || MODE == MODE_SYM_HALF);
+  constexpr int FB = TE >> M;  // phase-B fibers per tile
+  constexpr int LFB = LT - M;
+  static_assert(M >= 4 && M <= 8 && LFB <= XB + 4, "phase-B fibre length 2^4..2^8");
+  static_assert(R >= XB && R - 4 >= 1 && R - 4 <= 4, "phase-A tile geometry");
+  extern __shared__ __align__(1024) unsigned char smem[];
+  double2* stage0 = reinterpret_cast<double2*>(smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * Cfg::TB);
+  uint64_t* empty = full + NS;
+  TileMeta* meta = reinterpret_cast<TileMeta*>(empty + NS);
+  constexpr int SIGD = Cfg::SIGD;
+  uint64_t* sigbar = reinterpret_cast<uint64_t*>(meta + NS);  // [NG][SIGD], count GW
+  uint64_t* sigfree = sigbar + NG * SIGD;                       // [NG][SIGD], count 1
+  unsigned** sigptr = reinterpret_cast<unsigned**>(sigfree + NG * SIGD);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t C = (uint32_t)a.nchunks;
+  unsigned* ticket = a.ctr;
+  unsigned* doneA = a.ctr + 1;
+  unsigned* doneB = a.ctr + 1 + C;
+  const uint32_t nslot = (uint32_t)a.nslot;
+  const unsigned done_target = 1u << M;  // one completion signal per tile
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], GW);
+      meta[s].seq = -1;
+    }
+    for (int i = 0; i < NG * SIGD; ++i) {
+      mbar_init(&sigbar[i], GW);
+      mbar_init(&sigfree[i], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  // ------------------------------------------------------------------ producer
+  if (warp == 0) {
+    if (lane == 0) {
+      prefetch_tmap(&tmap);
+      const uint64_t pol = policy_evict_first();
+      const uint32_t total = C << (M + 1);
+      // Decoded ticket: (tk, phase, chunk, tile) and its dependency counter, whose value is
+      // requested (dv) one tile before it is checked.
+      auto decode_into = [&](uint32_t tk, uint32_t& tkX, int& phX, uint32_t& chX, uint32_t& tlX,
+                             const unsigned*& depX, unsigned& dvX) {
+        tkX = tk;
+        phX = 0; chX = 0; tlX = 0;
+        depX = nullptr;
+        dvX = 0;
+        if (tk < total) {
+          decode_ticket32(tk, M, C, (uint32_t)a.L, phX, chX, tlX);
+          if (phX == 1) depX = &doneA[chX];
+          else if (chX >= nslot) depX = &doneB[chX - nslot];
+          if (depX) dvX = ld_relaxed(depX);
+        }
+      };
+      int k = 0, ends = 0;
+      // Publish one tile (or an end marker) into stage k % NS.  Returns true when all
+      // groups have received their end marker.
+      auto process = [&](const uint32_t& tkX, const int& phX, const uint32_t& chX,
+                         const uint32_t& tlX, const unsigned* const& depX,
+                         const unsigned& dvX) -> bool {
+        const int s = k % NS;
+        trace_stamp(a.trace, k, 0);
+        if (k >= NS) mbar_wait(&empty[s], (uint32_t)((k / NS) - 1) & 1u);
+        trace_stamp(a.trace, k, 1);
+        if (tkX >= total) {
+          // one invalid tile per group ends the consumers
+          meta[s].valid = 0;
+          meta[s].seq = k;
+          mbar_arrive(&full[s]);
+          ++k;
+          return ++ends == NG;
+        }
+        if (depX) {
+          unsigned v = dvX;
+          while (v < done_target) {
+            __nanosleep(64);
+            v = ld_relaxed(depX);
+          }
+        }
+        trace_stamp(a.trace, k, 2);
+        if (a.trace && blockIdx.x == 0 && k < kTraceTiles) a.trace[k * 16 + 8] = phX;
+        double2* dst = stage0 + (size_t)s * TE;
+        meta[s].valid = 1;
+        meta[s].phase = phX;
+        meta[s].tile = (int)tlX;
+        meta[s].chunk = chX;
+        meta[s].seq = k;
+        if (phX == 0) {
+          mbar_arrive_expect_tx(&full[s], (uint32_t)Cfg::TB);
+          const uint32_t x0 = (uint32_t)a.x_base + (chX << XB);
+          const int t = HALF ? 31 - __clz(x0) : 0;
+          const uint32_t cm = (uint32_t)a.colmask & ~(uint32_t)(W - 1);
+#pragma unroll
+          for (int rb = 0; rb < (1 << (R - XB)); ++rb) {
+            const uint32_t iv0 = (tlX << R) + (uint32_t)rb * W;
+            const uint32_t row0 = HALF ? insert0_32(iv0, t) : iv0;
+            const uint32_t col0 = (row0 ^ x0) & cm;
+            tma_load_2d(dst + rb * W * W, &tmap, (int)(col0 * 2u), (int)row0, &full[s], pol);
+          }
+        } else {
+          // scratch written by other CTAs' generic stores, read by the async proxy
+          fence_proxy_async_global();
+          mbar_arrive_expect_tx(&full[s], (uint32_t)Cfg::TB);
+          const double2* src = a.scratch + (size_t)(chX % nslot) * a.slot_elems + ((size_t)tlX << LT);
+          bulk_load(dst, src, (uint32_t)Cfg::TB, &full[s], pol);
+        }
+        trace_stamp(a.trace, k, 3);
+        ++k;
+        return false;
+      };
+      // Tickets come in pairs (one atomic per two tiles, one pair ahead), and the two
+      // decoded tickets live in fixed register sets P and Q that alternate: no register
+      // holding an in-flight load result is ever copied (a copy would stall on it).
+      // A claimed ticket is always processed, in claim order, so this is deadlock-free.
+      uint32_t tkP, chP, tlP, tkQ, chQ, tlQ;
+      int phP, phQ;
+      const unsigned *depP, *depQ;
+      unsigned dvP, dvQ;
+      const uint32_t b0 = atomicAdd(ticket, 2u);
+      decode_into(b0, tkP, phP, chP, tlP, depP, dvP);
+      decode_into(b0 + 1, tkQ, phQ, chQ, tlQ, depQ, dvQ);
+      uint32_t nb = (b0 + 1 < total) ? atomicAdd(ticket, 2u) : total;
+      for (;;) {
+        if (process(tkP, phP, chP, tlP, depP, dvP)) break;
+        decode_into(nb, tkP, phP, chP, tlP, depP, dvP);
+        if (process(tkQ, phQ, chQ, tlQ, depQ, dvQ)) break;
+        decode_into(nb + 1, tkQ, phQ, chQ, tlQ, depQ, dvQ);
+        nb = (nb + 1 < total) ? atomicAdd(ticket, 2u) : total;
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------ signaler
+  // Consumers arrive (per warp, non-blocking) on sigbar after their global stores; this
+  // thread turns each completed tile into one release increment of the tile's counter
+  // (cumulative over the stores observed through the mbarrier, as a CTA barrier followed
+  // by one thread's release would be), so no consumer warp ever waits on a memory fence.
+  if (warp == 1) {
+    if (lane == 0) {
+      int jg[NG];
+#pragma unroll
+      for (int gg = 0; gg < NG; ++gg) jg[gg] = 0;
+      int ended = 0;
+      while (ended < NG) {
+        bool progress = false;
+#pragma unroll
+        for (int gg = 0; gg < NG; ++gg) {
+          if (jg[gg] < 0) continue;
+          const int d = jg[gg] % SIGD;
+          if (mbar_try_wait(&sigbar[gg * SIGD + d], (uint32_t)(jg[gg] / SIGD) & 1u)) {
+            unsigned* p = sigptr[gg * SIGD + d];
+            if (p == nullptr) {
+              jg[gg] = -1;
+              ++ended;
+            } else {
+              red_release_add(p, 1u);
+              ++jg[gg];
+            }
+            mbar_arrive(&sigfree[gg * SIGD + d]);
+            progress = true;
+          }
+        }
+        if (!progress) __nanosleep(32);
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------ consumers
+  const int g = (warp - 2) / GW;
+  const int gtid = threadIdx.x - 64 - g * GT;
+  const int wig = gtid >> 5;  // warp index within the group
+  // per-warp completion signal of the group's j-th tile (see the signaler)
+  auto signal = [&](int j, unsigned* counter) {
+    __syncwarp();
+    if (lane == 0) {
+      const int d = j % SIGD;
+      if (j >= SIGD) mbar_wait(&sigfree[g * SIGD + d], (uint32_t)((j / SIGD) - 1) & 1u);
+      if (wig == 0) sigptr[g * SIGD + d] = counter;
+      mbar_arrive(&sigbar[g * SIGD + d]);
+    }
+  };
+  const int bar_id = 1 + g;
+  int j = 0;
+  for (int k = g;; k += NG, ++j) {
+    const int s = k % NS;
+    // stages are shared round-robin by the groups, so a parity wait alone could match an
+    // older phase: first wait until the producer has published tile k in this stage
+    if (gtid == 0) trace_stamp(a.trace, k, 4);
+    while (*reinterpret_cast<volatile int*>(&meta[s].seq) != k) __nanosleep(20);
+    mbar_wait(&full[s], (uint32_t)(k / NS) & 1u);
+    if (gtid == 0) trace_stamp(a.trace, k, 5);
+    const TileMeta m = meta[s];
+    if (!m.valid) {
+      signal(j, nullptr);  // end marker for the signaler
+      break;
+    }
+    double2* S = stage0 + (size_t)s * TE;
+    const uint32_t chunk = m.chunk;
+    double2* Y = a.scratch + (size_t)(chunk % nslot) * a.slot_elems;
+    double2 v[16];
+    if (m.phase == 0) {
+      // ---- phase A: v_x[i] for x = x0+u, i = tile*2^R + r, r = jh*16 + kk; the element
+      //      sits in SMEM row r at column (r mod W) ^ u (XOR transpose in the read)
+      {
+        const int u = gtid & (W - 1), jh = gtid >> XB;
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) {
+          const int r = jh * 16 + kk;
+          v[kk] = S[r * W + ((r & (W - 1)) ^ u)];
+          if (MODE == MODE_SYM_HALF) v[kk].y = 0.0;
+        }
+        wht_regs<4>(v);
+        __syncwarp();  // rows of this jh are read and written only by this warp
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) S[(jh * 16 + kk) * W + u] = v[kk];
+      }
+      named_bar_sync(bar_id, GT);
+      constexpr int R2 = R - 4;
+      constexpr int UA = (W * 16) / GT;  // (u, jl) units per thread, each 2^R2 registers
+#pragma unroll
+      for (int p = 0; p < UA; ++p) {
+        const int uu = gtid + GT * p;
+        const int u = uu & (W - 1), jl = uu >> XB;
+#pragma unroll
+        for (int j = 0; j < (1 << R2); ++j) v[p * (1 << R2) + j] = S[(j * 16 + jl) * W + u];
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (gtid == 0) trace_stamp(a.trace, k, 6);
+      const uint64_t pol_last = policy_evict_last();
+#pragma unroll
+      for (int p = 0; p < UA; ++p) {
+        const int uu = gtid + GT * p;
+        const int u = uu & (W - 1), jl = uu >> XB;
+        wht_regs<R2>(&v[p * (1 << R2)]);
+        // element (u, ih = tile, zl = j*16 + jl) -> Y[tileB][ih][f]
+        const uint32_t phi_lo = phi_of<XB>((uint32_t)u, (uint32_t)jl);
+        double2* base = Y + (((phi_lo >> LFB) << LT) | ((uint32_t)m.tile << LFB) | (phi_lo & (FB - 1)));
+#pragma unroll
+        for (int j = 0; j < (1 << R2); ++j)
+          st_global_hint(base + ((size_t)j << (XB + 4 - LFB + LT)), v[p * (1 << R2) + j], pol_last);
+      }
+      signal(j, &doneA[chunk]);
+      if (gtid == 0) trace_stamp(a.trace, k, 7);
+    } else {
+      // ---- phase B: SMEM holds Y[tileB][ih][f] = [j][f]; WHT over j for FB fibers
+      const u64 x0 = a.x_base + ((u64)chunk << XB);
+      const int t = HALF ? 63 - __clzll(x0) : 0;
+      const int f = gtid % FB, jh = gtid / FB;
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) v[kk] = S[(jh * 16 + kk) * FB + f];
+      if (a.discard) {
+        // this tile's scratch is dead once in SMEM: drop it from L2 without write-back
+        // (the next writer of the slot waits for doneB of this chunk)
+        char* yb = reinterpret_cast<char*>(Y + ((size_t)m.tile << LT));
+#pragma unroll
+        for (int d = 0; d < Cfg::TB / 128 / GT; ++d) discard_l2(yb + ((size_t)(gtid + GT * d) << 7));
+      }
+      wht_regs<4>(v);
+      if constexpr (M == 4) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        const uint32_t phi = (uint32_t)m.tile * FB + (uint32_t)f;
+        EpiUnit<4, HALF> e;
+        e.init((uint32_t)x0 + phi_u_of<XB>(phi), phi_zl_of<XB>(phi), R, t, a.gshift);
+        emit_all<MODE, 4>(a, e, v);
+      } else {
+        constexpr int R2 = M - 4;
+        constexpr int UB = (FB * 16) / GT;  // (f, jl) units per thread, 2^R2 registers each
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) S[(jh * 16 + kk) * FB + f] = v[kk];
+        named_bar_sync(bar_id, GT);
+#pragma unroll
+        for (int p = 0; p < UB; ++p) {
+          const int uu = gtid + GT * p;
+          const int f2 = uu % FB, jl = uu / FB;
+#pragma unroll
+          for (int j = 0; j < (1 << R2); ++j) v[p * (1 << R2) + j] = S[(j * 16 + jl) * FB + f2];
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (gtid == 0) trace_stamp(a.trace, k, 6);
+#pragma unroll
+        for (int p = 0; p < UB; ++p) {
+          const int uu = gtid + GT * p;
+          const int f2 = uu % FB, jl = uu / FB;
+          const uint32_t phi = (uint32_t)m.tile * FB + (uint32_t)f2;
+          wht_regs<R2>(&v[p * (1 << R2)]);
+          EpiUnit<R2, HALF> e;
+          e.init((uint32_t)x0 + phi_u_of<XB>(phi), ((uint32_t)jl << R) | phi_zl_of<XB>(phi), R + 4, t,
+                 a.gshift);
+          emit_all<MODE, R2>(a, e, &v[p * (1 << R2)]);
+        }
+      }
+      signal(j, &doneB[chunk]);
+      if (gtid == 0) trace_stamp(a.trace, k, 7);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ launch template
+template <int LT, int XB, int GW, int NG, int NS, int M, int MODE>
+static cudaError_t launch_pipe_impl(const CUtensorMap& map, const DenseArgs& a, cudaStream_t st) {
+  using Cfg = PipeCfg<LT, XB, GW, NG, NS>;
+  constexpr auto kern = dense_pipe_kernel<LT, XB, GW, NG, NS, M, MODE>;
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [&]() {
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+  });
+  if (err != cudaSuccess) return err;
+  kern<<<device_sm_count(), Cfg::THREADS, Cfg::SMEM, st>>>(map, a);
+  return cudaGetLastError();
+}
+
+template <int LT, int XB, int GW, int NG, int NS, int MODE>
+static cudaError_t launch_pipe_m(const CUtensorMap& map, const DenseArgs& a, int M, cudaStream_t st) {
+  switch (M) {
+    case 4: return launch_pipe_impl<LT, XB, GW, NG, NS, 4, MODE>(map, a, st);
+    case 5: return launch_pipe_impl<LT, XB, GW, NG, NS, 5, MODE>(map, a, st);
+    case 6: return launch_pipe_impl<LT, XB, GW, NG, NS, 6, MODE>(map, a, st);
+    case 7: return launch_pipe_impl<LT, XB, GW, NG, NS, 7, MODE>(map, a, st);
+    case 8: return launch_pipe_impl<LT, XB, GW, NG, NS, 8, MODE>(map, a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int LT, int XB, int GW, int NG, int NS>
+static cudaError_t launch_pipe_cfg(int mode, const CUtensorMap& map, const DenseArgs& a, int M,
+                                   cudaStream_t st) {
+  switch (mode) {
+    case MODE_GENERAL: return launch_pipe_m<LT, XB, GW, NG, NS, MODE_GENERAL>(map, a, M, st);
+    case MODE_HERM_HALF: return launch_pipe_m<LT, XB, GW, NG, NS, MODE_HERM_HALF>(map, a, M, st);
+    case MODE_SYM_HALF: return launch_pipe_m<LT, XB, GW, NG, NS, MODE_SYM_HALF>(map, a, M, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+#define PTDR_DEFINE_PIPE_CFG(NAME, LT, XB, GW, NG, NS)                                         \
+  cudaError_t NAME(int mode, const CUtensorMap& map, const DenseArgs& a, int M, cudaStream_t st) { \
+    return launch_pipe_cfg<LT, XB, GW, NG, NS>(mode, map, a, M, st);                           \
+  }
+
+}  // namespace ptdr

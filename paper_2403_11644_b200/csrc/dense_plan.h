@@ -22,7 +22,8 @@ struct DensePlan {
   int NA = 0, NB = 0;  // tiles per chunk in phase A / B (two-phase)
   int L = 0;           // look-ahead (chunks of phase A issued ahead of phase B)
   int nslot = 0;       // scratch ring slots
-  int pipe_cfg = 0;    // 0: dense_impl.cuh kernels; else a dense_pipe.cu configuration
+  int pipe_cfg = 0;    // 0: dense_impl.cuh kernels; else a dense_pipe.cuh configuration
+  int W = 16;          // X-masks per chunk
   uint64_t nchunks = 0;
   uint64_t slot_elems = 0;  // complex128 elements per scratch slot
   size_t ctr_bytes = 0;
@@ -30,41 +31,67 @@ struct DensePlan {
   size_t ws_bytes() const { return ctr_bytes + scratch_bytes; }
 };
 
-// dense_pipe.cu configurations: tile 2^LT elements, GW warps per group, NG groups, NS stages.
-enum { kPipeNone = 0, kPipeCfg12 = 1 /* 12,8,2,3 */, kPipeCfg11x4 = 2 /* 11,4,4,6 */,
-       kPipeCfg11x3 = 3 /* 11,4,3,6 */ };
-inline int pipe_lt(int cfg) { return cfg == kPipeCfg12 ? 12 : 11; }
-inline int pipe_stages(int cfg) { return cfg == kPipeCfg12 ? 3 : 6; }
+// dense_pipe.cuh configurations (dense_pipe_c<k>.cu): tile 2^LT elements, chunk width 2^XB,
+// GW warps per group, NG groups, NS stages.
+struct PipeGeom {
+  int LT, XB, GW, NG, NS;
+};
+constexpr int kPipeNone = 0;
+constexpr int kPipeCfgCount = 5;
+inline PipeGeom pipe_geom(int cfg) {
+  switch (cfg) {
+    case 1: return {12, 4, 8, 2, 3};
+    case 2: return {11, 4, 4, 4, 6};
+    case 3: return {11, 4, 4, 3, 6};
+    case 4: return {12, 5, 8, 2, 3};
+    case 5: return {11, 5, 4, 3, 6};
+    default: return {0, 4, 0, 0, 0};
+  }
+}
+constexpr int kPipeDefault = 4;   // preferred configuration
+constexpr int kPipeFallback = 1;  // when the preferred one does not fit (nv, x_count)
 
 // Tiles resident at once on a B200 (fixes L deterministically, independent of the device).
 constexpr int kNominalSMs = 148;
-constexpr int kNominalResidentCtas = 296;          // v1: 148 SMs x 2 CTAs
+constexpr int kNominalResidentCtas = 296;            // v1: 148 SMs x 2 CTAs
 constexpr uint64_t kPipeScratchBudget = 2ull << 30;  // bytes of scratch slots for the pipeline
 
-// pipe_cfg: requested dense_pipe.cu configuration (0 = v1 kernels).  Falls back to v1 when
-// the phase split does not fit the configuration (M = nv - (LT-4) must be in [4, 8]).
-inline DensePlan make_dense_plan(int nv, uint64_t nchunks, int pipe_cfg = kPipeNone) {
+inline bool pipe_fits(int cfg, int nv, uint64_t x_count) {
+  if (cfg == kPipeNone) return false;
+  const PipeGeom g = pipe_geom(cfg);
+  const int R = g.LT - g.XB, M = nv - R;
+  return M >= 4 && M <= 8 && (g.LT - M) <= g.XB + 4 && x_count % (1ull << g.XB) == 0 &&
+         x_count >= (1ull << g.XB);
+}
+
+// Plan for one launch transforming vectors of 2^nv elements for x_count X-masks.
+// pipe_cfg: requested dense_pipe configuration (0 = v1 kernels); falls back when it does
+// not fit (phase-B length M = nv - (LT - XB) must be in [4, 8], x_count a multiple of the
+// chunk width).
+inline DensePlan make_dense_plan(int nv, uint64_t x_count, int pipe_cfg = kPipeNone) {
   DensePlan p;
   p.nv = nv;
-  p.nchunks = nchunks;
-  if (nv <= 5) { p.kind = 0; return p; }
-  if (nv <= 7) { p.kind = 1; p.R = nv; p.M = 0; return p; }
+  if (nv <= 5) { p.kind = 0; p.nchunks = x_count >= 16 ? x_count / 16 : 1; return p; }
+  if (nv <= 7) { p.kind = 1; p.R = nv; p.M = 0; p.nchunks = x_count / 16; return p; }
   p.kind = 2;
-  if (pipe_cfg != kPipeNone) {
-    const int R = pipe_lt(pipe_cfg) - 4;
-    if (nv - R < 4 || nv - R > 8) pipe_cfg = kPipeNone;
-  }
+  if (pipe_cfg != kPipeNone && !pipe_fits(pipe_cfg, nv, x_count))
+    pipe_cfg = pipe_fits(kPipeFallback, nv, x_count) ? kPipeFallback : kPipeNone;
   p.pipe_cfg = pipe_cfg;
   int resident;
   if (pipe_cfg != kPipeNone) {
-    p.R = pipe_lt(pipe_cfg) - 4;
+    const PipeGeom g = pipe_geom(pipe_cfg);
+    p.W = 1 << g.XB;
+    p.R = g.LT - g.XB;
     p.M = nv - p.R;
-    resident = kNominalSMs * pipe_stages(pipe_cfg);
+    resident = kNominalSMs * g.NS;
   } else {
+    p.W = 16;
     if (nv <= 11) { p.R = nv - 4; p.M = 4; }
     else { p.R = 8; p.M = nv - 8; }
     resident = kNominalResidentCtas;
   }
+  p.nchunks = x_count / (uint64_t)p.W;
+  const uint64_t nchunks = p.nchunks;
   p.NA = 1 << p.M;
   p.NB = 1 << p.M;
   const int period = p.NA + p.NB;
@@ -78,8 +105,9 @@ inline DensePlan make_dense_plan(int nv, uint64_t nchunks, int pipe_cfg = kPipeN
   // byte budget): consumed slots are discarded from L2, so only the live ~L chunks occupy
   // L2 and the extra slots cost HBM capacity, not bandwidth.
   uint64_t ns = (uint64_t)L + 2;
+  p.slot_elems = (uint64_t)p.W << nv;
   if (pipe_cfg != kPipeNone) {
-    const uint64_t slot_bytes = ((uint64_t)16 << nv) * 16;
+    const uint64_t slot_bytes = p.slot_elems * 16;
     uint64_t budget = kPipeScratchBudget / slot_bytes;
     const uint64_t need = 2ull * (uint64_t)L + 2ull + (uint64_t)(resident / period);
     if (budget < need) budget = need;
@@ -87,7 +115,6 @@ inline DensePlan make_dense_plan(int nv, uint64_t nchunks, int pipe_cfg = kPipeN
   }
   if (ns > nchunks) ns = nchunks;
   p.nslot = (int)ns;
-  p.slot_elems = (uint64_t)16 << nv;
   p.ctr_bytes = ((4 * (1 + 2 * nchunks)) + 255) / 256 * 256;
   p.scratch_bytes = (size_t)p.nslot * p.slot_elems * 16;
   return p;

@@ -49,8 +49,10 @@ def test_workspace_is_deterministic_and_small(L):
         for s in ("general", "hermitian", "real_symmetric"):
             a = ptdr.workspace_bytes(n, s)
             assert a == ptdr.workspace_bytes(n, s)
-            # the scratch ring stays a small fraction of the 126 MB L2 + counters
-            assert a <= 80 << 20, (n, s, a)
+            # scratch slots are capped by a 2 GiB budget, never more
+            # than the input itself
+            assert a <= (2 << 30) + (1 << 20), (n, s, a)
+            assert a <= 16 * 4 ** n + (1 << 20), (n, s, a)
     assert ptdr.workspace_bytes(24, "diagonal") == 0
     assert ptdr.workspace_bytes(24, "tridiagonal") == 2 * (1 << 24) * 16
     with pytest.raises(ptdr.PtdrError):

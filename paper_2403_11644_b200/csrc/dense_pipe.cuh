@@ -100,38 +100,57 @@ struct EpiUnit {
   }
 };
 
-template <int MODE, int NB, int J>
-__device__ __forceinline__ void emit_reg(const DenseArgs& a, const EpiUnit<NB, (MODE >= 3)>& e,
+// One output register: alpha = 2^-n i^p w at q (GENERAL), or the two real outputs of the
+// half-length modes.  Branch-free: i^p w * scale = (p&1 ? (-w.y, w.x) : (w.x, w.y)) *
+// (p&2 ? -scale : scale).
+template <int MODE>
+__device__ __forceinline__ void emit_one(const DenseArgs& a, uint32_t q, uint32_t p, uint32_t dt,
                                          double2 w) {
-  uint32_t q = e.q0, p = e.p0;
-#pragma unroll
-  for (int b = 0; b < NB; ++b) {
-    if (J & (1 << b)) {
-      q += e.D[b];
-      p += e.P[b];
-    }
-  }
   if constexpr (MODE == MODE_GENERAL) {
-    const double2 c = rot_ipow(w, (int)p);
-    st_stream(a.out + q, make_double2(c.x * a.scale, c.y * a.scale));
+    const bool sw = (p & 1u) != 0;
+    const double s = (p & 2u) ? -a.scale : a.scale;
+    const double re = sw ? -w.y : w.x;
+    const double im = sw ? w.x : w.y;
+    st_stream(a.out + q, make_double2(re * s, im * s));
   } else {
-    // half-length modes: alpha = 2^{1-n} {Re, -Im, -Re, Im}[popcount(x&z) mod 4] (real)
-    const uint32_t p0 = p & 3u, p1 = (p + 1u) & 3u;
+    // half-length modes: alpha = 2^{1-n} {Re, -Im, -Re, Im}[p mod 4] for z_t = 0 and the
+    // same with p + 1 for z_t = 1 (real)
     const double s = 2.0 * a.scale;
-    const double v0 = (p0 == 0) ? w.x : (p0 == 1) ? -w.y : (p0 == 2) ? -w.x : w.y;
-    const double v1 = (p1 == 0) ? w.x : (p1 == 1) ? -w.y : (p1 == 2) ? -w.x : w.y;
-    st_stream(a.out + q, make_double2(v0 * s, 0.0));
-    st_stream(a.out + (q + e.Dt), make_double2(v1 * s, 0.0));
+    const uint32_t p1 = p + 1u;
+    const double v0 = ((p & 1u) ? w.y : w.x) * ((((p ^ (p >> 1)) & 1u) != 0) ? -s : s);
+    const double v1 = ((p1 & 1u) ? w.y : w.x) * ((((p1 ^ (p1 >> 1)) & 1u) != 0) ? -s : s);
+    st_stream(a.out + q, make_double2(v0, 0.0));
+    st_stream(a.out + (q + dt), make_double2(v1, 0.0));
   }
 }
 
-template <int MODE, int NB, int J = 0>
+// All 2^NB registers of a unit, visited in Gray-code order so that consecutive outputs
+// differ in one z bit: q and p are updated with one add each (q += +-D[b], p += +-P[b]).
+template <int MODE, int NB, int I = 0>
+__device__ __forceinline__ void emit_gray(const DenseArgs& a, const EpiUnit<NB, (MODE >= 3)>& e,
+                                          const double2* w, uint32_t q, uint32_t p) {
+  if constexpr (I < (1 << NB)) {
+    constexpr int J = I ^ (I >> 1);
+    if constexpr (I > 0) {
+      constexpr int PREV = (I - 1) ^ ((I - 1) >> 1);
+      constexpr int B = __builtin_ctz(J ^ PREV);
+      if constexpr ((J >> B) & 1) {
+        q += e.D[B];
+        p += e.P[B];
+      } else {
+        q -= e.D[B];
+        p -= e.P[B];
+      }
+    }
+    emit_one<MODE>(a, q, p, e.Dt, w[J]);
+    emit_gray<MODE, NB, I + 1>(a, e, w, q, p);
+  }
+}
+
+template <int MODE, int NB>
 __device__ __forceinline__ void emit_all(const DenseArgs& a, const EpiUnit<NB, (MODE >= 3)>& e,
                                          const double2* w) {
-  if constexpr (J < (1 << NB)) {
-    emit_reg<MODE, NB, J>(a, e, w[J]);
-    emit_all<MODE, NB, J + 1>(a, e, w);
-  }
+  emit_gray<MODE, NB, 0>(a, e, w, e.q0, e.p0);
 }
 
 // Ticket order of dense_impl.cuh's decode_ticket, 32-bit, NA = NB = 2^M.

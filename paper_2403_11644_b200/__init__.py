@@ -11,7 +11,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libptdr.so")
+LIB_PATH = os.path.join(HERE, os.environ.get("PTDR_LIB_NAME", "libptdr.so"))
 
 STRUCTURES = {
     "general": 0,

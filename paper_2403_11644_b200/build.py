@@ -9,8 +9,9 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-BUILD = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "libptdr.so")
+BUILD = os.path.join(HERE, "_build_trace" if os.environ.get("PTDR_TRACE_BUILD") == "1" else "_build")
+TRACE_BUILD = os.environ.get("PTDR_TRACE_BUILD") == "1"  # developer timeline build
+LIB = os.path.join(HERE, "libptdr_trace.so" if TRACE_BUILD else "libptdr.so")
 ROOT = os.path.dirname(HERE)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
@@ -21,7 +22,7 @@ NVCC_FLAGS = [
     "-Xptxas", "-v",
     "--expt-relaxed-constexpr",
     f"-I{os.path.join(ROOT, 'include')}",
-]
+] + (["-DPTDR_ENABLE_TRACE=1"] if os.environ.get("PTDR_TRACE_BUILD") == "1" else [])
 
 
 def _deps():

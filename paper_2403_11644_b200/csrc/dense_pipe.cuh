@@ -46,8 +46,14 @@ __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
 // Debug timeline (PTDR_TRACE=1): CTA 0 records clock64 stamps of its first kTraceTiles
 // tiles into a.trace[tile * 16 + field].
 constexpr int kTraceTiles = 512;
+// Compiled in only with -DPTDR_ENABLE_TRACE=1 (PTDR_TRACE_BUILD=1 python build.py).
+#ifndef PTDR_ENABLE_TRACE
+#define PTDR_ENABLE_TRACE 0
+#endif
 __device__ __forceinline__ void trace_stamp(unsigned long long* tr, int k, int field) {
-  if (tr != nullptr && blockIdx.x == 0 && k < kTraceTiles) tr[k * 16 + field] = clock64();
+  if constexpr (PTDR_ENABLE_TRACE) {
+    if (tr != nullptr && blockIdx.x == 0 && k < kTraceTiles) tr[k * 16 + field] = clock64();
+  }
 }
 
 __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
@@ -183,7 +189,15 @@ struct PipeCfg {
   static constexpr int R = LT - XB;           // phase-A index bits (rows per phase-A tile = 2^R)
   static constexpr int GT = GW * 32;          // threads per group (= TE / 16)
   static constexpr int SIGD = 4;               // completion-signal slots per group
-  static constexpr int THREADS = 32 * (2 + NG * GW);  // warp 0 producer, warp 1 signaler
+  // Warpgroup 0 (warps 0-3): warp 0 producer, warp 1 signaler, warps 2-3 idle; they give
+  // their registers back (setmaxnreg) to the consumer warpgroups that follow.
+  static constexpr int THREADS = 32 * (4 + NG * GW);
+  static constexpr int CONS_THREADS = 32 * NG * GW;
+  static_assert(CONS_THREADS % 128 == 0, "consumer warps form whole warpgroups");
+  static constexpr int LAUNCH_REGS = ((65536 / THREADS) / 8) * 8 > 255 ? 248 : ((65536 / THREADS) / 8) * 8;
+  static constexpr int PROD_REGS = 40;
+  static constexpr int CONS_REGS_RAW = ((65536 - PROD_REGS * 128) / CONS_THREADS / 8) * 8;
+  static constexpr int CONS_REGS = CONS_REGS_RAW > 248 ? 248 : CONS_REGS_RAW;
   static constexpr int SMEM = NS * TB + 2048;
   static_assert(GT * 16 == TE, "16 elements per consumer thread");
 };
@@ -247,6 +261,9 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS>::THREADS, 1)
   }
   __syncthreads();
 
+  if (warp < 4) {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Cfg::PROD_REGS));
+
   // ------------------------------------------------------------------ producer
   if (warp == 0) {
     if (lane == 0) {
@@ -294,7 +311,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS>::THREADS, 1)
           }
         }
         trace_stamp(a.trace, k, 2);
-        if (a.trace && blockIdx.x == 0 && k < kTraceTiles) a.trace[k * 16 + 8] = phX;
+        if (PTDR_ENABLE_TRACE && a.trace && blockIdx.x == 0 && k < kTraceTiles) a.trace[k * 16 + 8] = phX;
         double2* dst = stage0 + (size_t)s * TE;
         meta[s].valid = 1;
         meta[s].phase = phX;
@@ -382,10 +399,16 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS>::THREADS, 1)
     }
     return;
   }
+  return;  // idle warps 2-3 of warpgroup 0
+  }  // warpgroup 0
+
+  // Consumer warpgroups: take the registers warpgroup 0 released.  (The setmaxnreg must
+  // head a region only consumers reach, or ptxas allocates the join at the low count.)
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(Cfg::CONS_REGS));
 
   // ------------------------------------------------------------------ consumers
-  const int g = (warp - 2) / GW;
-  const int gtid = threadIdx.x - 64 - g * GT;
+  const int g = (warp - 4) / GW;
+  const int gtid = threadIdx.x - 128 - g * GT;
   const int wig = gtid >> 5;  // warp index within the group
   // per-warp completion signal of the group's j-th tile (see the signaler)
   auto signal = [&](int j, unsigned* counter) {

@@ -1,6 +1,7 @@
 """Run one n=15 decomposition with PTDR_TRACE=1 and print the CTA-0 pipeline timeline."""
 import ctypes, os, sys
 os.environ["PTDR_TRACE"] = "1"
+os.environ["PTDR_LIB_NAME"] = "libptdr_trace.so"   # build with PTDR_TRACE_BUILD=1
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import numpy as np
 import torch

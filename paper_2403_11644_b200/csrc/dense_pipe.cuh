@@ -194,10 +194,15 @@ struct PipeCfg {
   static constexpr int THREADS = 32 * (4 + NG * GW);
   static constexpr int CONS_THREADS = 32 * NG * GW;
   static_assert(CONS_THREADS % 128 == 0, "consumer warps form whole warpgroups");
-  static constexpr int LAUNCH_REGS = ((65536 / THREADS) / 8) * 8 > 255 ? 248 : ((65536 / THREADS) / 8) * 8;
-  static constexpr int PROD_REGS = 40;
-  static constexpr int CONS_REGS_RAW = ((65536 - PROD_REGS * 128) / CONS_THREADS / 8) * 8;
+  // The CTA's register pool is fixed at launch (THREADS x LAUNCH_REGS, LAUNCH_REGS = what
+  // ptxas allocates under __launch_bounds__(THREADS, 1)); setmaxnreg.inc blocks until the
+  // pool can satisfy it, so PROD_REGS x 128 + CONS_REGS x CONS_THREADS must fit in it.
+  static constexpr int LAUNCH_REGS = ((65536 / THREADS) / 8) * 8 > 248 ? 248 : ((65536 / THREADS) / 8) * 8;
+  static constexpr int PROD_REGS = 32;
+  static constexpr int CONS_REGS_RAW = ((THREADS * LAUNCH_REGS - PROD_REGS * 128) / CONS_THREADS / 8) * 8;
   static constexpr int CONS_REGS = CONS_REGS_RAW > 248 ? 248 : CONS_REGS_RAW;
+  static_assert(CONS_REGS >= LAUNCH_REGS && PROD_REGS * 128 + CONS_REGS * CONS_THREADS <= THREADS * LAUNCH_REGS,
+                "register rebalancing must fit the launch-time pool");
   static constexpr int SMEM = NS * TB + 2048;
   static_assert(GT * 16 == TE, "16 elements per consumer thread");
 };

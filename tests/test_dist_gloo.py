@@ -1,0 +1,86 @@
+"""Multi-process host logic of the X-mask sharded path (CPU, gloo, world_size 2 and 4).
+
+The CUDA per-rank computation is tested on the GPU (test_gpu_configs.py emulates every
+rank's shard bitwise); here the exchange, the shard layout contract the kernels rely on,
+and the rank-local output ordering are checked with real torch.distributed processes.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n, result_q):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import ptdr_inputs
+        from paper_2403_11644_b200 import dist as pdist
+        from paper_2403_11644_b200 import xz_of
+
+        N = 1 << n
+        R = N // world
+        g = world.bit_length() - 1
+        rows = ptdr_inputs.dense(n, 4, "general", row0=rank * R, nrows=R)
+        # send layout [world][R][R]: block b = my rows x column block (rank ^ b)
+        send = np.stack([rows[:, (rank ^ b) * R:((rank ^ b) + 1) * R] for b in range(world)])
+        send_t = torch.from_numpy(np.ascontiguousarray(send))
+        recv = pdist.exchange(send_t)
+        local = recv.numpy().reshape(N, R)
+        A = ptdr_inputs.dense(n, 4, "general")
+        ok = True
+        # shard contract: A_local[i][c] = A[i][((i >> (n-g)) ^ rank) * R + c]
+        for i in range(N):
+            blk = (i >> (n - g)) ^ rank
+            ok &= np.array_equal(local[i], A[i, blk * R:(blk + 1) * R])
+        # every XOR-diagonal the rank owns is available locally:
+        # v_x[i] = A[i][i ^ x] = A_local[i][(i ^ x) & (R-1)] for x with x >> (n-g) == rank
+        for x in range(rank * R, (rank + 1) * R):
+            i = np.arange(N)
+            ok &= np.array_equal(local[i, (i ^ x) & (R - 1)], A[i, i ^ x])
+        # rank-local output order: global q of each local index, all with x_top == rank
+        qs = pdist.global_q_array(rank, n, world)
+        for q in qs[:: max(1, qs.size // 64)]:
+            x, _ = xz_of(int(q), n)
+            ok &= (x >> (n - g)) == rank
+        result_q.put((rank, bool(ok), qs.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 5), (4, 6)])
+def test_xmask_exchange_and_layout(world, n):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    allq = []
+    for rank, ok, qs in sorted(results):
+        assert ok, f"rank {rank} layout/contract check failed"
+        allq += qs
+    # the ranks' outputs tile the global q range exactly once
+    assert sorted(allq) == list(range(4 ** n))

@@ -302,7 +302,7 @@ def main():
                        f"X-mask shards over {world} GPUs, 1 NCCL all-to-all"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "peak_kind": peak_kind, "kernel": "dense_fused_kernel<8,7,0>",
+                         "peak_kind": peak_kind, "kernel": "dense_pipe_kernel (PTDR_PIPE_CFG=%s)" % os.environ.get("PTDR_PIPE_CFG", "default"),
                          "kernel_ms": kmean, "algorithmic_bytes_per_launch": alg_bytes},
             "hbm_gbs_step": 32 * coeffs_total / (ms_per_step * 1e-3) / 1e9 / world,
             "gpu_launches": launches,

@@ -45,6 +45,12 @@ cudaError_t launch_dense_pipe(int mode, const DenseArgs& a_in, const DensePlan& 
   if (p.kind != 2 || p.pipe_cfg == 0) return cudaErrorInvalidValue;
   DenseArgs a = a_in;
   a.L = p.L;
+  {
+    // developer override of the look-ahead (the workspace formula already covers any L:
+    // nslot is fixed by the byte budget, counters by the chunk count)
+    const char* el = getenv("PTDR_L");
+    if (el && atoi(el) > 0) a.L = atoi(el);
+  }
   a.nslot = p.nslot;
   a.slot_elems = p.slot_elems;
   PFN_cuTensorMapEncodeTiled_v12000 enc = encode_fn();

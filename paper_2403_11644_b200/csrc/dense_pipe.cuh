@@ -210,6 +210,13 @@ struct PipeCfg {
 // Fiber index of the phase-B tiles: phi encodes (u, zl) with bits [0,1]=u0,u1 [2,3]=zl0,zl1
 // [4, XB+2)=u2.. [XB+2, ..)=zl2.., so 2^k consecutive fibers form a (u, zl) square of
 // 4^(k/2) consecutive q (coalesced epilogue stores).
+// Phase-B tiles: consumers load the scratch straight into registers (L2 hits) instead of a
+// TMA bulk copy into the stage (saves 2 x 64 KiB of SMEM traffic per tile).
+#ifndef PTDR_B_DIRECT
+#define PTDR_B_DIRECT 1
+#endif
+constexpr bool kBDirect = PTDR_B_DIRECT != 0;
+
 template <int XB>
 __device__ __forceinline__ uint32_t phi_of(uint32_t u, uint32_t zl) {
   return (u & 3u) | ((zl & 3u) << 2) | ((u >> 2) << 4) | ((zl >> 2) << (XB + 2));
@@ -336,11 +343,18 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS>::THREADS, 1)
             tma_load_2d(dst + rb * W * W, &tmap, (int)(col0 * 2u), (int)row0, &full[s], pol);
           }
         } else {
-          // scratch written by other CTAs' generic stores, read by the async proxy
-          fence_proxy_async_global();
-          mbar_arrive_expect_tx(&full[s], (uint32_t)Cfg::TB);
-          const double2* src = a.scratch + (size_t)(chX % nslot) * a.slot_elems + ((size_t)tlX << LT);
-          bulk_load(dst, src, (uint32_t)Cfg::TB, &full[s], pol);
+          if constexpr (kBDirect) {
+            // phase-B consumers read the (L2-resident) scratch themselves; the stage is
+            // only their exchange buffer
+            mbar_arrive(&full[s]);
+          } else {
+            // scratch written by other CTAs' generic stores, read by the async proxy
+            fence_proxy_async_global();
+            mbar_arrive_expect_tx(&full[s], (uint32_t)Cfg::TB);
+            const double2* src =
+                a.scratch + (size_t)(chX % nslot) * a.slot_elems + ((size_t)tlX << LT);
+            bulk_load(dst, src, (uint32_t)Cfg::TB, &full[s], pol);
+          }
         }
         trace_stamp(a.trace, k, 3);
         ++k;
@@ -490,21 +504,33 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS>::THREADS, 1)
       signal(j, &doneA[chunk]);
       if (gtid == 0) trace_stamp(a.trace, k, 7);
     } else {
-      // ---- phase B: SMEM holds Y[tileB][ih][f] = [j][f]; WHT over j for FB fibers
+      // ---- phase B: tile Y[tileB][ih][f] = [j][f] (one contiguous 2^LT block of the
+      //      scratch); WHT over j for FB fibers
       const u64 x0 = a.x_base + ((u64)chunk << XB);
       const int t = HALF ? 63 - __clzll(x0) : 0;
       const int f = gtid % FB, jh = gtid / FB;
+      const double2* yt = Y + ((size_t)m.tile << LT);
+      // the tile's scratch lines are dead once every thread of the group has loaded them:
+      // drop them from L2 without write-back (the next writer of the slot waits for doneB
+      // of this chunk).  Called after a group barrier that follows all stage-1 loads.
+      auto discard_tile = [&]() {
+        if (a.discard) {
+          const char* yb = reinterpret_cast<const char*>(yt);
 #pragma unroll
-      for (int kk = 0; kk < 16; ++kk) v[kk] = S[(jh * 16 + kk) * FB + f];
-      if (a.discard) {
-        // this tile's scratch is dead once in SMEM: drop it from L2 without write-back
-        // (the next writer of the slot waits for doneB of this chunk)
-        char* yb = reinterpret_cast<char*>(Y + ((size_t)m.tile << LT));
+          for (int d = 0; d < Cfg::TB / 128 / GT; ++d) discard_l2(yb + ((size_t)(gtid + GT * d) << 7));
+        }
+      };
+      if constexpr (kBDirect) {
 #pragma unroll
-        for (int d = 0; d < Cfg::TB / 128 / GT; ++d) discard_l2(yb + ((size_t)(gtid + GT * d) << 7));
+        for (int kk = 0; kk < 16; ++kk) v[kk] = __ldcg(yt + (jh * 16 + kk) * FB + f);
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) v[kk] = S[(jh * 16 + kk) * FB + f];
       }
       wht_regs<4>(v);
       if constexpr (M == 4) {
+        named_bar_sync(bar_id, GT);
+        discard_tile();
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
@@ -518,6 +544,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS>::THREADS, 1)
 #pragma unroll
         for (int kk = 0; kk < 16; ++kk) S[(jh * 16 + kk) * FB + f] = v[kk];
         named_bar_sync(bar_id, GT);
+        discard_tile();
 #pragma unroll
         for (int p = 0; p < UB; ++p) {
           const int uu = gtid + GT * p;

@@ -213,7 +213,7 @@ struct PipeCfg {
 // Phase-B tiles: consumers load the scratch straight into registers (L2 hits) instead of a
 // TMA bulk copy into the stage (saves 2 x 64 KiB of SMEM traffic per tile).
 #ifndef PTDR_B_DIRECT
-#define PTDR_B_DIRECT 1
+#define PTDR_B_DIRECT 0
 #endif
 constexpr bool kBDirect = PTDR_B_DIRECT != 0;
 

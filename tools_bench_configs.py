@@ -1,0 +1,83 @@
+"""Time every BASELINE.json configuration on one GPU (CUDA events, device-resident input).
+
+Prints one JSON line per configuration with ms, coefficients/s and the achieved
+algorithmic HBM bandwidth (bytes per coefficient as in DESIGN.md section 7):
+dense 32 B, Hermitian/real-symmetric 24 B (upper triangle read + output), diagonal
+32 B, tridiagonal (band bytes + output bytes)."""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_2403_11644_b200 as ptdr  # noqa: E402
+
+PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+    os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6534.8
+
+
+def time_it(fn, iters=10, warm=3):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
+    for e0, e1 in ev:
+        e0.record()
+        fn()
+        e1.record()
+    torch.cuda.synchronize()
+    t = sorted(e0.elapsed_time(e1) for e0, e1 in ev)
+    return t[len(t) // 2]
+
+
+def dense(name, n, seed, variant):
+    A = ptdr.generate_dense(n, seed, variant, device="cuda")
+    out = torch.empty(1 << (2 * n), dtype=torch.complex128, device="cuda")
+    ws = ptdr.alloc_workspace(n, variant, 1, "cuda")
+    ms = time_it(lambda: ptdr.decompose(A, variant, out=out, workspace=ws))
+    coeffs = 1 << (2 * n)
+    bpc = 32 if variant == "general" else 24
+    gbs = bpc * coeffs / (ms * 1e-3) / 1e9
+    print(json.dumps({"config": name, "n": n, "structure": variant, "ms": ms,
+                      "coeffs_per_s": coeffs / (ms * 1e-3), "alg_bytes_per_coeff": bpc,
+                      "hbm_gbs": gbs, "frac_of_measured": gbs / PEAK}), flush=True)
+    del A, out, ws
+    torch.cuda.empty_cache()
+
+
+def band(name, n, seed, variant):
+    B = ptdr.generate_band(n, seed, variant, device="cuda")
+    out = torch.empty(ptdr.output_count(n, variant), dtype=torch.complex128, device="cuda")
+    ws = ptdr.alloc_workspace(n, variant, 1, "cuda")
+    ms = time_it(lambda: ptdr.decompose(B, variant, out=out, workspace=ws))
+    coeffs = out.numel()
+    alg = (B.numel() + out.numel()) * 16
+    gbs = alg / (ms * 1e-3) / 1e9
+    print(json.dumps({"config": name, "n": n, "structure": variant, "ms": ms,
+                      "coeffs_per_s": coeffs / (ms * 1e-3), "alg_bytes": alg, "hbm_gbs": gbs,
+                      "frac_of_measured": gbs / PEAK, "launches": ptdr.last_launch_count()}),
+          flush=True)
+    del B, out, ws
+    torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["all"]
+    if "all" in which or "small" in which:
+        dense("n6", 6, 0, "general")
+        dense("n10a", 10, 1, "general")
+        dense("n10b", 10, 1, "hermitian")
+    if "all" in which or "n13" in which:
+        dense("n13a", 13, 2, "hermitian")
+        dense("n13b", 13, 2, "real_symmetric")
+        dense("n13_general", 13, 2, "general")
+    if "all" in which or "band" in which:
+        band("n24tri", 24, 3, "tridiagonal")
+        band("n24diag", 24, 3, "diagonal")
+    if "all" in which or "big" in which:
+        dense("n15", 15, 4, "general")
+        dense("n15_hermitian", 15, 4, "hermitian")
+        dense("n16", 16, 4, "general")

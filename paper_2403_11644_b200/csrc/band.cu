@@ -39,130 +39,6 @@ struct FlatSt {
   }
 };
 
-template <int K>
-__global__ void __launch_bounds__(kThreads, 2) wht_pass_kernel(const double2* in, double2* out,
-                                                               u64 ntiles, int b0, double scale) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* S = reinterpret_cast<double2*>(smem_raw);
-  constexpr int F = kTileElems >> K;
-  for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    FlatLd<K> ld{in, tile * F, b0};
-    FlatSt<K> st{out, tile * F, b0, scale};
-    fiber_tile<K>(S, ld, st);
-    __syncthreads();
-  }
-}
-
-template <int K>
-static cudaError_t launch_pass(const double2* in, double2* out, u64 total, int b0, double scale,
-                               cudaStream_t st) {
-  static bool attr_done = false;  // idempotent attribute set; benign race
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(wht_pass_kernel<K>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kTileBytes);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
-  const u64 ntiles = total / kTileElems;
-  u64 grid = (u64)device_sm_count() * 2;
-  if (grid > ntiles) grid = ntiles;
-  wht_pass_kernel<K><<<(unsigned)grid, kThreads, kTileBytes, st>>>(in, out, ntiles, b0, scale);
-  return cudaGetLastError();
-}
-
-static cudaError_t launch_pass_k(int K, const double2* in, double2* out, u64 total, int b0,
-                                 double scale, cudaStream_t st) {
-  switch (K) {
-    case 4: return launch_pass<4>(in, out, total, b0, scale, st);
-    case 5: return launch_pass<5>(in, out, total, b0, scale, st);
-    case 6: return launch_pass<6>(in, out, total, b0, scale, st);
-    case 7: return launch_pass<7>(in, out, total, b0, scale, st);
-    case 8: return launch_pass<8>(in, out, total, b0, scale, st);
-    default: return cudaErrorInvalidValue;
-  }
-}
-
-// WHT over the low `lambda` bits (lambda >= 13) of `total` contiguous elements
-// (a batch of total/2^lambda vectors), in -> out (out may equal in), scaled.
-static cudaError_t run_passes(const double2* in, double2* out, u64 total, int lambda,
-                              double scale, cudaStream_t st, int* nl) {
-  const int np = (lambda + 7) / 8;
-  int b0 = 0;
-  for (int p = 0; p < np; ++p) {
-    const int K = (lambda - b0) / (np - p);
-    cudaError_t e = launch_pass_k(K, p == 0 ? in : out, out, total, b0,
-                                  p == np - 1 ? scale : 1.0, st);
-    if (e != cudaSuccess) return e;
-    *nl += 1;
-    b0 += K;
-  }
-  return cudaSuccess;
-}
-
-// ---- small WHTs (length <= 4096) entirely in SMEM, one CTA per vector --------------
-// mode 0: one vector of length 2^lam at in/out offset 0, scaled.
-// mode 1: tridiagonal P/M segments t = tmin + blockIdx.x/2 of a size-2^n problem,
-//         in place in `out` (the PM workspace), unscaled.
-__global__ void __launch_bounds__(kThreads) wht_small_kernel(const double2* in, double2* out,
-                                                             int mode, int n, int lam_or_tmin,
-                                                             double scale) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* S = reinterpret_cast<double2*>(smem_raw);
-  int lam;
-  u64 off;
-  if (mode == 0) {
-    lam = lam_or_tmin;
-    off = 0;
-  } else {
-    const int t = lam_or_tmin + (int)(blockIdx.x >> 1);
-    lam = n - t - 1;
-    const u64 N = 1ull << n;
-    off = 2ull * (N - (N >> t)) + ((u64)(blockIdx.x & 1) << lam);
-    in = out;
-  }
-  const int len = 1 << lam;
-  for (int i = threadIdx.x; i < len; i += blockDim.x) S[i] = ld_l2(in + off + i);
-  for (int s = 0; s < lam; ++s) {
-    __syncthreads();
-    for (int p = threadIdx.x; p < len / 2; p += blockDim.x) {
-      const int lo = p & ((1 << s) - 1);
-      const int i0 = ((p >> s) << (s + 1)) | lo;
-      const int i1 = i0 | (1 << s);
-      const double2 a = S[i0], b = S[i1];
-      S[i0] = cadd(a, b);
-      S[i1] = csub(a, b);
-    }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < len; i += blockDim.x) {
-    const double2 v = S[i];
-    out[off + i] = make_double2(v.x * scale, v.y * scale);
-  }
-}
-
-static cudaError_t launch_small(const double2* in, double2* out, int mode, int n, int arg,
-                                double scale, unsigned blocks, cudaStream_t st) {
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(wht_small_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kTileBytes);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
-  wht_small_kernel<<<blocks, kThreads, kTileBytes, st>>>(in, out, mode, n, arg, scale);
-  return cudaGetLastError();
-}
-
-// out[0..2^n) = 2^-n WHT(in[0..2^n))
-static cudaError_t wht_vector(const double2* in, double2* out, int n, cudaStream_t st, int* nl) {
-  const double scale = ldexp(1.0, -n);
-  if (n <= 12) {
-    *nl += 1;
-    return launch_small(in, out, 0, n, n, scale, 1, st);
-  }
-  return run_passes(in, out, 1ull << n, n, scale, st, nl);
-}
-
 // ---- tridiagonal split: (S_t, U_t) -> (S_t + U_t, S_t - U_t) compacted per t --------
 __global__ void tridiag_split_kernel(const double2* band, double2* PM, int n) {
   const u64 N = 1ull << n;
@@ -203,6 +79,152 @@ __global__ void tridiag_expand_kernel(const double2* PM, double2* out, int n, do
   }
 }
 
+// ---- multi-segment WHT passes ---------------------------------------------------------
+// One launch runs pass p (index bits [8p, 8p+8)) for every segment that needs it: the x=0
+// vector (main diagonal) and the tridiagonal P/M segments.  Segments with lambda <= 12 are
+// transformed whole, one vector per tile, in pass 0.  Tiles of all segments are handed out
+// grid-stride; each tile dispatches its fibre length K at run time.
+struct SegPass {
+  const double2* in;
+  double2* out;
+  unsigned long long first_tile;  // prefix sum of tiles over the table
+  int b0;                         // first index bit of this pass
+  int K;                          // bits transformed in this pass (flat tiles)
+  int small;                      // 1: whole-vector WHT of 2^small_lam elements per tile
+  int small_lam;
+  double scale;
+};
+constexpr int kMaxSeg = 40;
+struct SegPassTable {
+  int count;
+  unsigned long long total_tiles;
+  SegPass s[kMaxSeg];
+};
+
+__device__ __forceinline__ void small_wht_tile(double2* S, const double2* in, double2* out, int lam,
+                                               double scale) {
+  const int len = 1 << lam;
+  for (int i = threadIdx.x; i < len; i += blockDim.x) S[i] = ld_l2(in + i);
+  for (int sb = 0; sb < lam; ++sb) {
+    __syncthreads();
+    for (int p = threadIdx.x; p < len / 2; p += blockDim.x) {
+      const int lo = p & ((1 << sb) - 1);
+      const int i0 = ((p >> sb) << (sb + 1)) | lo;
+      const int i1 = i0 | (1 << sb);
+      const double2 a = S[i0], b = S[i1];
+      S[i0] = cadd(a, b);
+      S[i1] = csub(a, b);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < len; i += blockDim.x) {
+    const double2 v = S[i];
+    st_l2(out + i, make_double2(v.x * scale, v.y * scale));
+  }
+}
+
+template <int K>
+__device__ __forceinline__ void flat_tile(double2* S, const SegPass& sp, u64 local) {
+  constexpr int F = kTileElems >> K;
+  FlatLd<K> ld{sp.in, local * F, sp.b0};
+  FlatSt<K> st{sp.out, local * F, sp.b0, sp.scale};
+  fiber_tile<K>(S, ld, st);
+}
+
+__global__ void __launch_bounds__(kThreads, 2) seg_pass_kernel(const __grid_constant__ SegPassTable T) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* S = reinterpret_cast<double2*>(smem_raw);
+  for (u64 tile = blockIdx.x; tile < T.total_tiles; tile += gridDim.x) {
+    int i = 0;
+    while (i + 1 < T.count && T.s[i + 1].first_tile <= tile) ++i;
+    const SegPass& sp = T.s[i];
+    const u64 local = tile - sp.first_tile;
+    if (sp.small) {
+      const u64 off = local << sp.small_lam;
+      small_wht_tile(S, sp.in + off, sp.out + off, sp.small_lam, sp.scale);
+    } else {
+      switch (sp.K) {
+        case 1: flat_tile<1>(S, sp, local); break;
+        case 2: flat_tile<2>(S, sp, local); break;
+        case 3: flat_tile<3>(S, sp, local); break;
+        case 4: flat_tile<4>(S, sp, local); break;
+        case 5: flat_tile<5>(S, sp, local); break;
+        case 6: flat_tile<6>(S, sp, local); break;
+        case 7: flat_tile<7>(S, sp, local); break;
+        default: flat_tile<8>(S, sp, local); break;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// A vector family for the pass planner: `count` contiguous vectors of 2^lam elements.
+struct WhtFamily {
+  const double2* in;  // input of pass 0
+  double2* out;       // output of every pass (later passes in place)
+  int lam;
+  u64 count;
+  double scale;       // applied on the last pass
+};
+
+// Runs all passes for all families (at most 3 launches for lam <= 24).
+static cudaError_t run_families(const WhtFamily* fam, int nfam, cudaStream_t st, int* nl) {
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(seg_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kTileBytes);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  int maxlam = 0;
+  for (int f = 0; f < nfam; ++f) maxlam = fam[f].lam > maxlam ? fam[f].lam : maxlam;
+  const int npass = maxlam <= 12 ? 1 : (maxlam + 7) / 8;
+  for (int p = 0; p < npass; ++p) {
+    SegPassTable T;
+    T.count = 0;
+    u64 tiles = 0;
+    for (int f = 0; f < nfam; ++f) {
+      const WhtFamily& w = fam[f];
+      if (w.count == 0) continue;
+      SegPass sp{};
+      if (w.lam == 0 && w.in == w.out && w.scale == 1.0) continue;  // length-1 WHT: identity
+      if (w.lam <= 12) {
+        if (p != 0) continue;
+        sp.small = 1;
+        sp.in = w.in;
+        sp.out = w.out;
+        sp.small_lam = w.lam;
+        sp.scale = w.scale;
+        sp.first_tile = tiles;
+        tiles += w.count;
+      } else {
+        const int b0 = 8 * p;
+        if (b0 >= w.lam) continue;
+        const int K = (w.lam - b0) < 8 ? (w.lam - b0) : 8;
+        const bool last = b0 + K >= w.lam;
+        sp.in = p == 0 ? w.in : w.out;
+        sp.out = w.out;
+        sp.b0 = b0;
+        sp.K = K;
+        sp.scale = last ? w.scale : 1.0;
+        sp.first_tile = tiles;
+        tiles += (w.count << w.lam) / kTileElems;
+      }
+      if (T.count >= kMaxSeg) return cudaErrorInvalidValue;
+      T.s[T.count++] = sp;
+    }
+    if (T.count == 0) continue;
+    T.total_tiles = tiles;
+    u64 grid = (u64)device_sm_count() * 2;
+    if (grid > tiles) grid = tiles;
+    seg_pass_kernel<<<(unsigned)grid, kThreads, kTileBytes, st>>>(T);
+    *nl += 1;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 size_t band_workspace_bytes(int n, int structure) {
   if (structure == 4) return (size_t)2 * ((size_t)1 << n) * 16;  // P/M segments
   return 0;
@@ -211,12 +233,15 @@ size_t band_workspace_bytes(int n, int structure) {
 cudaError_t launch_band(const double2* A, double2* out, int n, int structure, void* ws,
                         cudaStream_t st, int* nl) {
   const u64 N = 1ull << n;
-  if (structure == 3) return wht_vector(A, out, n, st, nl);
+  const double scale = ldexp(1.0, -n);
+  if (structure == 3) {
+    WhtFamily f{A, out, n, 1, scale};
+    return run_families(&f, 1, st, nl);
+  }
   // TRIDIAGONAL: A = [sub | main | sup]
-  cudaError_t e = wht_vector(A + N, out, n, st, nl);  // block 0 (x = 0)
-  if (e != cudaSuccess) return e;
   double2* PM = reinterpret_cast<double2*>(ws);
   const int sms = device_sm_count();
+  cudaError_t e;
   {
     u64 blocks = (N + 255) / 256;
     if (blocks > (u64)sms * 16) blocks = (u64)sms * 16;
@@ -224,21 +249,21 @@ cudaError_t launch_band(const double2* A, double2* out, int n, int structure, vo
     *nl += 1;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  int tmin = n - 13 > 0 ? n - 13 : 0;  // segments with lambda = n-t-1 <= 12 done in SMEM
-  for (int t = 0; t < tmin; ++t) {
+  // block 0 (x = 0): WHT(main) scaled; blocks t+1: P_t / M_t (two vectors of 2^(n-t-1))
+  WhtFamily fam[kMaxSeg];
+  int nf = 0;
+  fam[nf++] = WhtFamily{A + N, out, n, 1, scale};
+  for (int t = 0; t < n; ++t) {
     const int lam = n - t - 1;
     const u64 seg = N - (N >> t);
-    e = run_passes(PM + 2 * seg, PM + 2 * seg, 2ull << lam, lam, 1.0, st, nl);
-    if (e != cudaSuccess) return e;
+    fam[nf++] = WhtFamily{PM + 2 * seg, PM + 2 * seg, lam, 2, 1.0};
   }
-  e = launch_small(nullptr, PM, 1, n, tmin, 1.0, (unsigned)(2 * (n - tmin)), st);
-  *nl += 1;
-  if (e != cudaSuccess) return e;
+  if ((e = run_families(fam, nf, st, nl)) != cudaSuccess) return e;
   {
     const u64 total = (u64)n * N;
     u64 blocks = (total + 255) / 256;
     if (blocks > (u64)sms * 32) blocks = (u64)sms * 32;
-    tridiag_expand_kernel<<<(unsigned)blocks, 256, 0, st>>>(PM, out, n, ldexp(1.0, -n));
+    tridiag_expand_kernel<<<(unsigned)blocks, 256, 0, st>>>(PM, out, n, scale);
     *nl += 1;
     e = cudaGetLastError();
   }

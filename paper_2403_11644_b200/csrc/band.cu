@@ -40,43 +40,80 @@ struct FlatSt {
 };
 
 // ---- tridiagonal split: (S_t, U_t) -> (S_t + U_t, S_t - U_t) compacted per t --------
+// One thread per super-diagonal index i (coalesced reads of sup[i] and sub[i+1]): i has t
+// trailing ones, b_h = i with h = i >> (t+1), S_t[h] = sup[i], U_t[h] = sub[i+1].
 __global__ void tridiag_split_kernel(const double2* band, double2* PM, int n) {
   const u64 N = 1ull << n;
   const double2* sub = band;
   const double2* sup = band + 2 * N;
-  for (u64 e = (u64)blockIdx.x * blockDim.x + threadIdx.x; e < N - 1;
-       e += (u64)gridDim.x * blockDim.x) {
-    const int t = __clzll(~(e << (64 - n)));  // leading ones of the n-bit e
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < N - 1;
+       i += (u64)gridDim.x * blockDim.x) {
+    const int t = __ffsll((long long)~i) - 1;  // trailing ones of i (i < N-1 so t <= n-1)
     const int lam = n - t - 1;
     const u64 seg = N - (N >> t);
-    const u64 h = e - seg;
-    const u64 b = (h << (t + 1)) + (1ull << t) - 1ull;
-    const double2 s = sup[b];
-    const double2 u = sub[b + 1];
+    const u64 h = i >> (t + 1);
+    const double2 s = ld_stream(sup + i);
+    const double2 u = ld_stream(sub + i + 1);
     PM[2 * seg + h] = cadd(s, u);
     PM[2 * seg + (1ull << lam) + h] = csub(s, u);
   }
 }
 
-// ---- tridiagonal expansion into blocks 1..n ----------------------------------------
-__global__ void tridiag_expand_kernel(const double2* PM, double2* out, int n, double scale) {
+// ---- tridiagonal expansion into blocks 1..n (write-bound) ------------------------------
+// Each thread writes 8 outputs of one block at z = base + lane + 32 k (512 B per warp store);
+// the P/M values (reused 2^(t+1) times) come through the read-only cache.
+__global__ void __launch_bounds__(256) tridiag_expand_kernel(const double2* PM, double2* out, int n,
+                                                             double scale) {
   const u64 N = 1ull << n;
-  const u64 total = (u64)n * N;
-  for (u64 id = (u64)blockIdx.x * blockDim.x + threadIdx.x; id < total;
-       id += (u64)gridDim.x * blockDim.x) {
-    const int t = (int)(id >> n);
-    const u64 z = id & (N - 1);
+  const u64 groups = ((u64)n * N) >> 8;  // 256 outputs per warp-group of 8 stores
+  const int lane = threadIdx.x & 31;
+  for (u64 gidx = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; gidx < groups;
+       gidx += ((u64)gridDim.x * blockDim.x) >> 5) {
+    const u64 id0 = gidx << 8;
+    const int t = (int)(id0 >> n);
     const int lam = n - t - 1;
     const u64 seg = N - (N >> t);
-    const u64 zl = z & ((2ull << t) - 1ull);
-    const u64 zh = z >> (t + 1);
-    const int s1 = __popcll(z & ((1ull << t) - 1ull)) & 1;
-    const int s2 = (int)((z >> t) & 1ull);
-    double2 w = ld_l2(PM + 2 * seg + (s1 == s2 ? 0ull : (1ull << lam)) + zh);
-    if (s1) w = make_double2(-w.x, -w.y);
-    const double2 c = rot_ipow(w, __popcll(zl));
-    st_stream(out + N + id, make_double2(c.x * scale, c.y * scale));
+    const double2* Pt = PM + 2 * seg;
+    const double2* Mt = Pt + (1ull << lam);
+    double2 w[8];
+    int ph[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const u64 z = (id0 & (N - 1)) + (u64)lane + 32ull * k;
+      const u64 zl = z & ((2ull << t) - 1ull);
+      const u64 zh = z >> (t + 1);
+      const int s1 = __popcll(z & ((1ull << t) - 1ull)) & 1;
+      const int s2 = (int)((z >> t) & 1ull);
+      w[k] = __ldg(((s1 == s2) ? Pt : Mt) + zh);
+      ph[k] = __popcll(zl) + 2 * s1;  // i^{popcount(zl)} * (-1)^{s1}
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const bool sw = (ph[k] & 1) != 0;
+      const double sc = (ph[k] & 2) ? -scale : scale;
+      const double re = sw ? -w[k].y : w[k].x;
+      const double im = sw ? w[k].x : w[k].y;
+      st_stream(out + N + id0 + (u64)lane + 32ull * k, make_double2(re * sc, im * sc));
+    }
   }
+}
+
+// Small n (2^n < 256): one output per thread.
+__global__ void tridiag_expand_small_kernel(const double2* PM, double2* out, int n, double scale) {
+  const u64 N = 1ull << n;
+  const u64 id = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= (u64)n * N) return;
+  const int t = (int)(id >> n);
+  const u64 z = id & (N - 1);
+  const int lam = n - t - 1;
+  const u64 seg = N - (N >> t);
+  const u64 zl = z & ((2ull << t) - 1ull);
+  const int s1 = __popcll(z & ((1ull << t) - 1ull)) & 1;
+  const int s2 = (int)((z >> t) & 1ull);
+  const double2 w = PM[2 * seg + (s1 == s2 ? 0ull : (1ull << lam)) + (z >> (t + 1))];
+  const int ph = __popcll(zl) + 2 * s1;
+  const double2 c = rot_ipow(w, ph);
+  out[N + id] = make_double2(c.x * scale, c.y * scale);
 }
 
 // ---- multi-segment WHT passes ---------------------------------------------------------
@@ -244,7 +281,7 @@ cudaError_t launch_band(const double2* A, double2* out, int n, int structure, vo
   cudaError_t e;
   {
     u64 blocks = (N + 255) / 256;
-    if (blocks > (u64)sms * 16) blocks = (u64)sms * 16;
+    if (blocks > (u64)sms * 32) blocks = (u64)sms * 32;
     tridiag_split_kernel<<<(unsigned)blocks, 256, 0, st>>>(A, PM, n);
     *nl += 1;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -261,9 +298,13 @@ cudaError_t launch_band(const double2* A, double2* out, int n, int structure, vo
   if ((e = run_families(fam, nf, st, nl)) != cudaSuccess) return e;
   {
     const u64 total = (u64)n * N;
-    u64 blocks = (total + 255) / 256;
-    if (blocks > (u64)sms * 32) blocks = (u64)sms * 32;
-    tridiag_expand_kernel<<<(unsigned)blocks, 256, 0, st>>>(PM, out, n, scale);
+    if (N >= 256) {
+      u64 blocks = (total / 8 + 255) / 256;
+      if (blocks > (u64)sms * 16) blocks = (u64)sms * 16;
+      tridiag_expand_kernel<<<(unsigned)blocks, 256, 0, st>>>(PM, out, n, scale);
+    } else {
+      tridiag_expand_small_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(PM, out, n, scale);
+    }
     *nl += 1;
     e = cudaGetLastError();
   }

@@ -9,9 +9,13 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-BUILD = os.path.join(HERE, "_build_trace" if os.environ.get("PTDR_TRACE_BUILD") == "1" else "_build")
 TRACE_BUILD = os.environ.get("PTDR_TRACE_BUILD") == "1"  # developer timeline build
-LIB = os.path.join(HERE, "libptdr_trace.so" if TRACE_BUILD else "libptdr.so")
+# Developer diagnostic builds: PTDR_DIAG_BUILD=<bits> compiles dense_pipe.cuh with
+# -DPTDR_DIAG=<bits> into libptdr_diag<bits>.so (never loaded by the product path).
+DIAG_BUILD = os.environ.get("PTDR_DIAG_BUILD", "")
+_VARIANT = "_trace" if TRACE_BUILD else (f"_diag{DIAG_BUILD}" if DIAG_BUILD else "")
+BUILD = os.path.join(HERE, "_build" + _VARIANT)
+LIB = os.path.join(HERE, f"libptdr{_VARIANT}.so")
 ROOT = os.path.dirname(HERE)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
@@ -22,7 +26,7 @@ NVCC_FLAGS = [
     "-Xptxas", "-v",
     "--expt-relaxed-constexpr",
     f"-I{os.path.join(ROOT, 'include')}",
-] + (["-DPTDR_ENABLE_TRACE=1"] if os.environ.get("PTDR_TRACE_BUILD") == "1" else [])
+] + (["-DPTDR_ENABLE_TRACE=1"] if TRACE_BUILD else []) + ([f"-DPTDR_DIAG={DIAG_BUILD}"] if DIAG_BUILD else [])
 
 
 def _deps():

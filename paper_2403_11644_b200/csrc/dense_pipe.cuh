@@ -28,6 +28,15 @@
 
 namespace ptdr {
 
+// Developer diagnostics (PTDR_DIAG_BUILD=<bits>; never in the product library):
+//   bit 0: phase B computes but does not store the output (isolates the read side);
+//   bit 1: phase-A TMA loads come from the first 256 rows of A (L2-resident: isolates
+//          the write side).
+#ifndef PTDR_DIAG
+#define PTDR_DIAG 0
+#endif
+constexpr int kDiag = PTDR_DIAG;
+
 struct TileMeta {
   int valid, phase, tile, seq;
   unsigned chunk, pad0, pad1, pad2;
@@ -117,7 +126,11 @@ __device__ __forceinline__ void emit_one(const DenseArgs& a, uint32_t q, uint32_
     const double s = (p & 2u) ? -a.scale : a.scale;
     const double re = sw ? -w.y : w.x;
     const double im = sw ? w.x : w.y;
-    st_stream(a.out + q, make_double2(re * s, im * s));
+    if constexpr ((kDiag & 1) != 0) {
+      if (re == 12345.678) st_stream(a.out + q, make_double2(re * s, im * s));  // keeps the math live
+    } else {
+      st_stream(a.out + q, make_double2(re * s, im * s));
+    }
   } else {
     // half-length modes: alpha = 2^{1-n} {Re, -Im, -Re, Im}[p mod 4] for z_t = 0 and the
     // same with p + 1 for z_t = 1 (real)
@@ -338,7 +351,8 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS>::THREADS, 1)
 #pragma unroll
           for (int rb = 0; rb < (1 << (R - XB)); ++rb) {
             const uint32_t iv0 = (tlX << R) + (uint32_t)rb * W;
-            const uint32_t row0 = HALF ? insert0_32(iv0, t) : iv0;
+            uint32_t row0 = HALF ? insert0_32(iv0, t) : iv0;
+            if constexpr ((kDiag & 2) != 0) row0 &= 255u;
             const uint32_t col0 = (row0 ^ x0) & cm;
             tma_load_2d(dst + rb * W * W, &tmap, (int)(col0 * 2u), (int)row0, &full[s], pol);
           }

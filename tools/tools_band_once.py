@@ -1,5 +1,5 @@
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2403_11644_b200 as ptdr
 v = sys.argv[1] if len(sys.argv) > 1 else "tridiagonal"

@@ -2,7 +2,7 @@
 import ctypes, os, sys
 os.environ["PTDR_TRACE"] = "1"
 os.environ["PTDR_LIB_NAME"] = "libptdr_trace.so"   # build with PTDR_TRACE_BUILD=1
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 import paper_2403_11644_b200 as ptdr

@@ -39,7 +39,7 @@ def _args():
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--n", type=int, default=15)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--e2e-steps", type=int, default=4)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -312,8 +312,11 @@ def main():
         }
 
     # ---- end to end through the public host API (rank 0, N == 1) ------------------------
+    # HostPlan (ptdr_plan_*): every step uploads the step's matrix from pinned host memory,
+    # decomposes it on the device and downloads all 4^n coefficients into pinned host
+    # memory; with two device slots the upload of step k+1 overlaps the download of step k.
     if world == 1 and not a.no_e2e:
-        del out, ws
+        del ws
         torch.cuda.empty_cache()
         import numpy as np
 
@@ -321,20 +324,28 @@ def main():
         host_in.copy_(A)
         del A
         torch.cuda.empty_cache()
-        host_out = torch.empty(coeffs_total, dtype=torch.complex128, pin_memory=True)
-        hin, hout = host_in.numpy(), host_out.numpy()
-        ptdr.decompose_host(hin, "general", hout)  # warm-up
-        times = []
-        for _ in range(max(1, a.e2e_steps)):
+        host_out = [torch.empty(coeffs_total, dtype=torch.complex128, pin_memory=True) for _ in range(2)]
+        hin = host_in.numpy()
+        houts = [h.numpy() for h in host_out]
+        K = max(2, a.e2e_steps)
+        with ptdr.HostPlan(n, "general", depth=2) as plan:
+            plan.decompose_async(hin, houts[0])          # warm-up (allocations, module load)
+            plan.wait()
             s0 = time.perf_counter()
-            ptdr.decompose_host(hin, "general", hout)
-            times.append(time.perf_counter() - s0)
-        e2e_s = statistics.median(times)
+            for k in range(K):
+                plan.decompose_async(hin, houts[k % 2])
+            plan.wait()
+            e2e_s = (time.perf_counter() - s0) / K
+            e2e_launches = plan.launch_count() * K
+        # the streamed result must equal the device-timed one (same kernels, same input)
+        idx = torch.from_numpy(np.random.default_rng(7).integers(0, coeffs_total, 1 << 16))
+        same = bool(torch.equal(host_out[(K - 1) % 2][idx], out[idx.to(dev)].cpu()))
         line["e2e"] = {"value": coeffs_total / e2e_s, "unit": UNIT,
                        "h2d_bytes_per_step": 16 * coeffs_total, "d2h_bytes_per_step": 16 * coeffs_total,
-                       "steps": len(times), "s_per_step": e2e_s,
-                       "api": "ptdr_decompose_host (pinned host buffers)"}
-        del host_in, host_out
+                       "steps": K, "s_per_step": e2e_s, "gpu_launches": e2e_launches,
+                       "matches_device_result": same,
+                       "api": "ptdr_plan_decompose_host_async, depth 2 (pinned host buffers)"}
+        del host_in, host_out, hin, houts
 
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(n, a.cpu_seconds)

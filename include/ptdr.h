@@ -141,6 +141,33 @@ ptdr_status ptdr_generate_band_async(int n, uint64_t seed, int variant, ptdr_c12
 ptdr_status ptdr_generate_sendblocks_async(int n, uint64_t seed, int rank, int world,
                                            ptdr_c128* send, void* stream);
 
+/* ---- Host plans: streaming decomposition of matrices held in HOST memory ----------------
+ * A plan owns `depth` (1..4) slots of device buffers for one (n, structure) -- input,
+ * output and workspace, ~2 x 16 x 4^n bytes per slot for dense structures -- plus three
+ * CUDA streams (host->device copy, kernels, device->host copy).  Every step of the
+ * decomposition runs on the device exactly as in ptdr_decompose_async; the plan only
+ * orders the copies around it.  Call k uses slot k mod depth: its H2D waits until the
+ * slot's previous D2H has finished, its kernels wait for its H2D, its D2H for its kernels.
+ * With depth >= 2 the H2D of one call overlaps the D2H of the previous one (full-duplex
+ * PCIe), so a sequence of matrices streams at the bidirectional copy rate.
+ * Host buffers should be pinned (cudaHostAlloc / torch pin_memory); pageable buffers
+ * work but the copies then serialise.  The caller must not modify A_host or read
+ * out_host of a call until ptdr_plan_wait() has returned after it.  A plan is used on
+ * the device that was current at creation (EINVAL otherwise) and by one host thread at
+ * a time.  Errors: EINVAL (bad n / structure / depth / pointer), ENOMEM (device
+ * allocation), ECUDA. */
+typedef struct ptdr_plan_s* ptdr_plan;
+ptdr_status ptdr_plan_create(int n, int structure, int depth, ptdr_plan* plan);
+/* Enqueue one decomposition: out_host <- decomposition of A_host (returns immediately). */
+ptdr_status ptdr_plan_decompose_host_async(ptdr_plan plan, const ptdr_c128* A_host,
+                                           ptdr_c128* out_host);
+/* Block until every call enqueued on the plan has completed (copies included). */
+ptdr_status ptdr_plan_wait(ptdr_plan plan);
+/* Kernel launches enqueued by the plan's most recent call. */
+int ptdr_plan_launch_count(ptdr_plan plan);
+/* Waits for outstanding work, then frees the plan's buffers and streams (NULL: no-op). */
+ptdr_status ptdr_plan_destroy(ptdr_plan plan);
+
 /* Number of kernel launches the last successful call on this host thread enqueued
  * (used by bench.py's gpu_launches count). */
 int ptdr_last_launch_count(void);

@@ -61,6 +61,15 @@ def lib():
         L.ptdr_last_error.restype = ctypes.c_char_p
         L.ptdr_last_launch_count.restype = i32
         L.ptdr_version.restype = i32
+        L.ptdr_plan_create.argtypes = [i32, i32, i32, ctypes.POINTER(vp)]
+        L.ptdr_plan_decompose_host_async.argtypes = [vp, vp, vp]
+        L.ptdr_plan_wait.argtypes = [vp]
+        L.ptdr_plan_launch_count.argtypes = [vp]
+        L.ptdr_plan_launch_count.restype = i32
+        L.ptdr_plan_destroy.argtypes = [vp]
+        for name in ("ptdr_plan_create", "ptdr_plan_decompose_host_async", "ptdr_plan_wait",
+                     "ptdr_plan_destroy"):
+            getattr(L, name).restype = i32
         for name in ("ptdr_decompose", "ptdr_decompose_async", "ptdr_decompose_host",
                      "ptdr_decompose_xshard_async", "ptdr_generate_dense_async",
                      "ptdr_generate_band_async", "ptdr_generate_sendblocks_async"):
@@ -182,6 +191,59 @@ def decompose_host(A_host, structure="general", out_host=None):
                                    ctypes.c_void_p(o.ctypes.data))
     _check(st, "ptdr_decompose_host")
     return out_host
+
+
+class HostPlan:
+    """Streaming decomposition of host-resident matrices (ptdr_plan_*, include/ptdr.h).
+
+    ``depth`` device buffer slots; with depth >= 2 the upload of one matrix overlaps the
+    download of the previous result.  Host arrays must stay untouched until ``wait()``."""
+
+    def __init__(self, n: int, structure="general", depth: int = 2):
+        self.n, self.structure, self.depth = n, _structure(structure), depth
+        h = ctypes.c_void_p()
+        _check(lib().ptdr_plan_create(n, self.structure, depth, ctypes.byref(h)), "ptdr_plan_create")
+        self._h = h
+
+    @staticmethod
+    def _np(x):
+        import numpy as np
+
+        a = x if isinstance(x, np.ndarray) else x.numpy()
+        if a.dtype != np.complex128 or not a.flags.c_contiguous:
+            raise TypeError("host buffers must be C-contiguous complex128")
+        return a
+
+    def decompose_async(self, A_host, out_host):
+        a, o = self._np(A_host), self._np(out_host)
+        if a.size != input_count(self.n, self.structure) or o.size != output_count(self.n, self.structure):
+            raise ValueError("host buffer sizes do not match the plan")
+        _check(lib().ptdr_plan_decompose_host_async(self._h, ctypes.c_void_p(a.ctypes.data),
+                                                    ctypes.c_void_p(o.ctypes.data)),
+               "ptdr_plan_decompose_host_async")
+
+    def wait(self):
+        _check(lib().ptdr_plan_wait(self._h), "ptdr_plan_wait")
+
+    def launch_count(self) -> int:
+        return lib().ptdr_plan_launch_count(self._h)
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            _check(lib().ptdr_plan_destroy(self._h), "ptdr_plan_destroy")
+        self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def decompose_xshard(A_local, n: int, rank: int, world: int, out=None, workspace=None,

@@ -42,6 +42,9 @@ static ptdr_status cuda_fail(cudaError_t e, const char* where) {
   g_last_error = std::string(where) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
   return PTDR_ECUDA;
 }
+// error reporting for plan.cu (same thread-local error string)
+ptdr_status plan_fail(ptdr_status s, const char* msg) { return fail(s, msg); }
+ptdr_status plan_cuda_fail(cudaError_t e, const char* where) { return cuda_fail(e, where); }
 
 static bool is_dense(int s) { return s >= PTDR_GENERAL && s <= PTDR_REAL_SYMMETRIC; }
 static bool is_band(int s) { return s == PTDR_DIAGONAL || s == PTDR_TRIDIAGONAL; }

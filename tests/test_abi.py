@@ -96,3 +96,16 @@ def test_q_helpers_roundtrip():
             ch = s[n - 1 - l]
             assert ((x >> l) & 1) == (ch in "XY")
             assert ((z >> l) & 1) == (ch in "YZ")
+
+
+def test_plan_validation_without_gpu(L):
+    """ptdr_plan_create validates its arguments before touching the device."""
+    h = ctypes.c_void_p()
+    assert L.ptdr_plan_create(0, 0, 2, ctypes.byref(h)) == ptdr.PTDR_EINVAL      # n = 0
+    assert L.ptdr_plan_create(17, 0, 2, ctypes.byref(h)) == ptdr.PTDR_EINVAL     # n > 16 dense
+    assert L.ptdr_plan_create(10, 0, 0, ctypes.byref(h)) == ptdr.PTDR_EINVAL     # depth 0
+    assert L.ptdr_plan_create(10, 0, 5, ctypes.byref(h)) == ptdr.PTDR_EINVAL     # depth > 4
+    assert L.ptdr_plan_create(10, 9, 1, ctypes.byref(h)) == ptdr.PTDR_EINVAL     # structure
+    assert L.ptdr_plan_create(10, 0, 1, None) == ptdr.PTDR_EINVAL                # null out
+    assert L.ptdr_plan_wait(None) == ptdr.PTDR_EINVAL
+    assert L.ptdr_plan_destroy(None) == ptdr.PTDR_OK

@@ -163,6 +163,40 @@ def test_host_entry_point(gpu):
     _assert_close(got, oracle.decompose(A), np.max(np.abs(A)), "decompose_host")
 
 
+@pytest.mark.parametrize("depth", [1, 2, 3])
+def test_host_plan_stream(gpu, depth):
+    """ptdr_plan_*: a stream of distinct host matrices through `depth` device slots; every
+    result equals the oracle (slot reuse must never mix up inputs and outputs)."""
+    torch = _torch()
+    n, mats = 9, 5
+    As = [_dense(n, 20 + k, "general") for k in range(mats)]
+    hin = [torch.from_numpy(a).pin_memory() for a in As]
+    hout = [torch.empty(4 ** n, dtype=torch.complex128).pin_memory() for _ in range(mats)]
+    with ptdr.HostPlan(n, "general", depth=depth) as plan:
+        for k in range(mats):
+            plan.decompose_async(hin[k], hout[k])
+        plan.wait()
+        assert plan.launch_count() >= 1
+    for k in range(mats):
+        _assert_close(hout[k].numpy(), oracle.decompose(As[k]), np.max(np.abs(As[k])), f"plan[{k}]")
+
+
+def test_host_plan_structures(gpu):
+    torch = _torch()
+    n = 8
+    H = _dense(n, 3, "hermitian")
+    out = np.empty(4 ** n, dtype=np.complex128)
+    with ptdr.HostPlan(n, "hermitian", depth=1) as plan:
+        plan.decompose_async(np.ascontiguousarray(H), out)
+        plan.wait()
+    _assert_close(out, oracle.decompose(H), np.max(np.abs(H)), "plan hermitian")
+    with pytest.raises(ptdr.PtdrError):
+        ptdr.HostPlan(n, "general", depth=0)
+    with pytest.raises(ValueError):
+        with ptdr.HostPlan(n, "general", depth=1) as plan:
+            plan.decompose_async(np.zeros(16, np.complex128), out)
+
+
 def test_error_paths(gpu):
     torch = _torch()
     A = torch.zeros((256, 256), dtype=torch.complex128, device="cuda")

@@ -87,7 +87,8 @@ size_t ptdr_input_count(int n, int structure);
 size_t ptdr_output_count(int n, int structure);
 
 /* Device workspace bytes needed by ptdr_decompose_async for (n, structure) on one
- * GPU (world = 1) or per rank of ptdr_decompose_xshard_async (world > 1).
+ * GPU (world = 1), or per rank of ptdr_decompose_xshard_async (GENERAL, world > 1) or
+ * ptdr_decompose_zshard_async (DIAGONAL / TRIDIAGONAL, world > 1).
  * Deterministic in its arguments.  (size_t)-1 if invalid. */
 size_t ptdr_workspace_bytes(int n, int structure, int world);
 
@@ -119,6 +120,17 @@ ptdr_status ptdr_decompose_host(const ptdr_c128* A_host, int n, int structure,
 ptdr_status ptdr_decompose_xshard_async(const ptdr_c128* A_local, int n, int rank, int world,
                                         ptdr_c128* out_local, void* workspace, size_t ws_bytes,
                                         void* stream);
+
+/* Multi-GPU, per rank, DIAGONAL / TRIDIAGONAL (replicated band,
+ * z-sharded output, no communication).  Every rank holds the whole band (input layout as
+ * for ptdr_decompose_async) and writes the z-slice z in [rank 2^(n-g), (rank+1) 2^(n-g))
+ * of every output block, world = 2^g <= 2^n: out_local has ptdr_output_count(n, s) / world
+ * elements, block-major, out_local[b * 2^(n-g) + (z - rank 2^(n-g))] = coefficient
+ * (block b, z) of ptdr_decompose_async's output.  Results are bitwise identical to the
+ * one-GPU path (same WHT schedule).  workspace >= ptdr_workspace_bytes(n, s, world). */
+ptdr_status ptdr_decompose_zshard_async(const ptdr_c128* band, int n, int structure, int rank,
+                                        int world, ptdr_c128* out_local, void* workspace,
+                                        size_t ws_bytes, void* stream);
 
 /* Seeded counter-based generator (the paper fixes no
  * distribution, "a generic matrix", l.631).  Writes rows [row0, row0+nrows) of the

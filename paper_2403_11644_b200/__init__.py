@@ -53,6 +53,8 @@ def lib():
         L.ptdr_decompose_async.argtypes = [vp, i32, i32, vp, vp, sz, vp]
         L.ptdr_decompose_host.argtypes = [vp, i32, i32, vp]
         L.ptdr_decompose_xshard_async.argtypes = [vp, i32, i32, i32, vp, vp, sz, vp]
+        L.ptdr_decompose_zshard_async.argtypes = [vp, i32, i32, i32, i32, vp, vp, sz, vp]
+        L.ptdr_decompose_zshard_async.restype = i32
         L.ptdr_generate_dense_async.argtypes = [i32, u64, i32, u64, u64, vp, vp]
         L.ptdr_generate_band_async.argtypes = [i32, u64, i32, vp, vp]
         L.ptdr_generate_sendblocks_async.argtypes = [i32, u64, i32, i32, vp, vp]
@@ -261,6 +263,28 @@ def decompose_xshard(A_local, n: int, rank: int, world: int, out=None, workspace
                                            ctypes.c_void_p(workspace.data_ptr()),
                                            workspace.numel(), _stream_ptr(stream))
     _check(st, "ptdr_decompose_xshard_async")
+    return out
+
+
+def decompose_zshard(band, structure, rank: int, world: int, out=None, workspace=None, stream=None):
+    """Per-rank z-slice of a DIAGONAL / TRIDIAGONAL decomposition (ptdr_decompose_zshard_async):
+    every rank holds the whole band, rank r writes z in [r 2^n/world, (r+1) 2^n/world) of
+    every output block (block-major, output_count / world elements)."""
+    import torch
+
+    _require_cuda_c128(band, "band")
+    s = _structure(structure)
+    n = n_of(band, s)
+    if out is None:
+        out = torch.empty(output_count(n, s) // world, dtype=torch.complex128, device=band.device)
+    _require_cuda_c128(out, "out")
+    if workspace is None:
+        workspace = alloc_workspace(n, s, world, band.device)
+    st = lib().ptdr_decompose_zshard_async(ctypes.c_void_p(band.data_ptr()), n, s, rank, world,
+                                           ctypes.c_void_p(out.data_ptr()),
+                                           ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
+                                           _stream_ptr(stream))
+    _check(st, "ptdr_decompose_zshard_async")
     return out
 
 

@@ -217,12 +217,17 @@ size_t ptdr_output_count(int n, int s) {
 size_t ptdr_workspace_bytes(int n, int s, int world) {
   if (!valid_n(n, s) || world < 1 || (world & (world - 1))) return (size_t)-1;
   if (world > 1) {
-    if (s != PTDR_GENERAL) return (size_t)-1;
     const int g = __builtin_ctz((unsigned)world);
-    if (n - g < 4) return (size_t)-1;
+    if (s == PTDR_GENERAL) {
+      if (n - g < 4) return (size_t)-1;
+    } else if (is_band(s)) {
+      if (g > n) return (size_t)-1;
+    } else {
+      return (size_t)-1;
+    }
   }
   if (is_dense(s)) return dense_ws(n, s, world);
-  return band_workspace_bytes(n, s);
+  return band_workspace_bytes(n, s, world);
 }
 
 const char* ptdr_status_string(int status) {
@@ -262,7 +267,7 @@ ptdr_status ptdr_decompose_async(const ptdr_c128* A, int n, int structure, ptdr_
                   workspace, st, &nl);
   } else {
     cudaError_t e = launch_band(reinterpret_cast<const double2*>(A), reinterpret_cast<double2*>(out), n,
-                                structure, workspace, st, &nl);
+                                structure, workspace, 0, 1, st, &nl);
     r = e == cudaSuccess ? PTDR_OK : cuda_fail(e, "band kernel launch");
   }
   g_last_launches = nl;
@@ -301,6 +306,30 @@ ptdr_status ptdr_decompose_xshard_async(const ptdr_c128* A_local, int n, int ran
   ptdr_status r = launch_mode(MODE_GENERAL, a, p, reinterpret_cast<cudaStream_t>(stream), &nl);
   g_last_launches = nl;
   return r;
+}
+
+ptdr_status ptdr_decompose_zshard_async(const ptdr_c128* band, int n, int structure, int rank, int world,
+                                        ptdr_c128* out_local, void* workspace, size_t ws_bytes,
+                                        void* stream) {
+  g_last_launches = 0;
+  if (!is_band(structure)) return fail(PTDR_EINVAL, "z-sharding is for DIAGONAL / TRIDIAGONAL");
+  if (!valid_n(n, structure)) return fail(PTDR_EINVAL, "invalid n");
+  if (world < 1 || (world & (world - 1))) return fail(PTDR_EINVAL, "world must be a power of two");
+  if ((uint64_t)world > (1ull << n)) return fail(PTDR_EINVAL, "world > 2^n");
+  if (rank < 0 || rank >= world) return fail(PTDR_EINVAL, "rank out of range");
+  if (!band || !out_local) return fail(PTDR_EINVAL, "null pointer");
+  if (((uintptr_t)band & 15) || ((uintptr_t)out_local & 15)) return fail(PTDR_EINVAL, "misaligned");
+  const size_t need = ptdr_workspace_bytes(n, structure, world);
+  if (need > 0 && (!workspace || ((uintptr_t)workspace & 255)))
+    return fail(PTDR_EINVAL, "workspace missing or not 256-byte aligned");
+  if (ws_bytes < need) return fail(PTDR_ENOMEM, "workspace too small");
+  const size_t inb = ptdr_input_count(n, structure) * 16, outb = ptdr_output_count(n, structure) * 16 / world;
+  if (overlaps(band, inb, out_local, outb)) return fail(PTDR_EUNSUPPORTED, "out overlaps the band");
+  int nl = 0;
+  cudaError_t e = launch_band(reinterpret_cast<const double2*>(band), reinterpret_cast<double2*>(out_local), n,
+                              structure, workspace, rank, world, reinterpret_cast<cudaStream_t>(stream), &nl);
+  g_last_launches = nl;
+  return e == cudaSuccess ? PTDR_OK : cuda_fail(e, "band kernel launch");
 }
 
 ptdr_status ptdr_decompose(const ptdr_c128* A, int n, int structure, ptdr_c128* out) {

@@ -24,9 +24,9 @@ cudaError_t launch_dense_pipe(int mode, const DenseArgs& a, const DensePlan& p, 
 int debug_trace_copy(void* host, size_t bytes);
 
 // band paths (band.cu)
-size_t band_workspace_bytes(int n, int structure);
-cudaError_t launch_band(const double2* A, double2* out, int n, int structure, void* ws,
-                        cudaStream_t st, int* nl);
+size_t band_workspace_bytes(int n, int structure, int world);
+cudaError_t launch_band(const double2* A, double2* out, int n, int structure, void* ws, int rank,
+                        int world, cudaStream_t st, int* nl);
 
 // generators (generate.cu)
 cudaError_t launch_generate_dense(int n, uint64_t seed, int variant, uint64_t row0,

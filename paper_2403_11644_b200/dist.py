@@ -1,4 +1,6 @@
-"""Multi-GPU X-mask sharding.
+"""Multi-GPU paths.
+
+Dense GENERAL: X-mask sharding.
 
 One process per GPU.  Rank g starts with its row block of A in the
 column-block-major send layout send[b][r][c] = A[g*R + r][(g ^ b)*R + c]
@@ -12,7 +14,7 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-from . import decompose_xshard, q_of
+from . import decompose_xshard, decompose_zshard, q_of
 
 
 def exchange(send: torch.Tensor, group=None, recv: torch.Tensor | None = None) -> torch.Tensor:
@@ -57,3 +59,45 @@ def global_q_array(rank: int, n: int, world: int):
     zt = local >> w
     top = np.array([q_of(rank, int(v), g) for v in range(1 << g)], dtype=np.int64)
     return (top[zt] << w) | (local & ((1 << w) - 1))
+
+
+# ---- structured (DIAGONAL / TRIDIAGONAL): replicated band, z-sharded output -------------
+def decompose_band_sharded(band: torch.Tensor, structure, group=None, out=None, workspace=None,
+                           stream=None) -> torch.Tensor:
+    """Every rank holds the whole band (generated locally from the shared seed: no
+    communication) and computes its z-slice of every output block."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    return decompose_zshard(band, structure, rank, world, out=out, workspace=workspace, stream=stream)
+
+
+def zshard_index(rank: int, n: int, world: int, blocks: int):
+    """Global output index of every rank-local element of a z-sharded band output
+    (block-major, 2^n/world per block): local b*NL + zl -> global b*2^n + rank*NL + zl."""
+    import numpy as np
+
+    NL = (1 << n) // world
+    local = np.arange(blocks * NL, dtype=np.int64)
+    return (local // NL) * (1 << n) + rank * NL + (local % NL)
+
+
+def assemble_zshards(parts, n: int, blocks: int):
+    """Host-side assembly of the per-rank slices into the one-GPU output layout."""
+    import numpy as np
+
+    world = len(parts)
+    out = np.empty(blocks << n, dtype=np.asarray(parts[0]).dtype)
+    for r, p in enumerate(parts):
+        out[zshard_index(r, n, world, blocks)] = np.asarray(p)
+    return out
+
+
+def gather_band_sharded(local: torch.Tensor, n: int, blocks: int, group=None) -> torch.Tensor:
+    """all_gather the slices and reorder them into the one-GPU output (for users who need
+    the whole result on every rank; not part of the timed path)."""
+    world = dist.get_world_size(group)
+    parts = [torch.empty_like(local) for _ in range(world)]
+    dist.all_gather(parts, local, group=group)
+    NL = (1 << n) // world
+    stacked = torch.stack([p.view(blocks, NL) for p in parts], dim=1)  # [blocks][world][NL]
+    return stacked.reshape(blocks << n)

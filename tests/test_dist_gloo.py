@@ -84,3 +84,73 @@ def test_xmask_exchange_and_layout(world, n):
         allq += qs
     # the ranks' outputs tile the global q range exactly once
     assert sorted(allq) == list(range(4 ** n))
+
+
+def _band_worker(rank, world, port, n, structure, result_q):
+    """z-sharded structured path: every rank holds the whole band, computes its z-slice of
+    every block (here with the oracle, standing in for the kernels), and the gloo all_gather
+    + reorder of dist.gather_band_sharded must rebuild the one-GPU output layout."""
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        import ptdr_inputs
+        from paper_2403_11644_b200 import dist as pdist
+        from paper_2403_11644_b200 import q_of
+
+        N = 1 << n
+        blocks = n + 1 if structure == "tridiagonal" else 1
+        gidx = pdist.zshard_index(rank, n, world, blocks)       # global index of each local one
+        b, z = gidx >> n, gidx & (N - 1)
+        xs = (1 << b) - 1 if structure == "tridiagonal" else np.zeros_like(b)
+        qs = np.array([q_of(int(x), int(zz), n) for x, zz in zip(xs, z)], dtype=np.uint64)
+        if structure == "tridiagonal":
+            sub, main, sup = ptdr_inputs.band(n, 3, "tridiagonal")
+            local = oracle.coeffs_tridiagonal(sub, main, sup, qs)
+        else:
+            d = ptdr_inputs.band(n, 3, "diagonal")
+            local = oracle.coeffs_diagonal(d, qs)
+        full = pdist.gather_band_sharded(torch.from_numpy(np.ascontiguousarray(local)), n, blocks)
+        result_q.put((rank, full.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n,structure", [(2, 5, "tridiagonal"), (4, 6, "tridiagonal"),
+                                               (2, 6, "diagonal")])
+def test_band_zshard_gather(world, n, structure):
+    import oracle
+    import ptdr_inputs
+    from paper_2403_11644_b200 import dist as pdist
+    from paper_2403_11644_b200 import q_of
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_band_worker, args=(r, world, port, n, structure, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    N = 1 << n
+    blocks = n + 1 if structure == "tridiagonal" else 1
+    xs = [(1 << b) - 1 for b in range(blocks)] if structure == "tridiagonal" else [0]
+    qs = np.array([q_of(x, z, n) for x in xs for z in range(N)], dtype=np.uint64)
+    if structure == "tridiagonal":
+        sub, main, sup = ptdr_inputs.band(n, 3, "tridiagonal")
+        want = oracle.coeffs_tridiagonal(sub, main, sup, qs)
+    else:
+        want = oracle.coeffs_diagonal(ptdr_inputs.band(n, 3, "diagonal"), qs)
+    for rank, full in results:
+        assert np.array_equal(full, want), f"rank {rank}"
+    # the host-side assembly agrees with the collective one, and the slices tile the output
+    parts = [want[pdist.zshard_index(r, n, world, blocks)] for r in range(world)]
+    assert np.array_equal(pdist.assemble_zshards(parts, n, blocks), want)
+    allidx = np.concatenate([pdist.zshard_index(r, n, world, blocks) for r in range(world)])
+    assert np.array_equal(np.sort(allidx), np.arange(blocks << n))

@@ -60,7 +60,19 @@ def band(name, n, seed, variant):
                       "coeffs_per_s": coeffs / (ms * 1e-3), "alg_bytes": alg, "hbm_gbs": gbs,
                       "frac_of_measured": gbs / PEAK, "launches": ptdr.last_launch_count()}),
           flush=True)
-    del B, out, ws
+    # 8 GPUs, replicated band + z-sharded output: ranks are independent (no communication),
+    # so the 8-GPU step time is the max over ranks of each rank's own time (ranks 0 and 7 here)
+    world = 8
+    outl = torch.empty(ptdr.output_count(n, variant) // world, dtype=torch.complex128, device="cuda")
+    wsl = ptdr.alloc_workspace(n, variant, world, "cuda")
+    ms8 = max(time_it(lambda: ptdr.decompose_zshard(B, variant, r, world, out=outl, workspace=wsl))
+              for r in (0, world - 1))
+    print(json.dumps({"config": name + "_8gpu_zshard", "n": n, "structure": variant, "ms_per_rank": ms8,
+                      "coeffs_per_s_total": coeffs / (ms8 * 1e-3),
+                      "alg_bytes_per_rank": (B.numel() + out.numel() // world) * 16,
+                      "hbm_gbs_per_rank": (B.numel() + out.numel() // world) * 16 / (ms8 * 1e-3) / 1e9}),
+          flush=True)
+    del B, out, ws, outl, wsl
     torch.cuda.empty_cache()
 
 

@@ -10,6 +10,9 @@ cudaError_t pipe_cfg2(int mode, const CUtensorMap& map, const DenseArgs& a, int 
 cudaError_t pipe_cfg3(int mode, const CUtensorMap& map, const DenseArgs& a, int M, cudaStream_t st);
 cudaError_t pipe_cfg4(int mode, const CUtensorMap& map, const DenseArgs& a, int M, cudaStream_t st);
 cudaError_t pipe_cfg5(int mode, const CUtensorMap& map, const DenseArgs& a, int M, cudaStream_t st);
+cudaError_t pipe_cfg6(int mode, const CUtensorMap& map, const DenseArgs& a, int M, cudaStream_t st);
+cudaError_t pipe_cfg7(int mode, const CUtensorMap& map, const DenseArgs& a, int M, cudaStream_t st);
+cudaError_t pipe_cfg8(int mode, const CUtensorMap& map, const DenseArgs& a, int M, cudaStream_t st);
 
 static unsigned long long* g_trace = nullptr;
 static unsigned long long* debug_trace_buffer() {
@@ -84,6 +87,9 @@ cudaError_t launch_dense_pipe(int mode, const DenseArgs& a_in, const DensePlan& 
     case 3: return pipe_cfg3(mode, map, a, p.M, st);
     case 4: return pipe_cfg4(mode, map, a, p.M, st);
     case 5: return pipe_cfg5(mode, map, a, p.M, st);
+    case 6: return pipe_cfg6(mode, map, a, p.M, st);
+    case 7: return pipe_cfg7(mode, map, a, p.M, st);
+    case 8: return pipe_cfg8(mode, map, a, p.M, st);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -194,7 +194,11 @@ __device__ __forceinline__ void decode_ticket32(uint32_t t, int M, uint32_t C, u
   phase = 1; chunk = steady + (t >> M); tile = t & (NA - 1u);
 }
 
-template <int LT, int XB, int GW, int NG, int NS>
+// NR = 0: the radix stages exchange in place in the stage buffer, which is released after
+// the exchange.  NR = 2 ("early release"): each group owns an exchange buffer of half a
+// tile; the stage is released right after its first read into registers and the exchange
+// runs in two rounds (exchange_rounds / xor_half_transpose below).
+template <int LT, int XB, int GW, int NG, int NS, int NR = 0>
 struct PipeCfg {
   static constexpr int TE = 1 << LT;          // tile elements
   static constexpr int TB = TE * 16;          // tile bytes
@@ -216,8 +220,11 @@ struct PipeCfg {
   static constexpr int CONS_REGS = CONS_REGS_RAW > 248 ? 248 : CONS_REGS_RAW;
   static_assert(CONS_REGS >= LAUNCH_REGS && PROD_REGS * 128 + CONS_REGS * CONS_THREADS <= THREADS * LAUNCH_REGS,
                 "register rebalancing must fit the launch-time pool");
-  static constexpr int SMEM = NS * TB + 2048;
+  static constexpr int XE = NR ? TE / NR : 0;  // exchange-buffer elements per group
+  static constexpr int SMEM = NS * TB + NG * XE * 16 + 2048;
   static_assert(GT * 16 == TE, "16 elements per consumer thread");
+  static_assert(NR == 0 || NR == 2, "exchange rounds");
+  static_assert(SMEM <= 227 * 1024, "shared memory per CTA");
 };
 
 // Fiber index of the phase-B tiles: phi encodes (u, zl) with bits [0,1]=u0,u1 [2,3]=zl0,zl1
@@ -243,12 +250,72 @@ __device__ __forceinline__ uint32_t phi_zl_of(uint32_t phi) {
   return ((phi >> 2) & 3u) | ((phi >> (XB + 2)) << 2);
 }
 
+// ---- exchange between the two radix stages through a half-tile buffer X (early release) --
+// Stage 1 leaves thread (c, a) with v[kk] = T[a][kk] (a = its row block, kk = 16 register
+// indices) for the column c it owns (X-mask u in phase A, fibre f in phase B; lanes run
+// along c, STR = number of columns).  Stage 2 needs, for unit p = (c, jl = a + 2^R2 p),
+// the 2^R2 values T[j][jl], j < 2^R2.  With U >= 2 units per thread, the units whose jl
+// falls in [8h, 8h+8) take exactly the registers v[8h..8h+8) that round h frees, so both
+// rounds are compile-time register maps: on exit v[p 2^R2 + j] = T[j][a + 2^R2 p].
+template <int R2, int U, int STR>
+__device__ __forceinline__ void exchange_rounds(double2 (&v)[16], double2* X, int a, int c, int bar_id,
+                                                int nthr) {
+  static_assert(U * (1 << R2) == 16 && U >= 2, "two rounds of 8 registers");
+  constexpr int PH = U / 2;  // units per round
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+#pragma unroll
+    for (int kq = 0; kq < 8; ++kq) X[(a * 8 + kq) * STR + c] = v[8 * h + kq];
+    named_bar_sync(bar_id, nthr);
+#pragma unroll
+    for (int pp = 0; pp < PH; ++pp) {
+      const int jl = a + (1 << R2) * (h * PH + pp);  // in [8h, 8h+8)
+#pragma unroll
+      for (int jj = 0; jj < (1 << R2); ++jj) v[8 * h + pp * (1 << R2) + jj] = X[(jj * 8 + (jl - 8 * h)) * STR + c];
+    }
+    named_bar_sync(bar_id, nthr);
+  }
+}
+
+// One unit of 16 (R2 = 4): a full 16 x 16 transpose per column through half a tile.  Entry
+// (j, kk) travels in round bit3(j ^ kk), so each round every thread sends 8 and receives 8
+// values; a thread whose row a has bit 3 set swaps its register halves before and after
+// (warp-uniform: a = 2 warp + lane/16 or coarser).  On exit v[j] = T[j][a].
+template <int STR>
+__device__ __forceinline__ void xor_half_transpose(double2 (&v)[16], double2* X, int a, int c, int bar_id,
+                                                   int nthr) {
+  const bool b = ((a >> 3) & 1) != 0;
+  auto swap_halves = [&]() {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const double2 lo = v[q], hi = v[q + 8];
+      v[q] = b ? hi : lo;
+      v[q + 8] = b ? lo : hi;
+    }
+  };
+  swap_halves();  // v[q] = T[a][q ^ 8b]
+  const int jb = b ? 8 : 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) X[(a * 8 + q) * STR + c] = v[q];
+  named_bar_sync(bar_id, nthr);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) v[q] = X[((q + jb) * 8 + (a & 7)) * STR + c];      // T[q + 8b][a]
+  named_bar_sync(bar_id, nthr);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) X[(a * 8 + q) * STR + c] = v[q + 8];
+  named_bar_sync(bar_id, nthr);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) v[q + 8] = X[((q + 8 - jb) * 8 + (a & 7)) * STR + c];  // T[q + 8(1-b)][a]
+  named_bar_sync(bar_id, nthr);
+  swap_halves();  // v[j] = T[j][a]
+}
+
 // Scratch layout (per chunk slot): B-tile-major Y[tileB][ih][f], 2^LT elements per phase-B
 // tile, so a phase-B tile is one contiguous bulk copy (fiber phi = tileB * FB + f).
-template <int LT, int XB, int GW, int NG, int NS, int M, int MODE>
-__global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS>::THREADS, 1)
+template <int LT, int XB, int GW, int NG, int NS, int NR, int M, int MODE>
+__global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
     dense_pipe_kernel(const __grid_constant__ CUtensorMap tmap, DenseArgs a) {
-  using Cfg = PipeCfg<LT, XB, GW, NG, NS>;
+  using Cfg = PipeCfg<LT, XB, GW, NG, NS, NR>;
   constexpr int R = Cfg::R, TE = Cfg::TE, GT = Cfg::GT, W = Cfg::W;
   constexpr bool HALF = (MODE == MODE_HERM_HALF || MODE == MODE_SYM_HALF);
   constexpr int FB = TE >> M;  // phase-B fibers per tile
@@ -257,7 +324,8 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS>::THREADS, 1)
   static_assert(R >= XB && R - 4 >= 1 && R - 4 <= 4, "phase-A tile geometry");
   extern __shared__ __align__(1024) unsigned char smem[];
   double2* stage0 = reinterpret_cast<double2*>(smem);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * Cfg::TB);
+  double2* xbuf = reinterpret_cast<double2*>(smem + NS * Cfg::TB);  // [NG][XE] (NR > 0)
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * Cfg::TB + NG * Cfg::XE * 16);
   uint64_t* empty = full + NS;
   TileMeta* meta = reinterpret_cast<TileMeta*>(empty + NS);
   constexpr int SIGD = Cfg::SIGD;
@@ -472,7 +540,46 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS>::THREADS, 1)
     const uint32_t chunk = m.chunk;
     double2* Y = a.scratch + (size_t)(chunk % nslot) * a.slot_elems;
     double2 v[16];
-    if (m.phase == 0) {
+    if (m.phase == 0 && NR > 0) {
+      // ---- phase A, early release: read the stage once, release it, exchange through X
+      const int u = gtid & (W - 1), jh = gtid >> XB;
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) {
+        const int r = jh * 16 + kk;
+        v[kk] = S[r * W + ((r & (W - 1)) ^ u)];
+        if (MODE == MODE_SYM_HALF) v[kk].y = 0.0;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (gtid == 0) trace_stamp(a.trace, k, 6);
+      wht_regs<4>(v);
+      constexpr int R2 = R - 4;
+      constexpr int UA = (W * 16) / GT;   // second-stage units per thread, 2^R2 registers each
+      double2* X = xbuf + g * Cfg::XE;
+      const uint64_t pol_last = policy_evict_last();
+      // unit (u, jl) -> Y[tileB][ih][f]
+      auto store_unit = [&](const double2* w, int jl) {
+        const uint32_t phi_lo = phi_of<XB>((uint32_t)u, (uint32_t)jl);
+        double2* base = Y + (((phi_lo >> LFB) << LT) | ((uint32_t)m.tile << LFB) | (phi_lo & (FB - 1)));
+#pragma unroll
+        for (int jj = 0; jj < (1 << R2); ++jj)
+          st_global_hint(base + ((size_t)jj << (XB + 4 - LFB + LT)), w[jj], pol_last);
+      };
+      if constexpr (UA >= 2) {
+        exchange_rounds<R2, UA, W>(v, X, jh, u, bar_id, GT);
+#pragma unroll
+        for (int p = 0; p < UA; ++p) {
+          wht_regs<R2>(&v[p * (1 << R2)]);
+          store_unit(&v[p * (1 << R2)], jh + (1 << R2) * p);
+        }
+      } else {
+        xor_half_transpose<W>(v, X, jh, u, bar_id, GT);
+        wht_regs<4>(v);
+        store_unit(v, jh);
+      }
+      signal(j, &doneA[chunk]);
+      if (gtid == 0) trace_stamp(a.trace, k, 7);
+    } else if (m.phase == 0) {
       // ---- phase A: v_x[i] for x = x0+u, i = tile*2^R + r, r = jh*16 + kk; the element
       //      sits in SMEM row r at column (r mod W) ^ u (XOR transpose in the read)
       {
@@ -534,6 +641,42 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS>::THREADS, 1)
           for (int d = 0; d < Cfg::TB / 128 / GT; ++d) discard_l2(yb + ((size_t)(gtid + GT * d) << 7));
         }
       };
+      if constexpr (NR > 0 && M > 4) {
+        // ---- early release: read the stage once, drop the scratch lines (the TMA copy has
+        //      completed), release the stage, exchange through X
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) v[kk] = S[(jh * 16 + kk) * FB + f];
+        discard_tile();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (gtid == 0) trace_stamp(a.trace, k, 6);
+        wht_regs<4>(v);
+        constexpr int R2 = M - 4;
+        constexpr int UB = (FB * 16) / GT;
+        double2* X = xbuf + g * Cfg::XE;
+        auto emit_unit = [&](const double2* w, int jl) {
+          const uint32_t phi = (uint32_t)m.tile * FB + (uint32_t)f;
+          EpiUnit<R2, HALF> e;
+          e.init((uint32_t)x0 + phi_u_of<XB>(phi), ((uint32_t)jl << R) | phi_zl_of<XB>(phi), R + 4, t,
+                 a.gshift);
+          emit_all<MODE, R2>(a, e, w);
+        };
+        if constexpr (UB >= 2) {
+          exchange_rounds<R2, UB, FB>(v, X, jh, f, bar_id, GT);
+#pragma unroll
+          for (int p = 0; p < UB; ++p) {
+            wht_regs<R2>(&v[p * (1 << R2)]);
+            emit_unit(&v[p * (1 << R2)], jh + (1 << R2) * p);
+          }
+        } else {
+          xor_half_transpose<FB>(v, X, jh, f, bar_id, GT);
+          wht_regs<4>(v);
+          emit_unit(v, jh);
+        }
+        signal(j, &doneB[chunk]);
+        if (gtid == 0) trace_stamp(a.trace, k, 7);
+        continue;
+      }
       if constexpr (kBDirect) {
 #pragma unroll
         for (int kk = 0; kk < 16; ++kk) v[kk] = __ldcg(yt + (jh * 16 + kk) * FB + f);
@@ -589,10 +732,10 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS>::THREADS, 1)
 }
 
 // ------------------------------------------------------------------ launch template
-template <int LT, int XB, int GW, int NG, int NS, int M, int MODE>
+template <int LT, int XB, int GW, int NG, int NS, int NR, int M, int MODE>
 static cudaError_t launch_pipe_impl(const CUtensorMap& map, const DenseArgs& a, cudaStream_t st) {
-  using Cfg = PipeCfg<LT, XB, GW, NG, NS>;
-  constexpr auto kern = dense_pipe_kernel<LT, XB, GW, NG, NS, M, MODE>;
+  using Cfg = PipeCfg<LT, XB, GW, NG, NS, NR>;
+  constexpr auto kern = dense_pipe_kernel<LT, XB, GW, NG, NS, NR, M, MODE>;
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [&]() {
@@ -603,32 +746,32 @@ static cudaError_t launch_pipe_impl(const CUtensorMap& map, const DenseArgs& a, 
   return cudaGetLastError();
 }
 
-template <int LT, int XB, int GW, int NG, int NS, int MODE>
+template <int LT, int XB, int GW, int NG, int NS, int NR, int MODE>
 static cudaError_t launch_pipe_m(const CUtensorMap& map, const DenseArgs& a, int M, cudaStream_t st) {
   switch (M) {
-    case 4: return launch_pipe_impl<LT, XB, GW, NG, NS, 4, MODE>(map, a, st);
-    case 5: return launch_pipe_impl<LT, XB, GW, NG, NS, 5, MODE>(map, a, st);
-    case 6: return launch_pipe_impl<LT, XB, GW, NG, NS, 6, MODE>(map, a, st);
-    case 7: return launch_pipe_impl<LT, XB, GW, NG, NS, 7, MODE>(map, a, st);
-    case 8: return launch_pipe_impl<LT, XB, GW, NG, NS, 8, MODE>(map, a, st);
+    case 4: return launch_pipe_impl<LT, XB, GW, NG, NS, NR, 4, MODE>(map, a, st);
+    case 5: return launch_pipe_impl<LT, XB, GW, NG, NS, NR, 5, MODE>(map, a, st);
+    case 6: return launch_pipe_impl<LT, XB, GW, NG, NS, NR, 6, MODE>(map, a, st);
+    case 7: return launch_pipe_impl<LT, XB, GW, NG, NS, NR, 7, MODE>(map, a, st);
+    case 8: return launch_pipe_impl<LT, XB, GW, NG, NS, NR, 8, MODE>(map, a, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
-template <int LT, int XB, int GW, int NG, int NS>
+template <int LT, int XB, int GW, int NG, int NS, int NR>
 static cudaError_t launch_pipe_cfg(int mode, const CUtensorMap& map, const DenseArgs& a, int M,
                                    cudaStream_t st) {
   switch (mode) {
-    case MODE_GENERAL: return launch_pipe_m<LT, XB, GW, NG, NS, MODE_GENERAL>(map, a, M, st);
-    case MODE_HERM_HALF: return launch_pipe_m<LT, XB, GW, NG, NS, MODE_HERM_HALF>(map, a, M, st);
-    case MODE_SYM_HALF: return launch_pipe_m<LT, XB, GW, NG, NS, MODE_SYM_HALF>(map, a, M, st);
+    case MODE_GENERAL: return launch_pipe_m<LT, XB, GW, NG, NS, NR, MODE_GENERAL>(map, a, M, st);
+    case MODE_HERM_HALF: return launch_pipe_m<LT, XB, GW, NG, NS, NR, MODE_HERM_HALF>(map, a, M, st);
+    case MODE_SYM_HALF: return launch_pipe_m<LT, XB, GW, NG, NS, NR, MODE_SYM_HALF>(map, a, M, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
-#define PTDR_DEFINE_PIPE_CFG(NAME, LT, XB, GW, NG, NS)                                         \
+#define PTDR_DEFINE_PIPE_CFG(NAME, LT, XB, GW, NG, NS, NR)                                     \
   cudaError_t NAME(int mode, const CUtensorMap& map, const DenseArgs& a, int M, cudaStream_t st) { \
-    return launch_pipe_cfg<LT, XB, GW, NG, NS>(mode, map, a, M, st);                           \
+    return launch_pipe_cfg<LT, XB, GW, NG, NS, NR>(mode, map, a, M, st);                       \
   }
 
 }  // namespace ptdr

@@ -2,5 +2,5 @@
 // 3 groups x 4 warps, 6 stages.
 #include "dense_pipe.cuh"
 namespace ptdr {
-PTDR_DEFINE_PIPE_CFG(pipe_cfg5, 11, 5, 4, 3, 6)
+PTDR_DEFINE_PIPE_CFG(pipe_cfg5, 11, 5, 4, 3, 6, 0)
 }  // namespace ptdr

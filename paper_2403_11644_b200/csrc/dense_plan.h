@@ -32,24 +32,31 @@ struct DensePlan {
 };
 
 // dense_pipe.cuh configurations (dense_pipe_c<k>.cu): tile 2^LT elements, chunk width 2^XB,
-// GW warps per group, NG groups, NS stages.
+// GW warps per group, NG groups, NS stages, NR exchange rounds (0: in-place exchange in the
+// stage; 2/4: early stage release with a per-group exchange buffer of 2^LT/NR elements).
 struct PipeGeom {
-  int LT, XB, GW, NG, NS;
+  int LT, XB, GW, NG, NS, NR;
 };
 constexpr int kPipeNone = 0;
-constexpr int kPipeCfgCount = 5;
+constexpr int kPipeCfgCount = 8;
 inline PipeGeom pipe_geom(int cfg) {
   switch (cfg) {
-    case 1: return {12, 4, 8, 2, 3};
-    case 2: return {11, 4, 4, 4, 6};
-    case 3: return {11, 4, 4, 3, 6};
-    case 4: return {12, 5, 8, 2, 3};
-    case 5: return {11, 5, 4, 3, 6};
-    default: return {0, 4, 0, 0, 0};
+    case 1: return {12, 4, 8, 2, 3, 0};
+    case 2: return {11, 4, 4, 4, 6, 0};
+    case 3: return {11, 4, 4, 3, 6, 0};
+    case 4: return {12, 5, 8, 2, 3, 0};
+    case 5: return {11, 5, 4, 3, 6, 0};
+    case 6: return {12, 5, 8, 2, 2, 2};
+    case 7: return {11, 4, 4, 4, 4, 2};
+    case 8: return {12, 4, 8, 2, 2, 2};
+    default: return {0, 4, 0, 0, 0, 0};
   }
 }
 constexpr int kPipeDefault = 4;   // preferred configuration
 constexpr int kPipeFallback = 1;  // when the preferred one does not fit (nv, x_count)
+// Fallback of a configuration that does not fit (nv, x_count): the same pipeline style
+// with 16-wide chunks.
+inline int pipe_fallback(int cfg) { return pipe_geom(cfg).NR ? 8 : kPipeFallback; }
 
 // Tiles resident at once on a B200 (fixes L deterministically, independent of the device).
 constexpr int kNominalSMs = 148;
@@ -75,7 +82,7 @@ inline DensePlan make_dense_plan(int nv, uint64_t x_count, int pipe_cfg = kPipeN
   if (nv <= 7) { p.kind = 1; p.R = nv; p.M = 0; p.nchunks = x_count / 16; return p; }
   p.kind = 2;
   if (pipe_cfg != kPipeNone && !pipe_fits(pipe_cfg, nv, x_count))
-    pipe_cfg = pipe_fits(kPipeFallback, nv, x_count) ? kPipeFallback : kPipeNone;
+    pipe_cfg = pipe_fits(pipe_fallback(pipe_cfg), nv, x_count) ? pipe_fallback(pipe_cfg) : kPipeNone;
   p.pipe_cfg = pipe_cfg;
   int resident;
   if (pipe_cfg != kPipeNone) {

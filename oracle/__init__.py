@@ -21,7 +21,7 @@ _ROOT = os.path.dirname(_HERE)
 _SRCS = [os.path.join(_HERE, "oracle.c"), os.path.join(_ROOT, "ptdr_inputs", "gen.c")]
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-ACC_DENSE, ACC_GENERATED, ACC_DIAG, ACC_TRIDIAG = 0, 1, 2, 3
+ACC_DENSE, ACC_GENERATED, ACC_DIAG, ACC_TRIDIAG, ACC_ANTIDIAG, ACC_BAND = 0, 1, 2, 3, 4, 5
 LETTERS = "IXYZ"  # text-lexicographic order, code = index
 
 _lib = None
@@ -142,6 +142,22 @@ def coeffs_tridiagonal(sub, main, sup, qs) -> np.ndarray:
     n = main.size.bit_length() - 1
     return _coeffs(ACC_TRIDIAG, n, main.view(np.float64), sub.view(np.float64),
                    sup.view(np.float64), 0, 0, qs)
+
+
+def coeffs_antidiagonal(a, qs) -> np.ndarray:
+    """a[i] = A[i][2^n - 1 - i] (anti-diagonal storage)."""
+    a = np.ascontiguousarray(a, dtype=np.complex128)
+    n = a.size.bit_length() - 1
+    return _coeffs(ACC_ANTIDIAG, n, a.view(np.float64), None, None, 0, 0, qs)
+
+
+def coeffs_band(diags, s: int, qs) -> np.ndarray:
+    """(2s+1)-band storage diags[d + s][i] = A[i][i + d]."""
+    diags = np.ascontiguousarray(diags, dtype=np.complex128)
+    if diags.ndim != 2 or diags.shape[0] != 2 * s + 1:
+        raise ValueError("diags must be [2s+1][2^n]")
+    n = diags.shape[1].bit_length() - 1
+    return _coeffs(ACC_BAND, n, diags.view(np.float64), None, None, 0, s, qs)
 
 
 def frobenius2(A) -> float:

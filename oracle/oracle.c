@@ -83,7 +83,7 @@ int oracle_compose(int n, const uint8_t* text, uint32_t* k, int8_t* m, int* n_y)
 
 /* Matrix accessor: the MatrixSource of the decomposition (dense storage, a
  * pure function per P:646, or band storage). */
-enum { ACC_DENSE = 0, ACC_GENERATED = 1, ACC_DIAG = 2, ACC_TRIDIAG = 3 };
+enum { ACC_DENSE = 0, ACC_GENERATED = 1, ACC_DIAG = 2, ACC_TRIDIAG = 3, ACC_ANTIDIAG = 4, ACC_BAND = 5 };
 
 typedef struct {
   int kind;
@@ -92,7 +92,7 @@ typedef struct {
   const double* sub;   /* ACC_TRIDIAG */
   const double* sup;   /* ACC_TRIDIAG */
   uint64_t seed;       /* ACC_GENERATED */
-  int variant;         /* ACC_GENERATED */
+  int variant;         /* ACC_GENERATED; ACC_BAND: half-width s */
 } oracle_acc;
 
 static void acc_entry(const oracle_acc* acc, uint64_t row, uint64_t col, double* re,
@@ -116,6 +116,20 @@ static void acc_entry(const oracle_acc* acc, uint64_t row, uint64_t col, double*
       else if (row == col + 1) { *re = acc->sub[2 * row]; *im = acc->sub[2 * row + 1]; }
       else { *re = 0.0; *im = 0.0; }
       return;
+    case ACC_ANTIDIAG:  /* a[row] = A[row][N-1-row] */
+      if (col == N - 1 - row) { *re = acc->a[2 * row]; *im = acc->a[2 * row + 1]; }
+      else { *re = 0.0; *im = 0.0; }
+      return;
+    case ACC_BAND: {    /* (2s+1)-band: diagonals D_d[row] = A[row][row+d], d in [-s, s],
+                           stored as a[(d + s) * N + row] */
+      int64_t d = (int64_t)col - (int64_t)row;
+      int64_t s = acc->variant;
+      if (d >= -s && d <= s) {
+        uint64_t o = (uint64_t)(d + s) * N + row;
+        *re = acc->a[2 * o]; *im = acc->a[2 * o + 1];
+      } else { *re = 0.0; *im = 0.0; }
+      return;
+    }
     default:
       *re = NAN; *im = NAN;
   }
@@ -169,7 +183,8 @@ static int oracle_make_acc(oracle_acc* acc, int kind, int n, const double* a, co
   if (n < 1 || n > 30) return -1;
   acc->kind = kind; acc->n = n; acc->a = a; acc->sub = sub; acc->sup = sup;
   acc->seed = seed; acc->variant = variant;
-  if ((kind == ACC_DENSE || kind == ACC_DIAG) && !a) return -1;
+  if ((kind == ACC_DENSE || kind == ACC_DIAG || kind == ACC_ANTIDIAG || kind == ACC_BAND) && !a) return -1;
+  if (kind == ACC_BAND && (variant < 0 || variant > 64)) return -1;
   if (kind == ACC_TRIDIAG && (!a || !sub || !sup)) return -1;
   return 0;
 }

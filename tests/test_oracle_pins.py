@@ -302,3 +302,70 @@ def test_generated_accessor_matches_dense():
         A = ptdr_inputs.dense(n, 4, v)
         qs = np.arange(0, 4 ** n, 7, dtype=np.uint64)
         assert np.array_equal(oracle.coeffs_generated(n, 4, v, qs), oracle.coeffs_dense(A, qs))
+
+
+# ---------------------------------------------------------------- anti-diagonal, band(s)
+def _band_storage(rng, n, s):
+    """diags[d + s][i] = A[i][i + d] and the dense matrix it stands for."""
+    N = 1 << n
+    diags = random_complex(rng, (2 * s + 1, N))
+    A = np.zeros((N, N), dtype=np.complex128)
+    for d in range(-s, s + 1):
+        for i in range(N):
+            if 0 <= i + d < N:
+                A[i, i + d] = diags[d + s, i]
+    return diags, A
+
+
+@pytest.mark.parametrize("n", [1, 2, 3])
+def test_antidiagonal_accessor_matches_kronecker(n):
+    # anti-diagonal remark (PAPER l.391-392): A[i][2^n-1-i] only
+    rng = np.random.default_rng(900 + n)
+    N = 1 << n
+    a = random_complex(rng, N)
+    A = np.zeros((N, N), dtype=np.complex128)
+    A[np.arange(N), N - 1 - np.arange(N)] = a
+    got = oracle.coeffs_antidiagonal(a, np.arange(4 ** n, dtype=np.uint64))
+    assert np.max(np.abs(got - brute_force_coeffs(A))) < 1e-14
+
+
+@pytest.mark.parametrize("n", [2, 4, 6])
+def test_antidiagonal_only_XY_strings(n):
+    # l.391-392: "swap I,Z <-> X,Y" of the diagonal case -- only {X,Y}^n strings, 2^n of them
+    rng = np.random.default_rng(910 + n)
+    a = random_complex(rng, 1 << n)
+    c = oracle.coeffs_antidiagonal(a, np.arange(4 ** n, dtype=np.uint64))
+    for q in np.nonzero(np.abs(c) > 1e-14)[0]:
+        assert set(oracle.string_of(int(q), n)) <= {"X", "Y"}
+    assert np.count_nonzero(np.abs(c) > 1e-14) == 1 << n
+
+
+@pytest.mark.parametrize("s,n", [(1, 3), (2, 3), (3, 2)])
+def test_band_accessor_matches_kronecker(s, n):
+    rng = np.random.default_rng(920 + 10 * s + n)
+    diags, A = _band_storage(rng, n, s)
+    got = oracle.coeffs_band(diags, s, np.arange(4 ** n, dtype=np.uint64))
+    assert np.max(np.abs(got - brute_force_coeffs(A))) < 1e-13
+
+
+@pytest.mark.parametrize("s,n", [(1, 5), (2, 5), (3, 5), (4, 6), (5, 6), (8, 6)])
+def test_band_xmask_set_and_count(s, n):
+    # Band theorem (PAPER l.467-496, Table I l.500-518): the nonzero X-masks are those of
+    # the 2s+1 diagonals, x in {0} U {i ^ (i+d)}, and there are s n - c(s) of them
+    # (SURVEY Appendix B: equality verified for generic data).
+    rng = np.random.default_rng(940 + 10 * s + n)
+    diags, A = _band_storage(rng, n, s)
+    c = oracle.coeffs_band(diags, s, np.arange(4 ** n, dtype=np.uint64))
+    xs = set()
+    for q in np.nonzero(np.abs(c) > 1e-14)[0]:
+        x = 0
+        for l in range(n):
+            code = (int(q) >> (2 * l)) & 3
+            x |= (1 if code in (1, 2) else 0) << l
+        xs.add(x)
+    N = 1 << n
+    want = {0} | {i ^ (i + d) for d in range(1, s + 1) for i in range(N - d)}
+    assert xs == want
+    L = int(np.floor(np.log2(s)))
+    cs = s * (L + 1) - (1 << (L + 1))
+    assert len(want) == s * n - cs

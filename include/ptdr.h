@@ -57,6 +57,9 @@ typedef struct {
  *                 x_b = 2^b - 1 (b = 0: the {I,Z}^n strings; b = n: the {X,Y}^n
  *                 strings), and inside a block coefficients are in ascending
  *                 Z-mask z, which is ascending q order restricted to that block.
+ *  ANTI_DIAGONAL  A = a[2^n] with a[i] = A[i][2^n - 1 - i] (the anti-diagonal remark,
+ *                 l.391-392: swap I,Z <-> X,Y); output = the 2^n {X,Y}^n coefficients
+ *                 (X-mask 2^n - 1), ascending z.
  * X-mask / Z-mask of a string: bit l of x is set iff sigma_l in {X,Y}; bit l of z
  * is set iff sigma_l in {Y,Z}. */
 typedef enum {
@@ -64,7 +67,8 @@ typedef enum {
   PTDR_HERMITIAN = 1,
   PTDR_REAL_SYMMETRIC = 2,
   PTDR_DIAGONAL = 3,
-  PTDR_TRIDIAGONAL = 4
+  PTDR_TRIDIAGONAL = 4,
+  PTDR_ANTI_DIAGONAL = 5
 } ptdr_structure;
 
 typedef enum {
@@ -75,15 +79,16 @@ typedef enum {
   PTDR_ECUDA = 4
 } ptdr_status;
 
-/* Supported n: dense structures 1 <= n <= 16; DIAGONAL / TRIDIAGONAL 1 <= n <= 28. */
+/* Supported n: dense structures 1 <= n <= 16; DIAGONAL / TRIDIAGONAL / ANTI_DIAGONAL
+ * 1 <= n <= 28. */
 int ptdr_max_n(int structure);
 
-/* Number of ptdr_c128 elements of the input A: 4^n (dense), 2^n (DIAGONAL),
- * 3*2^n (TRIDIAGONAL).  0 if (n, structure) is invalid. */
+/* Number of ptdr_c128 elements of the input A: 4^n (dense), 2^n (DIAGONAL,
+ * ANTI_DIAGONAL), 3*2^n (TRIDIAGONAL).  0 if (n, structure) is invalid. */
 size_t ptdr_input_count(int n, int structure);
 
-/* Number of ptdr_c128 output coefficients: 4^n, 2^n (DIAGONAL), (n+1)*2^n
- * (TRIDIAGONAL).  0 if invalid. */
+/* Number of ptdr_c128 output coefficients: 4^n, 2^n (DIAGONAL, ANTI_DIAGONAL),
+ * (n+1)*2^n (TRIDIAGONAL).  0 if invalid. */
 size_t ptdr_output_count(int n, int structure);
 
 /* Device workspace bytes needed by ptdr_decompose_async for (n, structure) on one
@@ -131,6 +136,23 @@ ptdr_status ptdr_decompose_xshard_async(const ptdr_c128* A_local, int n, int ran
 ptdr_status ptdr_decompose_zshard_async(const ptdr_c128* band, int n, int structure, int rank,
                                         int world, ptdr_c128* out_local, void* workspace,
                                         size_t ws_bytes, void* stream);
+
+/* ---- BAND(s): (2s+1)-band matrices (Table I l.500-518) -----------
+ * Input diags: device [2s+1][2^n], row d+s holds the d-th diagonal D_d[i] = A[i][i+d],
+ * d in [-s, s] (entries with i+d outside [0, 2^n) are ignored).  The coefficients can be
+ * nonzero only for the X-masks X_s = {0} U {i ^ (i+d) : 1 <= d <= s}, |X_s| = s n - c(s)
+ * (Table I); ptdr_band_xmasks lists them in ascending order, which is the block order of
+ * the output: out[b * 2^n + z] = coefficient of the string with X-mask xs[b] and Z-mask z
+ * (ascending z = ascending q within the block).  s = 0 is the diagonal, s = 1 the
+ * tridiagonal band (same values as DIAGONAL / TRIDIAGONAL).  Valid: 1 <= n <= 28,
+ * 0 <= s <= 64, s < 2^n. */
+size_t ptdr_band_xmask_count(int n, int s); /* 0 if invalid */
+ptdr_status ptdr_band_xmasks(int n, int s, uint64_t* xs_host, size_t cap);
+size_t ptdr_band_workspace_bytes(int n, int s); /* (size_t)-1 if invalid */
+/* workspace: device, >= ptdr_band_workspace_bytes, 256-byte aligned, disjoint from the
+ * operands; out: ptdr_band_xmask_count(n, s) * 2^n elements. */
+ptdr_status ptdr_decompose_band_async(const ptdr_c128* diags, int n, int s, ptdr_c128* out,
+                                      void* workspace, size_t ws_bytes, void* stream);
 
 /* Seeded counter-based generator (the paper fixes no
  * distribution, "a generic matrix", l.631).  Writes rows [row0, row0+nrows) of the

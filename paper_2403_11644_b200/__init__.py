@@ -19,6 +19,7 @@ STRUCTURES = {
     "real_symmetric": 2,
     "diagonal": 3,
     "tridiagonal": 4,
+    "anti_diagonal": 5,
 }
 PTDR_OK, PTDR_EINVAL, PTDR_EUNSUPPORTED, PTDR_ENOMEM, PTDR_ECUDA = 0, 1, 2, 3, 4
 
@@ -55,6 +56,14 @@ def lib():
         L.ptdr_decompose_xshard_async.argtypes = [vp, i32, i32, i32, vp, vp, sz, vp]
         L.ptdr_decompose_zshard_async.argtypes = [vp, i32, i32, i32, i32, vp, vp, sz, vp]
         L.ptdr_decompose_zshard_async.restype = i32
+        L.ptdr_band_xmask_count.argtypes = [i32, i32]
+        L.ptdr_band_xmask_count.restype = sz
+        L.ptdr_band_xmasks.argtypes = [i32, i32, ctypes.POINTER(ctypes.c_uint64), sz]
+        L.ptdr_band_xmasks.restype = i32
+        L.ptdr_band_workspace_bytes.argtypes = [i32, i32]
+        L.ptdr_band_workspace_bytes.restype = sz
+        L.ptdr_decompose_band_async.argtypes = [vp, i32, i32, vp, vp, sz, vp]
+        L.ptdr_decompose_band_async.restype = i32
         L.ptdr_generate_dense_async.argtypes = [i32, u64, i32, u64, u64, vp, vp]
         L.ptdr_generate_band_async.argtypes = [i32, u64, i32, vp, vp]
         L.ptdr_generate_sendblocks_async.argtypes = [i32, u64, i32, i32, vp, vp]
@@ -133,7 +142,7 @@ def n_of(A, structure="general") -> int:
         N = A.shape[-1]
         if A.dim() != 2 or A.shape[0] != N:
             raise ValueError("dense A must be 2^n x 2^n")
-    elif s == 3:
+    elif s in (3, 5):
         N = A.numel()
     else:
         N = A.numel() // 3
@@ -184,7 +193,7 @@ def decompose_host(A_host, structure="general", out_host=None):
         a = a.numpy()
     if a.dtype != np.complex128 or not a.flags.c_contiguous:
         raise TypeError("A_host must be C-contiguous complex128")
-    N = a.shape[-1] if s <= 2 else (a.size if s == 3 else a.size // 3)
+    N = a.shape[-1] if s <= 2 else (a.size // 3 if s == 4 else a.size)
     n = N.bit_length() - 1
     if out_host is None:
         out_host = np.empty(output_count(n, s), dtype=np.complex128)
@@ -285,6 +294,45 @@ def decompose_zshard(band, structure, rank: int, world: int, out=None, workspace
                                            ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
                                            _stream_ptr(stream))
     _check(st, "ptdr_decompose_zshard_async")
+    return out
+
+
+def band_xmasks(n: int, s: int):
+    """Ascending X-masks of the (2s+1)-band support (block order of decompose_band)."""
+    import numpy as np
+
+    cnt = int(lib().ptdr_band_xmask_count(n, s))
+    if cnt == 0:
+        raise PtdrError(PTDR_EINVAL, f"invalid (n={n}, s={s})")
+    xs = np.empty(cnt, dtype=np.uint64)
+    _check(lib().ptdr_band_xmasks(n, s, xs.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), cnt),
+           "ptdr_band_xmasks")
+    return xs
+
+
+def decompose_band(diags, s: int, out=None, workspace=None, stream=None):
+    """(2s+1)-band matrix given as diags[2s+1][2^n] (diags[d+s][i] = A[i][i+d]) -> the
+    [len(band_xmasks(n, s))][2^n] nonzero-X-mask coefficient blocks (ptdr_decompose_band_async)."""
+    import torch
+
+    _require_cuda_c128(diags, "diags")
+    if diags.dim() != 2 or diags.shape[0] != 2 * s + 1:
+        raise ValueError("diags must be [2s+1, 2^n]")
+    N = diags.shape[1]
+    n = N.bit_length() - 1
+    if (1 << n) != N:
+        raise ValueError("2^n columns")
+    cnt = int(lib().ptdr_band_xmask_count(n, s))
+    if out is None:
+        out = torch.empty(cnt * N, dtype=torch.complex128, device=diags.device)
+    _require_cuda_c128(out, "out")
+    if workspace is None:
+        nb = int(lib().ptdr_band_workspace_bytes(n, s))
+        workspace = torch.empty(max(nb, 1), dtype=torch.uint8, device=diags.device)
+    st = lib().ptdr_decompose_band_async(ctypes.c_void_p(diags.data_ptr()), n, s, ctypes.c_void_p(out.data_ptr()),
+                                         ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
+                                         _stream_ptr(stream))
+    _check(st, "ptdr_decompose_band_async")
     return out
 
 

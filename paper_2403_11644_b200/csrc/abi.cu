@@ -47,7 +47,7 @@ ptdr_status plan_fail(ptdr_status s, const char* msg) { return fail(s, msg); }
 ptdr_status plan_cuda_fail(cudaError_t e, const char* where) { return cuda_fail(e, where); }
 
 static bool is_dense(int s) { return s >= PTDR_GENERAL && s <= PTDR_REAL_SYMMETRIC; }
-static bool is_band(int s) { return s == PTDR_DIAGONAL || s == PTDR_TRIDIAGONAL; }
+static bool is_band(int s) { return s == PTDR_DIAGONAL || s == PTDR_TRIDIAGONAL || s == PTDR_ANTI_DIAGONAL; }
 static bool valid_n(int n, int s) {
   if (is_dense(s)) return n >= 1 && n <= 16;
   if (is_band(s)) return n >= 1 && n <= 28;
@@ -204,14 +204,14 @@ size_t ptdr_input_count(int n, int s) {
   if (!valid_n(n, s)) return 0;
   const size_t N = (size_t)1 << n;
   if (is_dense(s)) return N * N;
-  return s == PTDR_DIAGONAL ? N : 3 * N;
+  return s == PTDR_TRIDIAGONAL ? 3 * N : N;
 }
 
 size_t ptdr_output_count(int n, int s) {
   if (!valid_n(n, s)) return 0;
   const size_t N = (size_t)1 << n;
   if (is_dense(s)) return N * N;
-  return s == PTDR_DIAGONAL ? N : (size_t)(n + 1) * N;
+  return s == PTDR_TRIDIAGONAL ? (size_t)(n + 1) * N : N;
 }
 
 size_t ptdr_workspace_bytes(int n, int s, int world) {
@@ -312,7 +312,7 @@ ptdr_status ptdr_decompose_zshard_async(const ptdr_c128* band, int n, int struct
                                         ptdr_c128* out_local, void* workspace, size_t ws_bytes,
                                         void* stream) {
   g_last_launches = 0;
-  if (!is_band(structure)) return fail(PTDR_EINVAL, "z-sharding is for DIAGONAL / TRIDIAGONAL");
+  if (!is_band(structure)) return fail(PTDR_EINVAL, "z-sharding is for DIAGONAL / TRIDIAGONAL / ANTI_DIAGONAL");
   if (!valid_n(n, structure)) return fail(PTDR_EINVAL, "invalid n");
   if (world < 1 || (world & (world - 1))) return fail(PTDR_EINVAL, "world must be a power of two");
   if ((uint64_t)world > (1ull << n)) return fail(PTDR_EINVAL, "world > 2^n");
@@ -330,6 +330,39 @@ ptdr_status ptdr_decompose_zshard_async(const ptdr_c128* band, int n, int struct
                               structure, workspace, rank, world, reinterpret_cast<cudaStream_t>(stream), &nl);
   g_last_launches = nl;
   return e == cudaSuccess ? PTDR_OK : cuda_fail(e, "band kernel launch");
+}
+
+size_t ptdr_band_xmask_count(int n, int s) { return band_s_xmask_count(n, s); }
+
+ptdr_status ptdr_band_xmasks(int n, int s, uint64_t* xs, size_t cap) {
+  if (!xs) return fail(PTDR_EINVAL, "null xs");
+  const int r = band_s_xmasks(n, s, reinterpret_cast<unsigned long long*>(xs), cap);
+  if (r == -1) return fail(PTDR_EINVAL, "invalid n or s");
+  if (r == -2) return fail(PTDR_EINVAL, "xs capacity smaller than ptdr_band_xmask_count");
+  return PTDR_OK;
+}
+
+size_t ptdr_band_workspace_bytes(int n, int s) { return band_s_workspace_bytes(n, s); }
+
+ptdr_status ptdr_decompose_band_async(const ptdr_c128* diags, int n, int s, ptdr_c128* out, void* workspace,
+                                      size_t ws_bytes, void* stream) {
+  g_last_launches = 0;
+  const size_t cnt = band_s_xmask_count(n, s);
+  if (cnt == 0) return fail(PTDR_EINVAL, "invalid n or s (need 1 <= n <= 28, 0 <= s <= 64, s < 2^n)");
+  if (!diags || !out) return fail(PTDR_EINVAL, "null pointer");
+  if (((uintptr_t)diags & 15) || ((uintptr_t)out & 15)) return fail(PTDR_EINVAL, "misaligned");
+  const size_t need = band_s_workspace_bytes(n, s);
+  if (!workspace || ((uintptr_t)workspace & 255)) return fail(PTDR_EINVAL, "workspace missing or not 256-byte aligned");
+  if (ws_bytes < need) return fail(PTDR_ENOMEM, "workspace too small");
+  const size_t N = (size_t)1 << n;
+  if (overlaps(diags, (2 * (size_t)s + 1) * N * 16, out, cnt * N * 16)) return fail(PTDR_EUNSUPPORTED, "out overlaps the band");
+  if (overlaps(workspace, need, out, cnt * N * 16) || overlaps(workspace, need, diags, (2 * (size_t)s + 1) * N * 16))
+    return fail(PTDR_EINVAL, "workspace overlaps an operand");
+  int nl = 0;
+  cudaError_t e = launch_band_s(reinterpret_cast<const double2*>(diags), n, s, reinterpret_cast<double2*>(out),
+                                workspace, reinterpret_cast<cudaStream_t>(stream), &nl);
+  g_last_launches = nl;
+  return e == cudaSuccess ? PTDR_OK : cuda_fail(e, "band(s) kernel launch");
 }
 
 ptdr_status ptdr_decompose(const ptdr_c128* A, int n, int structure, ptdr_c128* out) {

@@ -9,6 +9,11 @@
 //   zl = z mod 2^{t+1}, zh = z >> (t+1), s1 = (-1)^{popcount(z mod 2^t)}, s2 = (-1)^{z_t}:
 //   alpha(x_b, z) = 2^-n i^{popcount(zl)} s1 (s1 == s2 ? P_t[zh] : M_t[zh]).
 //   DESIGN.md derives this from the per-x WHT identity.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
 #include "engine.cuh"
 #include "internal.h"
 
@@ -31,6 +36,16 @@ struct FlatLd {
 // zshift = 63 keeps everything (one GPU, or a workspace-targeted pass).
 __device__ __forceinline__ bool in_slice(u64 e, int zshift, u64 zrank) { return (e >> zshift) == zrank; }
 
+// Last-pass store of element e (= z of a single-vector family): scale, the phase
+// i^{popcount(px & z)} of a fixed X-mask px (ANTI_DIAGONAL: px = 2^n - 1; 0 otherwise) and the
+// slice filter.
+__device__ __forceinline__ void store_final(double2* out, u64 e, double2 v, double scale, int zshift,
+                                            u64 zrank, u64 px) {
+  if (!in_slice(e, zshift, zrank)) return;
+  if (px) v = rot_ipow(v, __popcll(px & e));
+  st_l2(out + (e - (zrank << zshift)), make_double2(v.x * scale, v.y * scale));
+}
+
 template <int K>
 struct FlatSt {
   double2* out;
@@ -39,10 +54,11 @@ struct FlatSt {
   double scale;
   int zshift;
   u64 zrank;
+  u64 px;
   __device__ __forceinline__ void operator()(int f, int j, double2 v) const {
     const u64 rho = rbase + (u64)f;
     const u64 e = ((rho >> b0) << (b0 + K)) | ((u64)j << b0) | (rho & ((1ull << b0) - 1ull));
-    if (in_slice(e, zshift, zrank)) st_l2(out + (e - (zrank << zshift)), make_double2(v.x * scale, v.y * scale));
+    store_final(out, e, v, scale, zshift, zrank, px);
   }
 };
 
@@ -59,7 +75,7 @@ constexpr int kBandSmem = kContigSlots * 16;  // >= kTileBytes: also the fiber_t
 static_assert(kBandSmem >= kTileBytes, "band tile buffer holds a full tile");
 
 __device__ __forceinline__ void contig8_tile(double2* S, const double2* in, double2* out, u64 base,
-                                             double scale, int zshift, u64 zrank) {
+                                             double scale, int zshift, u64 zrank, u64 px) {
   const int tid = threadIdx.x;
   double2 v[16];
   {
@@ -84,9 +100,8 @@ __device__ __forceinline__ void contig8_tile(double2* S, const double2* in, doub
     const int f = tid >> 4, jl = tid & 15;
 #pragma unroll
     for (int kk = 0; kk < 16; ++kk) {
-      const double2 w = S[contig_slot(f, jl + 16 * kk)];
-      const u64 e = base + (u64)(f * 256 + jl + 16 * kk);
-      if (in_slice(e, zshift, zrank)) st_l2(out + (e - (zrank << zshift)), make_double2(w.x * scale, w.y * scale));
+      store_final(out, base + (u64)(f * 256 + jl + 16 * kk), S[contig_slot(f, jl + 16 * kk)], scale, zshift,
+                  zrank, px);
     }
   }
 }
@@ -190,6 +205,7 @@ struct SegPass {
   double scale;
   int zshift;  // slice filter of the stores (63: none)
   unsigned long long zrank;
+  unsigned long long px;  // X-mask phase of the last pass (0: none)
 };
 constexpr int kMaxSeg = 40;
 struct SegPassTable {
@@ -199,7 +215,7 @@ struct SegPassTable {
 };
 
 __device__ __forceinline__ void small_wht_tile(double2* S, const double2* in, double2* out, int lam,
-                                               double scale, u64 e0, int zshift, u64 zrank) {
+                                               double scale, u64 e0, int zshift, u64 zrank, u64 px) {
   const int len = 1 << lam;
   for (int i = threadIdx.x; i < len; i += blockDim.x) S[i] = ld_l2(in + i);
   for (int sb = 0; sb < lam; ++sb) {
@@ -214,18 +230,14 @@ __device__ __forceinline__ void small_wht_tile(double2* S, const double2* in, do
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < len; i += blockDim.x) {
-    const double2 v = S[i];
-    const u64 e = e0 + (u64)i;
-    if (in_slice(e, zshift, zrank)) st_l2(out + (e - (zrank << zshift)), make_double2(v.x * scale, v.y * scale));
-  }
+  for (int i = threadIdx.x; i < len; i += blockDim.x) store_final(out, e0 + (u64)i, S[i], scale, zshift, zrank, px);
 }
 
 template <int K>
 __device__ __forceinline__ void flat_tile(double2* S, const SegPass& sp, u64 local) {
   constexpr int F = kTileElems >> K;
   FlatLd<K> ld{sp.in, local * F, sp.b0};
-  FlatSt<K> st{sp.out, local * F, sp.b0, sp.scale, sp.zshift, sp.zrank};
+  FlatSt<K> st{sp.out, local * F, sp.b0, sp.scale, sp.zshift, sp.zrank, sp.px};
   fiber_tile<K>(S, ld, st);
 }
 
@@ -239,9 +251,9 @@ __global__ void __launch_bounds__(kThreads, 2) seg_pass_kernel(const __grid_cons
     const u64 local = tile - sp.first_tile;
     if (sp.small) {
       const u64 off = local << sp.small_lam;
-      small_wht_tile(S, sp.in + off, sp.out, sp.small_lam, sp.scale, off, sp.zshift, sp.zrank);
+      small_wht_tile(S, sp.in + off, sp.out, sp.small_lam, sp.scale, off, sp.zshift, sp.zrank, sp.px);
     } else if (sp.b0 == 0 && sp.K == 8) {
-      contig8_tile(S, sp.in, sp.out, local * (u64)kTileElems, sp.scale, sp.zshift, sp.zrank);
+      contig8_tile(S, sp.in, sp.out, local * (u64)kTileElems, sp.scale, sp.zshift, sp.zrank, sp.px);
     } else {
       switch (sp.K) {
         case 1: flat_tile<1>(S, sp, local); break;
@@ -268,6 +280,7 @@ struct WhtFamily {
   double2* final_out = nullptr;  // output of the last pass (nullptr: `out`, in place)
   int zshift = 63;               // slice filter of the last pass (single-vector families)
   u64 zrank = 0;
+  u64 px = 0;                    // X-mask phase i^{popcount(px & z)} of the last pass
 };
 
 // Runs all passes for all families (at most 3 launches for lam <= 24).
@@ -294,6 +307,7 @@ static cudaError_t run_families(const WhtFamily* fam, int nfam, cudaStream_t st,
       double2* fin = w.final_out ? w.final_out : w.out;
       sp.zshift = 63;
       sp.zrank = 0;
+      sp.px = 0;
       if (w.lam <= 12) {
         if (p != 0) continue;
         sp.small = 1;
@@ -303,6 +317,7 @@ static cudaError_t run_families(const WhtFamily* fam, int nfam, cudaStream_t st,
         sp.scale = w.scale;
         sp.zshift = w.zshift;
         sp.zrank = w.zrank;
+        sp.px = w.px;
         sp.first_tile = tiles;
         tiles += w.count;
       } else {
@@ -318,6 +333,7 @@ static cudaError_t run_families(const WhtFamily* fam, int nfam, cudaStream_t st,
         if (last) {
           sp.zshift = w.zshift;
           sp.zrank = w.zrank;
+          sp.px = w.px;
         }
         sp.first_tile = tiles;
         tiles += (w.count << w.lam) / kTileElems;
@@ -364,8 +380,11 @@ cudaError_t launch_band(const double2* A, double2* out, int n, int structure, vo
     f.zrank = zrank;
     return f;
   };
-  if (structure == 3) {
+  if (structure == 3 || structure == 5) {
+    // DIAGONAL: x = 0.  ANTI_DIAGONAL: v_x[i] = A[i][i ^ (2^n - 1)] = a[i] is
+    // nonzero only for x = 2^n - 1, so alpha(2^n - 1, z) = 2^-n i^{popcount(z)} WHT(a)[z].
     WhtFamily f = x0_family(A);
+    if (structure == 5) f.px = N - 1;
     return run_families(&f, 1, st, nl);
   }
   // TRIDIAGONAL: A = [sub | main | sup]
@@ -400,6 +419,243 @@ cudaError_t launch_band(const double2* A, double2* out, int n, int structure, vo
       tridiag_expand_small_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(PM, out, n, scale, zs,
                                                                                  zrank);
     }
+    *nl += 1;
+    e = cudaGetLastError();
+  }
+  return e;
+}
+
+
+// =====================================================================================
+// BAND(s): (2s+1)-band matrices (Table I l.500-518).
+//
+// Input diags[d + s][i] = A[i][i + d], d in [-s, s].  For an X-mask x with top bit t,
+// v_x[i] = A[i][i ^ x] with i ^ x - i = x - 2 (i & x) (the high bits of i above t are
+// unchanged), so v_x[i] != 0 only if m = i & x satisfies |x - 2m| <= s, a condition on the
+// low t+1 bits l of i alone.  Writing i = h 2^{t+1} + l:
+//   WHT_n(v_x)[z] = sum_{l in L_x} (-1)^{popcount(l & z_lo)} W_{x,l}[z_hi],
+//   W_{x,l} = WHT_{n-t-1}(h -> D_{x - 2(l & x)}[h 2^{t+1} + l]),
+// z_lo = z mod 2^{t+1}, z_hi = z >> (t+1), and alpha(x, z) = 2^-n i^{popcount(x & z)}
+// WHT_n(v_x)[z].  L_x = {m | f : m subset of x, |x - 2m| <= s, f subset of the zero bits of
+// x below t+1}.  x is in the support X_s iff L_x is non-empty; that forces
+// x >= 2^{t+1} - s, so at most s candidates per top bit (|X_s| = s n - c(s), Table I).
+// The tridiagonal path is s = 1 with the two segments folded into P/M; x = 0 is the main
+// diagonal (t = -1, one segment of length 2^n).
+// =====================================================================================
+struct BandBlockDev {
+  unsigned long long x;
+  int t;      // top bit of x (-1 for x = 0)
+  int nL;     // segments of this block
+  int first;  // index into the segment-reference list
+  int pad;
+};
+struct BandSegRef {
+  unsigned long long l;
+  unsigned long long off;  // element offset of W_{x,l} in the segment storage
+};
+
+struct BandPlan {
+  int n = 0, s = 0;
+  std::vector<BandBlockDev> blocks;
+  std::vector<BandSegRef> refs;
+  std::vector<int> seg_d, seg_t, seg_lam;  // per segment (same order as refs)
+  std::vector<int> fam_lam;                // families: lam and their [first, count) in refs
+  std::vector<int> fam_count;
+  std::vector<unsigned long long> fam_off;  // storage offset of each family
+  unsigned long long seg_elems = 0;
+  size_t table_bytes = 0, ws_bytes = 0;
+};
+
+static bool band_member(unsigned long long x, int s) {
+  // exists m subset of x with |x - 2m| <= s
+  const long long lo = ((long long)x - s + 1) / 2 > 0 ? ((long long)x - s + 1) / 2 : 0;
+  const long long hi = ((long long)x + s) / 2;
+  for (long long m = lo; m <= hi && m <= (long long)x; ++m)
+    if (((unsigned long long)m & ~x) == 0ull && std::llabs((long long)x - 2 * m) <= s) return true;
+  return false;
+}
+
+static BandPlan make_band_plan(int n, int s) {
+  BandPlan p;
+  p.n = n;
+  p.s = s;
+  struct Seg { unsigned long long x, l; int t, d, lam, block; };
+  std::vector<Seg> segs;
+  auto add_block = [&](unsigned long long x, int t) {
+    BandBlockDev b{};
+    b.x = x;
+    b.t = t;
+    b.first = 0;
+    b.nL = 0;
+    const int lam = n - t - 1;
+    const int blk = (int)p.blocks.size();
+    if (t < 0) {
+      segs.push_back({0ull, 0ull, -1, 0, n, blk});
+      b.nL = 1;
+    } else {
+      const unsigned long long F = (~x) & ((2ull << t) - 1ull);  // free bits
+      const long long lo = ((long long)x - s + 1) / 2 > 0 ? ((long long)x - s + 1) / 2 : 0;
+      for (long long m = lo; m <= ((long long)x + s) / 2 && m <= (long long)x; ++m) {
+        if (((unsigned long long)m & ~x) != 0ull || std::llabs((long long)x - 2 * m) > s) continue;
+        // every submask f of F
+        unsigned long long f = 0;
+        for (;;) {
+          segs.push_back({x, (unsigned long long)m | f, t, (int)((long long)x - 2 * m), lam, blk});
+          ++b.nL;
+          if (f == F) break;
+          f = (f - F) & F;  // next submask in increasing order
+        }
+      }
+    }
+    p.blocks.push_back(b);
+  };
+  add_block(0ull, -1);
+  for (int t = 0; t < n; ++t) {
+    const unsigned long long top = 1ull << t, hi = (2ull << t) - 1ull;
+    const unsigned long long lo = (hi + 1 > (unsigned long long)s && hi + 1 - s > top) ? hi + 1 - s : top;
+    for (unsigned long long x = lo; x <= hi; ++x)
+      if (band_member(x, s)) add_block(x, t);
+  }
+  // storage grouped by lam (one WHT family per length), refs in block order
+  std::vector<int> order(segs.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return segs[a].lam > segs[b].lam; });
+  std::vector<unsigned long long> off(segs.size());
+  unsigned long long cur = 0;
+  for (size_t k = 0; k < order.size(); ++k) {
+    const Seg& sg = segs[order[k]];
+    if (p.fam_lam.empty() || p.fam_lam.back() != sg.lam) {
+      p.fam_lam.push_back(sg.lam);
+      p.fam_off.push_back(cur);
+      p.fam_count.push_back(0);
+    }
+    ++p.fam_count.back();
+    off[order[k]] = cur;
+    cur += 1ull << sg.lam;
+  }
+  p.seg_elems = cur;
+  // refs grouped per block (segments were appended block by block)
+  int first = 0;
+  for (size_t bi = 0; bi < p.blocks.size(); ++bi) {
+    p.blocks[bi].first = first;
+    first += p.blocks[bi].nL;
+  }
+  p.refs.resize(segs.size());
+  p.seg_d.resize(segs.size());
+  p.seg_t.resize(segs.size());
+  p.seg_lam.resize(segs.size());
+  for (size_t k = 0; k < segs.size(); ++k) {
+    p.refs[k] = BandSegRef{segs[k].l, off[k]};
+    p.seg_d[k] = segs[k].d;
+    p.seg_t[k] = segs[k].t;
+    p.seg_lam[k] = segs[k].lam;
+  }
+  const size_t tb = p.blocks.size() * sizeof(BandBlockDev) + p.refs.size() * sizeof(BandSegRef) +
+                    segs.size() * sizeof(int4);
+  p.table_bytes = (tb + 255) / 256 * 256;
+  p.ws_bytes = p.table_bytes + (size_t)p.seg_elems * 16;
+  return p;
+}
+
+// Gather: seg[h] = diags[d + s][h 2^{t+1} + l] for every segment; one thread per element.
+// gat[k] = {t, d, lam, unused} per segment (segment order = refs order).
+__global__ void band_gather_kernel(const double2* diags, int n, int s, const BandSegRef* refs,
+                                   const int4* gat, int nseg, double2* segs) {
+  const u64 N = 1ull << n;
+  for (int k = blockIdx.y; k < nseg; k += gridDim.y) {
+    const int4 g = gat[k];
+    const u64 len = 1ull << g.z;
+    const u64 l = refs[k].l;
+    const int sh = g.x + 1;  // t + 1 (0 for x = 0)
+    const double2* D = diags + (u64)(g.y + s) * N;
+    double2* dst = segs + refs[k].off;
+    for (u64 h = (u64)blockIdx.x * blockDim.x + threadIdx.x; h < len; h += (u64)gridDim.x * blockDim.x)
+      dst[h] = ld_stream(D + ((h << sh) | l));
+  }
+}
+
+// Expansion: out[b][z] = 2^-n i^{popcount(x_b & z)} sum_k (-1)^{popcount(l_k & z_lo)} W_k[z_hi].
+__global__ void __launch_bounds__(256) band_expand_kernel(const BandBlockDev* blocks, const BandSegRef* refs,
+                                                          const double2* segs, int nblocks, int n,
+                                                          double scale, double2* out) {
+  const u64 N = 1ull << n;
+  for (int b = blockIdx.y; b < nblocks; b += gridDim.y) {
+    const BandBlockDev B = blocks[b];
+    const int sh = B.t + 1;
+    const u64 lomask = (1ull << sh) - 1ull;
+    for (u64 z = (u64)blockIdx.x * blockDim.x + threadIdx.x; z < N; z += (u64)gridDim.x * blockDim.x) {
+      const u64 zlo = z & lomask, zhi = z >> sh;
+      double re = 0.0, im = 0.0;
+      for (int k = 0; k < B.nL; ++k) {
+        const BandSegRef r = refs[B.first + k];
+        const double2 w = __ldg(segs + r.off + zhi);
+        if (__popcll(r.l & zlo) & 1) { re -= w.x; im -= w.y; }
+        else { re += w.x; im += w.y; }
+      }
+      const double2 c = rot_ipow(make_double2(re, im), __popcll(B.x & z));
+      st_stream(out + (u64)b * N + z, make_double2(c.x * scale, c.y * scale));
+    }
+  }
+}
+
+static bool band_args_ok(int n, int s) { return n >= 1 && n <= 28 && s >= 0 && s <= 64 && (1ll << n) > s; }
+
+size_t band_s_xmask_count(int n, int s) {
+  if (!band_args_ok(n, s)) return 0;
+  return make_band_plan(n, s).blocks.size();
+}
+int band_s_xmasks(int n, int s, unsigned long long* xs, size_t cap) {
+  if (!band_args_ok(n, s)) return -1;
+  BandPlan p = make_band_plan(n, s);
+  if (cap < p.blocks.size()) return -2;
+  for (size_t i = 0; i < p.blocks.size(); ++i) xs[i] = p.blocks[i].x;
+  return (int)p.blocks.size();
+}
+size_t band_s_workspace_bytes(int n, int s) {
+  if (!band_args_ok(n, s)) return (size_t)-1;
+  return make_band_plan(n, s).ws_bytes;
+}
+
+cudaError_t launch_band_s(const double2* diags, int n, int s, double2* out, void* ws, cudaStream_t st,
+                          int* nl) {
+  BandPlan p = make_band_plan(n, s);
+  const int nseg = (int)p.refs.size(), nb = (int)p.blocks.size();
+  char* base = reinterpret_cast<char*>(ws);
+  BandBlockDev* dblocks = reinterpret_cast<BandBlockDev*>(base);
+  BandSegRef* drefs = reinterpret_cast<BandSegRef*>(base + nb * sizeof(BandBlockDev));
+  int4* dgat = reinterpret_cast<int4*>(base + nb * sizeof(BandBlockDev) + nseg * sizeof(BandSegRef));
+  double2* segs = reinterpret_cast<double2*>(base + p.table_bytes);
+  std::vector<char> host(p.table_bytes, 0);
+  memcpy(host.data(), p.blocks.data(), nb * sizeof(BandBlockDev));
+  memcpy(host.data() + nb * sizeof(BandBlockDev), p.refs.data(), nseg * sizeof(BandSegRef));
+  std::vector<int4> gat(nseg);
+  for (int k = 0; k < nseg; ++k) gat[k] = make_int4(p.seg_t[k], p.seg_d[k], p.seg_lam[k], 0);
+  memcpy(host.data() + nb * sizeof(BandBlockDev) + nseg * sizeof(BandSegRef), gat.data(), nseg * sizeof(int4));
+  // pageable source: the call returns once the bytes are staged, so `host` may go
+  cudaError_t e = cudaMemcpyAsync(base, host.data(), p.table_bytes, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return e;
+  const int sms = device_sm_count();
+  {
+    dim3 grid((unsigned)(sms * 4 > 1 ? sms * 4 : 1), (unsigned)(nseg < 65535 ? nseg : 65535));
+    // long segments dominate; short ones use a few threads of their row of blocks
+    band_gather_kernel<<<grid, 256, 0, st>>>(diags, n, s, drefs, dgat, nseg, segs);
+    *nl += 1;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  // WHT of every segment, in place (one family per length)
+  std::vector<WhtFamily> fam;
+  for (size_t f = 0; f < p.fam_lam.size(); ++f)
+    fam.push_back(WhtFamily{segs + p.fam_off[f], segs + p.fam_off[f], p.fam_lam[f], (u64)p.fam_count[f], 1.0});
+  for (size_t f0 = 0; f0 < fam.size(); f0 += kMaxSeg) {
+    const int cnt = (int)(fam.size() - f0 < (size_t)kMaxSeg ? fam.size() - f0 : kMaxSeg);
+    if ((e = run_families(fam.data() + f0, cnt, st, nl)) != cudaSuccess) return e;
+  }
+  {
+    const u64 N = 1ull << n;
+    u64 gx = (N + 255) / 256;
+    if (gx > (u64)sms * 8) gx = (u64)sms * 8;
+    dim3 grid((unsigned)gx, (unsigned)(nb < 65535 ? nb : 65535));
+    band_expand_kernel<<<grid, 256, 0, st>>>(dblocks, drefs, segs, nb, n, ldexp(1.0, -n), out);
     *nl += 1;
     e = cudaGetLastError();
   }

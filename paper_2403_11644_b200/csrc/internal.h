@@ -28,6 +28,13 @@ size_t band_workspace_bytes(int n, int structure, int world);
 cudaError_t launch_band(const double2* A, double2* out, int n, int structure, void* ws, int rank,
                         int world, cudaStream_t st, int* nl);
 
+// BAND(s) (band.cu)
+size_t band_s_xmask_count(int n, int s);
+int band_s_xmasks(int n, int s, unsigned long long* xs, size_t cap);
+size_t band_s_workspace_bytes(int n, int s);
+cudaError_t launch_band_s(const double2* diags, int n, int s, double2* out, void* ws, cudaStream_t st,
+                          int* nl);
+
 // generators (generate.cu)
 cudaError_t launch_generate_dense(int n, uint64_t seed, int variant, uint64_t row0,
                                   uint64_t nrows, double2* A, cudaStream_t st);

@@ -109,3 +109,32 @@ def test_plan_validation_without_gpu(L):
     assert L.ptdr_plan_create(10, 0, 1, None) == ptdr.PTDR_EINVAL                # null out
     assert L.ptdr_plan_wait(None) == ptdr.PTDR_EINVAL
     assert L.ptdr_plan_destroy(None) == ptdr.PTDR_OK
+
+
+@pytest.mark.parametrize("s", [0, 1, 2, 3, 4, 5, 8])
+def test_band_xmask_list_matches_definition(L, s):
+    """Host planner of BAND(s): the block list is {0} U {i ^ (i+d) : 1 <= d <= s}, ascending,
+    of size s n - c(s) (PAPER Table I, l.500-518) -- brute force for small n, count for large."""
+    import numpy as np
+
+    for n in range(max(1, s.bit_length()), 11):
+        if (1 << n) <= s:
+            continue
+        xs = ptdr.band_xmasks(n, s)
+        N = 1 << n
+        want = sorted({0} | {i ^ (i + d) for d in range(1, s + 1) for i in range(N - d)})
+        assert xs.tolist() == want, (n, s)
+    if s >= 1:
+        Lg = s.bit_length() - 1
+        cs = s * (Lg + 1) - (1 << (Lg + 1))
+        for n in (16, 24, 28):
+            assert L.ptdr_band_xmask_count(n, s) == s * n - cs
+    assert L.ptdr_band_xmask_count(0, s) == 0
+    assert L.ptdr_band_xmask_count(29, s) == 0
+
+
+def test_anti_diagonal_counts(L):
+    assert ptdr.input_count(10, "anti_diagonal") == 1 << 10
+    assert ptdr.output_count(10, "anti_diagonal") == 1 << 10
+    assert ptdr.workspace_bytes(24, "anti_diagonal") == 0
+    assert L.ptdr_max_n(5) == 28

@@ -76,6 +76,36 @@ def band(name, n, seed, variant):
     torch.cuda.empty_cache()
 
 
+def band_s(name, n, s):
+    """(2s+1)-band: seeded N(0,1) diagonals, all nonzero-X-mask blocks."""
+    g = torch.Generator(device="cuda").manual_seed(5)
+    diags = torch.complex(torch.randn(2 * s + 1, 1 << n, generator=g, device="cuda", dtype=torch.float64),
+                          torch.randn(2 * s + 1, 1 << n, generator=g, device="cuda", dtype=torch.float64))
+    nb = len(ptdr.band_xmasks(n, s))
+    out = torch.empty(nb << n, dtype=torch.complex128, device="cuda")
+    ws = torch.empty(int(ptdr.lib().ptdr_band_workspace_bytes(n, s)), dtype=torch.uint8, device="cuda")
+    ms = time_it(lambda: ptdr.decompose_band(diags, s, out=out, workspace=ws))
+    alg = (diags.numel() + out.numel()) * 16
+    print(json.dumps({"config": name, "n": n, "s": s, "blocks": nb, "ms": ms,
+                      "coeffs_per_s": out.numel() / (ms * 1e-3), "alg_bytes": alg,
+                      "hbm_gbs": alg / (ms * 1e-3) / 1e9, "frac_of_measured": alg / (ms * 1e-3) / 1e9 / PEAK,
+                      "launches": ptdr.last_launch_count()}), flush=True)
+    del diags, out, ws
+    torch.cuda.empty_cache()
+
+
+def anti(name, n):
+    g = torch.Generator(device="cuda").manual_seed(6)
+    a = torch.complex(torch.randn(1 << n, generator=g, device="cuda", dtype=torch.float64),
+                      torch.randn(1 << n, generator=g, device="cuda", dtype=torch.float64))
+    out = torch.empty(1 << n, dtype=torch.complex128, device="cuda")
+    ms = time_it(lambda: ptdr.decompose(a, "anti_diagonal", out=out))
+    alg = 32 * (1 << n)
+    print(json.dumps({"config": name, "n": n, "ms": ms, "coeffs_per_s": (1 << n) / (ms * 1e-3),
+                      "hbm_gbs": alg / (ms * 1e-3) / 1e9, "frac_of_measured": alg / (ms * 1e-3) / 1e9 / PEAK,
+                      "launches": ptdr.last_launch_count()}), flush=True)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["all"]
     if "all" in which or "small" in which:
@@ -89,6 +119,10 @@ if __name__ == "__main__":
     if "all" in which or "band" in which:
         band("n24tri", 24, 3, "tridiagonal")
         band("n24diag", 24, 3, "diagonal")
+    if "all" in which or "next" in which:
+        anti("n24anti", 24)
+        band_s("n24band_s2", 24, 2)
+        band_s("n22band_s5", 22, 5)
     if "all" in which or "big" in which:
         dense("n15", 15, 4, "general")
         dense("n15_hermitian", 15, 4, "hermitian")

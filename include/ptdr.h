@@ -154,6 +154,35 @@ size_t ptdr_band_workspace_bytes(int n, int s); /* (size_t)-1 if invalid */
 ptdr_status ptdr_decompose_band_async(const ptdr_c128* diags, int n, int s, ptdr_c128* out,
                                       void* workspace, size_t ws_bytes, void* stream);
 
+/* ---- Decomposition algebra and the inverse transform (Sec. IV-B, l.521-627) ----
+ * All coefficient arrays are device complex128 in q order.  A new leftmost qubit makes
+ * the output four consecutive blocks of 4^n, one per leading letter I, X, Y, Z. */
+
+/* Inverse transform A = sum_P alpha_P P (l.116-121): dense row-major A [2^n][2^n] from the
+ * 4^n q-ordered coefficients.  Same path as the decomposition run backwards (per X-mask:
+ * conjugate phase, WHT over z, XOR scatter into rows).  workspace >= 16 * 4^n bytes
+ * (ptdr_reconstruct_workspace_bytes), 256-byte aligned; coeffs, A, workspace disjoint. */
+size_t ptdr_reconstruct_workspace_bytes(int n);
+ptdr_status ptdr_reconstruct_async(const ptdr_c128* coeffs, int n, ptdr_c128* A, void* workspace,
+                                   size_t ws_bytes, void* stream);
+/* Linear combination (l.570-577): out = mu x + nu y elementwise over `count` coefficients
+ * (decomposition of mu A + nu B from those of A and B).  out may alias x or y. */
+ptdr_status ptdr_axpby_async(ptdr_c128* out, double mu_re, double mu_im, const ptdr_c128* x,
+                             double nu_re, double nu_im, const ptdr_c128* y, size_t count,
+                             void* stream);
+/* Block diagonal diag(A_0, ..., A_{2^k-1}) (l.524-568; k = 1 is the direct sum A_0 (+) A_1,
+ * l.537-540): blocks = [2^k][4^n] coefficient arrays of the A_j (A_j occupies rows and
+ * columns [j 2^n, (j+1) 2^n)); out = [4^(n+k)].  The output strings whose k leading letters
+ * are in {I, Z} with Z-mask zt carry 2^-k sum_j (-1)^{popcount(j & zt)} alpha_j; all others
+ * are 0.  1 <= k <= 4, n + k <= 16. */
+ptdr_status ptdr_block_diag_async(const ptdr_c128* blocks, int n, int k, ptdr_c128* out,
+                                  void* stream);
+/* Hermitian augmentation [[0, A^*], [A, 0]] = X (x) Re A + Y (x) Im A (l.590-627): out =
+ * [4^(n+1)] with the X block = Re alpha, the Y block = Im alpha (imaginary parts exactly 0),
+ * I and Z blocks 0. */
+ptdr_status ptdr_hermitian_augment_async(const ptdr_c128* coeffs, int n, ptdr_c128* out,
+                                         void* stream);
+
 /* Seeded counter-based generator (the paper fixes no
  * distribution, "a generic matrix", l.631).  Writes rows [row0, row0+nrows) of the
  * dense variant (0 GENERAL, 1 HERMITIAN, 2 REAL_SYMMETRIC) into A (row-major,

@@ -64,6 +64,16 @@ def lib():
         L.ptdr_band_workspace_bytes.restype = sz
         L.ptdr_decompose_band_async.argtypes = [vp, i32, i32, vp, vp, sz, vp]
         L.ptdr_decompose_band_async.restype = i32
+        dbl = ctypes.c_double
+        L.ptdr_reconstruct_workspace_bytes.argtypes = [i32]
+        L.ptdr_reconstruct_workspace_bytes.restype = sz
+        L.ptdr_reconstruct_async.argtypes = [vp, i32, vp, vp, sz, vp]
+        L.ptdr_axpby_async.argtypes = [vp, dbl, dbl, vp, dbl, dbl, vp, sz, vp]
+        L.ptdr_block_diag_async.argtypes = [vp, i32, i32, vp, vp]
+        L.ptdr_hermitian_augment_async.argtypes = [vp, i32, vp, vp]
+        for name in ("ptdr_reconstruct_async", "ptdr_axpby_async", "ptdr_block_diag_async",
+                     "ptdr_hermitian_augment_async"):
+            getattr(L, name).restype = i32
         L.ptdr_generate_dense_async.argtypes = [i32, u64, i32, u64, u64, vp, vp]
         L.ptdr_generate_band_async.argtypes = [i32, u64, i32, vp, vp]
         L.ptdr_generate_sendblocks_async.argtypes = [i32, u64, i32, i32, vp, vp]
@@ -333,6 +343,85 @@ def decompose_band(diags, s: int, out=None, workspace=None, stream=None):
                                          ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
                                          _stream_ptr(stream))
     _check(st, "ptdr_decompose_band_async")
+    return out
+
+
+def _n_of_coeffs(c) -> int:
+    n = (c.numel().bit_length() - 1) // 2
+    if 4 ** n != c.numel():
+        raise ValueError("coefficient arrays hold 4^n elements")
+    return n
+
+
+def reconstruct(coeffs, out=None, workspace=None, stream=None):
+    """Inverse transform A = sum_P alpha_P P (ptdr_reconstruct_async): [2^n, 2^n] complex128."""
+    import torch
+
+    _require_cuda_c128(coeffs, "coeffs")
+    n = _n_of_coeffs(coeffs)
+    if out is None:
+        out = torch.empty((1 << n, 1 << n), dtype=torch.complex128, device=coeffs.device)
+    _require_cuda_c128(out, "out")
+    if workspace is None:
+        workspace = torch.empty(int(lib().ptdr_reconstruct_workspace_bytes(n)), dtype=torch.uint8,
+                                device=coeffs.device)
+    _check(lib().ptdr_reconstruct_async(ctypes.c_void_p(coeffs.data_ptr()), n, ctypes.c_void_p(out.data_ptr()),
+                                        ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
+                                        _stream_ptr(stream)), "ptdr_reconstruct_async")
+    return out
+
+
+def axpby(mu, x, nu, y, out=None, stream=None):
+    """Coefficients of mu A + nu B from those of A (x) and B (y) (ptdr_axpby_async)."""
+    import torch
+
+    _require_cuda_c128(x, "x")
+    _require_cuda_c128(y, "y")
+    if x.numel() != y.numel():
+        raise ValueError("x and y sizes differ")
+    if out is None:
+        out = torch.empty_like(x)
+    mu, nu = complex(mu), complex(nu)
+    _check(lib().ptdr_axpby_async(ctypes.c_void_p(out.data_ptr()), mu.real, mu.imag, ctypes.c_void_p(x.data_ptr()),
+                                  nu.real, nu.imag, ctypes.c_void_p(y.data_ptr()), x.numel(), _stream_ptr(stream)),
+           "ptdr_axpby_async")
+    return out
+
+
+def block_diag(blocks, out=None, stream=None):
+    """Coefficients of diag(A_0, ..., A_{2^k-1}) from blocks[2^k][4^n] (ptdr_block_diag_async)."""
+    import torch
+
+    _require_cuda_c128(blocks, "blocks")
+    nb = blocks.shape[0]
+    k = nb.bit_length() - 1
+    if (1 << k) != nb or blocks.dim() != 2:
+        raise ValueError("blocks must be [2^k, 4^n]")
+    n = _n_of_coeffs(blocks[0])
+    if out is None:
+        out = torch.empty(4 ** (n + k), dtype=torch.complex128, device=blocks.device)
+    _check(lib().ptdr_block_diag_async(ctypes.c_void_p(blocks.data_ptr()), n, k, ctypes.c_void_p(out.data_ptr()),
+                                       _stream_ptr(stream)), "ptdr_block_diag_async")
+    return out
+
+
+def direct_sum(a, b, out=None, stream=None):
+    """Coefficients of A (+) B (l.537-540) = block_diag with k = 1."""
+    import torch
+
+    return block_diag(torch.stack([a, b]).contiguous(), out=out, stream=stream)
+
+
+def hermitian_augment(coeffs, out=None, stream=None):
+    """Coefficients of [[0, A^*], [A, 0]] (ptdr_hermitian_augment_async)."""
+    import torch
+
+    _require_cuda_c128(coeffs, "coeffs")
+    n = _n_of_coeffs(coeffs)
+    if out is None:
+        out = torch.empty(4 ** (n + 1), dtype=torch.complex128, device=coeffs.device)
+    _check(lib().ptdr_hermitian_augment_async(ctypes.c_void_p(coeffs.data_ptr()), n, ctypes.c_void_p(out.data_ptr()),
+                                              _stream_ptr(stream)), "ptdr_hermitian_augment_async")
     return out
 
 

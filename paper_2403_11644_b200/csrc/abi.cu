@@ -365,6 +365,69 @@ ptdr_status ptdr_decompose_band_async(const ptdr_c128* diags, int n, int s, ptdr
   return e == cudaSuccess ? PTDR_OK : cuda_fail(e, "band(s) kernel launch");
 }
 
+// ---- algebra and inverse transform (algebra.cu) ---------------------------------------
+size_t ptdr_reconstruct_workspace_bytes(int n) {
+  if (n < 1 || n > 16) return (size_t)-1;
+  return reconstruct_workspace_bytes(n);
+}
+
+ptdr_status ptdr_reconstruct_async(const ptdr_c128* coeffs, int n, ptdr_c128* A, void* workspace,
+                                   size_t ws_bytes, void* stream) {
+  g_last_launches = 0;
+  if (n < 1 || n > 16) return fail(PTDR_EINVAL, "invalid n (1..16)");
+  if (!coeffs || !A || !workspace) return fail(PTDR_EINVAL, "null pointer");
+  if (((uintptr_t)coeffs & 15) || ((uintptr_t)A & 15) || ((uintptr_t)workspace & 255))
+    return fail(PTDR_EINVAL, "misaligned pointer");
+  const size_t nb = (size_t)16 << (2 * n);
+  if (ws_bytes < reconstruct_workspace_bytes(n)) return fail(PTDR_ENOMEM, "workspace too small");
+  if (overlaps(coeffs, nb, A, nb) || overlaps(workspace, nb, A, nb) || overlaps(workspace, nb, coeffs, nb))
+    return fail(PTDR_EUNSUPPORTED, "coeffs, A and workspace must be disjoint");
+  int nl = 0;
+  cudaError_t e = launch_reconstruct(reinterpret_cast<const double2*>(coeffs), n, reinterpret_cast<double2*>(A),
+                                     workspace, reinterpret_cast<cudaStream_t>(stream), &nl);
+  g_last_launches = nl;
+  return e == cudaSuccess ? PTDR_OK : cuda_fail(e, "reconstruct launch");
+}
+
+ptdr_status ptdr_axpby_async(ptdr_c128* out, double mu_re, double mu_im, const ptdr_c128* x, double nu_re,
+                             double nu_im, const ptdr_c128* y, size_t count, void* stream) {
+  g_last_launches = 0;
+  if (!out || !x || !y) return fail(PTDR_EINVAL, "null pointer");
+  if (((uintptr_t)out | (uintptr_t)x | (uintptr_t)y) & 15) return fail(PTDR_EINVAL, "misaligned pointer");
+  if (count == 0) return PTDR_OK;
+  cudaError_t e = launch_axpby(reinterpret_cast<double2*>(out), make_double2(mu_re, mu_im),
+                               reinterpret_cast<const double2*>(x), make_double2(nu_re, nu_im),
+                               reinterpret_cast<const double2*>(y), count, reinterpret_cast<cudaStream_t>(stream));
+  g_last_launches = 1;
+  return e == cudaSuccess ? PTDR_OK : cuda_fail(e, "axpby launch");
+}
+
+ptdr_status ptdr_block_diag_async(const ptdr_c128* blocks, int n, int k, ptdr_c128* out, void* stream) {
+  g_last_launches = 0;
+  if (n < 1 || k < 1 || k > 4 || n + k > 16) return fail(PTDR_EINVAL, "need n >= 1, 1 <= k <= 4, n + k <= 16");
+  if (!blocks || !out) return fail(PTDR_EINVAL, "null pointer");
+  if (((uintptr_t)blocks | (uintptr_t)out) & 15) return fail(PTDR_EINVAL, "misaligned pointer");
+  const size_t in_b = ((size_t)16 << (2 * n)) << k, out_b = (size_t)16 << (2 * (n + k));
+  if (overlaps(blocks, in_b, out, out_b)) return fail(PTDR_EUNSUPPORTED, "out overlaps the blocks");
+  cudaError_t e = launch_block_diag(reinterpret_cast<const double2*>(blocks), n, k, reinterpret_cast<double2*>(out),
+                                    reinterpret_cast<cudaStream_t>(stream));
+  g_last_launches = 1;
+  return e == cudaSuccess ? PTDR_OK : cuda_fail(e, "block_diag launch");
+}
+
+ptdr_status ptdr_hermitian_augment_async(const ptdr_c128* coeffs, int n, ptdr_c128* out, void* stream) {
+  g_last_launches = 0;
+  if (n < 1 || n > 15) return fail(PTDR_EINVAL, "need 1 <= n <= 15");
+  if (!coeffs || !out) return fail(PTDR_EINVAL, "null pointer");
+  if (((uintptr_t)coeffs | (uintptr_t)out) & 15) return fail(PTDR_EINVAL, "misaligned pointer");
+  if (overlaps(coeffs, (size_t)16 << (2 * n), out, (size_t)64 << (2 * n)))
+    return fail(PTDR_EUNSUPPORTED, "out overlaps the input");
+  cudaError_t e = launch_herm_augment(reinterpret_cast<const double2*>(coeffs), n, reinterpret_cast<double2*>(out),
+                                      reinterpret_cast<cudaStream_t>(stream));
+  g_last_launches = 1;
+  return e == cudaSuccess ? PTDR_OK : cuda_fail(e, "hermitian_augment launch");
+}
+
 ptdr_status ptdr_decompose(const ptdr_c128* A, int n, int structure, ptdr_c128* out) {
   if (!valid_n(n, structure)) return fail(PTDR_EINVAL, "invalid n or structure");
   const size_t need = ptdr_workspace_bytes(n, structure, 1);

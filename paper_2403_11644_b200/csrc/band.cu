@@ -16,6 +16,7 @@
 
 #include "engine.cuh"
 #include "internal.h"
+#include "wht_passes.h"
 
 namespace ptdr {
 
@@ -270,21 +271,8 @@ __global__ void __launch_bounds__(kThreads, 2) seg_pass_kernel(const __grid_cons
   }
 }
 
-// A vector family for the pass planner: `count` contiguous vectors of 2^lam elements.
-struct WhtFamily {
-  const double2* in;  // input of pass 0
-  double2* out;       // output of every pass but the last (later passes in place)
-  int lam;
-  u64 count;
-  double scale;       // applied on the last pass
-  double2* final_out = nullptr;  // output of the last pass (nullptr: `out`, in place)
-  int zshift = 63;               // slice filter of the last pass (single-vector families)
-  u64 zrank = 0;
-  u64 px = 0;                    // X-mask phase i^{popcount(px & z)} of the last pass
-};
-
 // Runs all passes for all families (at most 3 launches for lam <= 24).
-static cudaError_t run_families(const WhtFamily* fam, int nfam, cudaStream_t st, int* nl) {
+cudaError_t run_families(const WhtFamily* fam, int nfam, cudaStream_t st, int* nl) {
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(seg_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

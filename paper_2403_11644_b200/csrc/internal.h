@@ -35,6 +35,14 @@ size_t band_s_workspace_bytes(int n, int s);
 cudaError_t launch_band_s(const double2* diags, int n, int s, double2* out, void* ws, cudaStream_t st,
                           int* nl);
 
+// algebra and inverse transform (algebra.cu)
+size_t reconstruct_workspace_bytes(int n);
+cudaError_t launch_reconstruct(const double2* c, int n, double2* A, void* ws, cudaStream_t st, int* nl);
+cudaError_t launch_axpby(double2* out, double2 mu, const double2* x, double2 nu, const double2* y,
+                         unsigned long long count, cudaStream_t st);
+cudaError_t launch_block_diag(const double2* blocks, int n, int k, double2* out, cudaStream_t st);
+cudaError_t launch_herm_augment(const double2* a, int n, double2* out, cudaStream_t st);
+
 // generators (generate.cu)
 cudaError_t launch_generate_dense(int n, uint64_t seed, int variant, uint64_t row0,
                                   uint64_t nrows, double2* A, cudaStream_t st);

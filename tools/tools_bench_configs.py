@@ -106,6 +106,22 @@ def anti(name, n):
                       "launches": ptdr.last_launch_count()}), flush=True)
 
 
+def inverse(name, n):
+    """Inverse transform: coefficients -> A, round trip checked."""
+    A = ptdr.generate_dense(n, 4, "general", device="cuda")
+    c = ptdr.decompose(A)
+    B = torch.empty_like(A)
+    ws = torch.empty(int(ptdr.lib().ptdr_reconstruct_workspace_bytes(n)), dtype=torch.uint8, device="cuda")
+    ms = time_it(lambda: ptdr.reconstruct(c, out=B, workspace=ws))
+    err = max(torch.max(torch.abs(A[i:i + 1024] - B[i:i + 1024])).item() for i in range(0, A.shape[0], 1024))
+    alg = 32 * 4 ** n
+    print(json.dumps({"config": name, "n": n, "ms": ms, "coeffs_per_s": 4 ** n / (ms * 1e-3),
+                      "hbm_gbs": alg / (ms * 1e-3) / 1e9, "frac_of_measured": alg / (ms * 1e-3) / 1e9 / PEAK,
+                      "round_trip_max_err": err, "launches": ptdr.last_launch_count()}), flush=True)
+    del A, B, c, ws
+    torch.cuda.empty_cache()
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["all"]
     if "all" in which or "small" in which:
@@ -123,6 +139,7 @@ if __name__ == "__main__":
         anti("n24anti", 24)
         band_s("n24band_s2", 24, 2)
         band_s("n22band_s5", 22, 5)
+        inverse("n15_inverse", 15)
     if "all" in which or "big" in which:
         dense("n15", 15, 4, "general")
         dense("n15_hermitian", 15, 4, "hermitian")

@@ -38,6 +38,7 @@ struct DenseArgs {
   int L;
   int nslot;
   int discard;         // pipeline: discard consumed scratch lines from L2 (no write-back)
+  int interleave;      // pipeline: steady-state tickets alternate B(c) / A(c+L+1) tiles
   unsigned long long* trace;  // pipeline debug timeline (nullptr unless PTDR_TRACE=1)
   double scale;        // 2^-n
 };

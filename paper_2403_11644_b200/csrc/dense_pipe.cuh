@@ -174,7 +174,7 @@ __device__ __forceinline__ void emit_all(const DenseArgs& a, const EpiUnit<NB, (
 
 // Ticket order of dense_impl.cuh's decode_ticket, 32-bit, NA = NB = 2^M.
 __device__ __forceinline__ void decode_ticket32(uint32_t t, int M, uint32_t C, uint32_t L, int& phase,
-                                                uint32_t& chunk, uint32_t& tile) {
+                                                uint32_t& chunk, uint32_t& tile, int interleave = 0) {
   const uint32_t NA = 1u << M;
   const uint32_t lp1 = (L + 1u < C) ? L + 1u : C;
   const uint32_t pro = lp1 << M;
@@ -186,7 +186,10 @@ __device__ __forceinline__ void decode_ticket32(uint32_t t, int M, uint32_t C, u
   const uint32_t steady = C > L + 1u ? C - L - 1u : 0u;
   if (t < (steady << (M + 1))) {
     const uint32_t c = t >> (M + 1), o = t & (2u * NA - 1u);
-    if (o < NA) { phase = 1; chunk = c; tile = o; }
+    if (interleave) {
+      if (o & 1u) { phase = 0; chunk = c + L + 1u; tile = o >> 1; }
+      else { phase = 1; chunk = c; tile = o >> 1; }
+    } else if (o < NA) { phase = 1; chunk = c; tile = o; }
     else { phase = 0; chunk = c + L + 1u; tile = o - NA; }
     return;
   }
@@ -372,7 +375,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
         depX = nullptr;
         dvX = 0;
         if (tk < total) {
-          decode_ticket32(tk, M, C, (uint32_t)a.L, phX, chX, tlX);
+          decode_ticket32(tk, M, C, (uint32_t)a.L, phX, chX, tlX, a.interleave);
           if (phX == 1) depX = &doneA[chX];
           else if (chX >= nslot) depX = &doneB[chX - nslot];
           if (depX) dvX = ld_relaxed(depX);

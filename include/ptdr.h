@@ -115,6 +115,18 @@ ptdr_status ptdr_decompose_async(const ptdr_c128* A, int n, int structure, ptdr_
 ptdr_status ptdr_decompose_host(const ptdr_c128* A_host, int n, int structure,
                                 ptdr_c128* out_host);
 
+/* Zero padding ("we can use a zero padding to make any size of matrix
+ * fit this constraint"): A is an m x m matrix of a dense structure stored row-major with
+ * row pitch lda >= m (elements); it is decomposed as the top-left block of a 2^n x 2^n
+ * zero matrix, n = max(1, ceil(log2 m)), and out receives the 4^n coefficients in q order.
+ * GENERAL matrices on the TMA pipeline (n >= 11) are read in place (out-of-bounds boxes
+ * are zero-filled by the TMA unit); everything else is first copied into a zero-padded
+ * workspace buffer.  m = 0 (empty) is EINVAL.  workspace >= ptdr_padded_workspace_bytes. */
+size_t ptdr_padded_workspace_bytes(uint64_t m, int structure); /* (size_t)-1 if invalid */
+ptdr_status ptdr_decompose_padded_async(const ptdr_c128* A, uint64_t m, uint64_t lda,
+                                        int structure, ptdr_c128* out, void* workspace,
+                                        size_t ws_bytes, void* stream);
+
 /* Multi-GPU, per rank, GENERAL only, after the caller's all-to-all (DESIGN.md
  * "Multi-GPU").  world = 2^g GPUs, R = 2^n / world.  Rank `rank` owns the X-masks
  * x with x >> (n-g) == rank.  A_local: device [2^n][R] row-major with

@@ -74,6 +74,10 @@ def lib():
         for name in ("ptdr_reconstruct_async", "ptdr_axpby_async", "ptdr_block_diag_async",
                      "ptdr_hermitian_augment_async"):
             getattr(L, name).restype = i32
+        L.ptdr_padded_workspace_bytes.argtypes = [u64, i32]
+        L.ptdr_padded_workspace_bytes.restype = sz
+        L.ptdr_decompose_padded_async.argtypes = [vp, u64, u64, i32, vp, vp, sz, vp]
+        L.ptdr_decompose_padded_async.restype = i32
         L.ptdr_generate_dense_async.argtypes = [i32, u64, i32, u64, u64, vp, vp]
         L.ptdr_generate_band_async.argtypes = [i32, u64, i32, vp, vp]
         L.ptdr_generate_sendblocks_async.argtypes = [i32, u64, i32, i32, vp, vp]
@@ -282,6 +286,35 @@ def decompose_xshard(A_local, n: int, rank: int, world: int, out=None, workspace
                                            ctypes.c_void_p(workspace.data_ptr()),
                                            workspace.numel(), _stream_ptr(stream))
     _check(st, "ptdr_decompose_xshard_async")
+    return out
+
+
+def decompose_padded(A, structure="general", out=None, workspace=None, stream=None):
+    """Any m x m dense matrix (a CUDA complex128 view with unit column stride, any row
+    pitch) decomposed as the top-left block of the zero-padded 2^n x 2^n matrix,
+    n = max(1, ceil(log2 m)) (ptdr_decompose_padded_async)."""
+    import torch
+
+    if not isinstance(A, torch.Tensor) or not A.is_cuda or A.dtype != torch.complex128:
+        raise TypeError("A must be a CUDA complex128 tensor (no CPU fallback)")
+    if A.dim() != 2 or A.shape[0] != A.shape[1] or A.stride(1) != 1:
+        raise ValueError("A must be square with unit column stride")
+    m, lda = A.shape[0], A.stride(0)
+    s = _structure(structure)
+    if m == 0:  # the ABI rejects an empty matrix (EINVAL)
+        _check(lib().ptdr_decompose_padded_async(None, 0, 0, s, None, None, 0, _stream_ptr(stream)),
+               "ptdr_decompose_padded_async")
+    n = max(1, (m - 1).bit_length())
+    if out is None:
+        out = torch.empty(4 ** n, dtype=torch.complex128, device=A.device)
+    _require_cuda_c128(out, "out")
+    if workspace is None:
+        nb = int(lib().ptdr_padded_workspace_bytes(m, s))
+        workspace = torch.empty(max(nb, 1), dtype=torch.uint8, device=A.device)
+    _check(lib().ptdr_decompose_padded_async(ctypes.c_void_p(A.data_ptr()), m, lda, s,
+                                             ctypes.c_void_p(out.data_ptr()),
+                                             ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
+                                             _stream_ptr(stream)), "ptdr_decompose_padded_async")
     return out
 
 

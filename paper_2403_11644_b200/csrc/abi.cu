@@ -141,13 +141,18 @@ static DenseArgs base_args(const double2* A, double2* out, int n, void* ws) {
 }
 
 static ptdr_status run_dense(const double2* A, int n, int s, double2* out, void* ws,
-                             cudaStream_t st, int* nl) {
+                             cudaStream_t st, int* nl, uint64_t lda = 0, uint64_t m = 0) {
   const uint64_t N = 1ull << n;
   if (s == PTDR_GENERAL || n <= 8) {
     const int mode = s == PTDR_GENERAL ? MODE_GENERAL
                      : s == PTDR_HERMITIAN ? MODE_HERM_MIRROR : MODE_SYM_MIRROR;
     DensePlan p = plan_for(mode, n, N);
     DenseArgs a = base_args(A, out, n, ws);
+    if (m) {  // zero-padded view (TMA pipeline only, see ptdr_decompose_padded_async)
+      a.ld = lda;
+      a.rows_valid = m;
+      a.cols_valid = m;
+    }
     a.nv = n;
     a.x_base = 0;
     a.nchunks = p.nchunks;
@@ -426,6 +431,80 @@ ptdr_status ptdr_hermitian_augment_async(const ptdr_c128* coeffs, int n, ptdr_c1
                                       reinterpret_cast<cudaStream_t>(stream));
   g_last_launches = 1;
   return e == cudaSuccess ? PTDR_OK : cuda_fail(e, "hermitian_augment launch");
+}
+
+// ---- zero padding -------------------------------------------------------
+__global__ void pad_copy_kernel(const double2* __restrict__ A, uint64_t m, uint64_t lda, int n,
+                                double2* __restrict__ P) {
+  const uint64_t N = 1ull << n;
+  for (uint64_t id = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; id < N * N;
+       id += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = id >> n, j = id & (N - 1);
+    P[id] = (i < m && j < m) ? A[i * lda + j] : make_double2(0.0, 0.0);
+  }
+}
+
+static int padded_n(uint64_t m) {
+  int n = 1;
+  while ((1ull << n) < m && n < 63) ++n;
+  return n;
+}
+// GENERAL with the TMA pipeline reads the stored block in place (out-of-bounds boxes are
+// zero-filled); every other case copies into a zero-padded 2^n x 2^n workspace buffer.
+static bool padded_in_place(int n, int structure) {
+  return structure == PTDR_GENERAL && plan_for(MODE_GENERAL, n, 1ull << n).pipe_cfg != kPipeNone &&
+         plan_for(MODE_GENERAL, n, 1ull << n).kind == 2;
+}
+
+size_t ptdr_padded_workspace_bytes(uint64_t m, int structure) {
+  if (m < 1 || !is_dense(structure)) return (size_t)-1;
+  const int n = padded_n(m);
+  if (n > 16) return (size_t)-1;
+  const size_t base = ptdr_workspace_bytes(n, structure, 1);
+  const bool exact = (1ull << n) == m;
+  if (exact || padded_in_place(n, structure)) return base;
+  return ((((size_t)16 << (2 * n)) + 255) / 256) * 256 + base;
+}
+
+ptdr_status ptdr_decompose_padded_async(const ptdr_c128* A, uint64_t m, uint64_t lda, int structure,
+                                        ptdr_c128* out, void* workspace, size_t ws_bytes, void* stream) {
+  g_last_launches = 0;
+  if (!is_dense(structure)) return fail(PTDR_EINVAL, "zero padding is for the dense structures");
+  if (m < 1) return fail(PTDR_EINVAL, "m must be >= 1 (an empty matrix has no decomposition)");
+  if (lda < m) return fail(PTDR_EINVAL, "lda < m");
+  const int n = padded_n(m);
+  if (n > 16) return fail(PTDR_EINVAL, "m > 65536");
+  if (!A || !out) return fail(PTDR_EINVAL, "null pointer");
+  if (((uintptr_t)A & 15) || ((uintptr_t)out & 15)) return fail(PTDR_EINVAL, "misaligned pointer");
+  const size_t need = ptdr_padded_workspace_bytes(m, structure);
+  if (need > 0 && (!workspace || ((uintptr_t)workspace & 255)))
+    return fail(PTDR_EINVAL, "workspace missing or not 256-byte aligned");
+  if (ws_bytes < need) return fail(PTDR_ENOMEM, "workspace too small");
+  const size_t inb = ((m - 1) * lda + m) * 16, outb = (size_t)16 << (2 * n);
+  if (overlaps(A, inb, out, outb)) return fail(PTDR_EUNSUPPORTED, "out overlaps A");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bool exact = (1ull << n) == m;
+  if (exact && lda == m) return ptdr_decompose_async(A, n, structure, out, workspace, ws_bytes, stream);
+  int nl = 0;
+  ptdr_status r;
+  if (padded_in_place(n, structure)) {
+    r = run_dense(reinterpret_cast<const double2*>(A), n, structure, reinterpret_cast<double2*>(out), workspace, st,
+                  &nl, lda, m);
+  } else {
+    const size_t pad_b = ((((size_t)16 << (2 * n)) + 255) / 256) * 256;
+    double2* P = reinterpret_cast<double2*>(workspace);
+    const uint64_t N = 1ull << n;
+    uint64_t g = (N * N + 255) / 256;
+    if (g > (uint64_t)device_sm_count() * 16) g = (uint64_t)device_sm_count() * 16;
+    pad_copy_kernel<<<(unsigned)g, 256, 0, st>>>(reinterpret_cast<const double2*>(A), m, lda, n, P);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "pad copy launch");
+    r = ptdr_decompose_async(reinterpret_cast<const ptdr_c128*>(P), n, structure, out,
+                             reinterpret_cast<char*>(workspace) + pad_b, ws_bytes - pad_b, stream);
+    nl = 1 + g_last_launches;
+  }
+  g_last_launches = nl;
+  return r;
 }
 
 ptdr_status ptdr_decompose(const ptdr_c128* A, int n, int structure, ptdr_c128* out) {

@@ -39,6 +39,8 @@ struct DenseArgs {
   int nslot;
   int discard;         // pipeline: discard consumed scratch lines from L2 (no write-back)
   int interleave;      // pipeline: steady-state tickets alternate B(c) / A(c+L+1) tiles
+  u64 rows_valid;      // zero padding: rows / columns of A actually stored;
+  u64 cols_valid;      // 0 = all (the TMA tensor map fills the rest with zeros)
   unsigned long long* trace;  // pipeline debug timeline (nullptr unless PTDR_TRACE=1)
   double scale;        // 2^-n
 };

@@ -59,7 +59,10 @@ cudaError_t launch_dense_pipe(int mode, const DenseArgs& a_in, const DensePlan& 
   PFN_cuTensorMapEncodeTiled_v12000 enc = encode_fn();
   if (!enc) return cudaErrorNotSupported;
   CUtensorMap map;
-  const cuuint64_t ncols = a.colmask + 1, nrows = 1ull << a.n;
+  // zero padding: the tensor map covers only the stored rows_valid x
+  // cols_valid block; TMA fills every out-of-bounds element of a box with zeros.
+  const cuuint64_t ncols = a.cols_valid ? a.cols_valid : a.colmask + 1;
+  const cuuint64_t nrows = a.rows_valid ? a.rows_valid : 1ull << a.n;
   cuuint64_t gdim[2] = {2 * ncols, nrows};
   cuuint64_t gstride[1] = {a.ld * 16};
   const cuuint32_t W = (cuuint32_t)p.W;

@@ -138,3 +138,16 @@ def test_anti_diagonal_counts(L):
     assert ptdr.output_count(10, "anti_diagonal") == 1 << 10
     assert ptdr.workspace_bytes(24, "anti_diagonal") == 0
     assert L.ptdr_max_n(5) == 28
+
+
+def test_padded_workspace_rules(L):
+    """Zero padding (PAPER l.118): m = 0 is invalid; powers of two need no pad buffer;
+    GENERAL at n >= 11 reads in place; everything else adds a 2^n x 2^n pad buffer."""
+    inval = ctypes.c_size_t(-1).value
+    assert L.ptdr_padded_workspace_bytes(0, 0) == inval
+    assert L.ptdr_padded_workspace_bytes(65537, 0) == inval
+    assert L.ptdr_padded_workspace_bytes(5, 3) == inval                        # band structure
+    assert L.ptdr_padded_workspace_bytes(1024, 0) == ptdr.workspace_bytes(10, "general")
+    assert L.ptdr_padded_workspace_bytes(3000, 0) == ptdr.workspace_bytes(12, "general")
+    assert L.ptdr_padded_workspace_bytes(1000, 0) >= 16 * 4 ** 10
+    assert L.ptdr_padded_workspace_bytes(3000, 1) >= 16 * 4 ** 12 + ptdr.workspace_bytes(12, "hermitian")

@@ -31,11 +31,17 @@ namespace ptdr {
 // Developer diagnostics (PTDR_DIAG_BUILD=<bits>; never in the product library):
 //   bit 0: phase B computes but does not store the output (isolates the read side);
 //   bit 1: phase-A TMA loads come from the first 256 rows of A (L2-resident: isolates
-//          the write side).
+//          the write side);
+//   bit 2: no butterflies (pure data movement through the same pipeline).
 #ifndef PTDR_DIAG
 #define PTDR_DIAG 0
 #endif
 constexpr int kDiag = PTDR_DIAG;
+// bit 2 (diagnostics): skip the radix butterflies (data movement only)
+template <int B>
+__device__ __forceinline__ void pwht(double2* v) {
+  if constexpr ((kDiag & 4) == 0) wht_regs<B>(v);
+}
 
 struct TileMeta {
   int valid, phase, tile, seq;
@@ -555,7 +561,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       if (gtid == 0) trace_stamp(a.trace, k, 6);
-      wht_regs<4>(v);
+      pwht<4>(v);
       constexpr int R2 = R - 4;
       constexpr int UA = (W * 16) / GT;   // second-stage units per thread, 2^R2 registers each
       double2* X = xbuf + g * Cfg::XE;
@@ -572,12 +578,12 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
         exchange_rounds<R2, UA, W>(v, X, jh, u, bar_id, GT);
 #pragma unroll
         for (int p = 0; p < UA; ++p) {
-          wht_regs<R2>(&v[p * (1 << R2)]);
+          pwht<R2>(&v[p * (1 << R2)]);
           store_unit(&v[p * (1 << R2)], jh + (1 << R2) * p);
         }
       } else {
         xor_half_transpose<W>(v, X, jh, u, bar_id, GT);
-        wht_regs<4>(v);
+        pwht<4>(v);
         store_unit(v, jh);
       }
       signal(j, &doneA[chunk]);
@@ -593,7 +599,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
           v[kk] = S[r * W + ((r & (W - 1)) ^ u)];
           if (MODE == MODE_SYM_HALF) v[kk].y = 0.0;
         }
-        wht_regs<4>(v);
+        pwht<4>(v);
         __syncwarp();  // rows of this jh are read and written only by this warp
 #pragma unroll
         for (int kk = 0; kk < 16; ++kk) S[(jh * 16 + kk) * W + u] = v[kk];
@@ -617,7 +623,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
       for (int p = 0; p < UA; ++p) {
         const int uu = gtid + GT * p;
         const int u = uu & (W - 1), jl = uu >> XB;
-        wht_regs<R2>(&v[p * (1 << R2)]);
+        pwht<R2>(&v[p * (1 << R2)]);
         // element (u, ih = tile, zl = j*16 + jl) -> Y[tileB][ih][f]
         const uint32_t phi_lo = phi_of<XB>((uint32_t)u, (uint32_t)jl);
         double2* base = Y + (((phi_lo >> LFB) << LT) | ((uint32_t)m.tile << LFB) | (phi_lo & (FB - 1)));
@@ -653,7 +659,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         if (gtid == 0) trace_stamp(a.trace, k, 6);
-        wht_regs<4>(v);
+        pwht<4>(v);
         constexpr int R2 = M - 4;
         constexpr int UB = (FB * 16) / GT;
         double2* X = xbuf + g * Cfg::XE;
@@ -668,12 +674,12 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
           exchange_rounds<R2, UB, FB>(v, X, jh, f, bar_id, GT);
 #pragma unroll
           for (int p = 0; p < UB; ++p) {
-            wht_regs<R2>(&v[p * (1 << R2)]);
+            pwht<R2>(&v[p * (1 << R2)]);
             emit_unit(&v[p * (1 << R2)], jh + (1 << R2) * p);
           }
         } else {
           xor_half_transpose<FB>(v, X, jh, f, bar_id, GT);
-          wht_regs<4>(v);
+          pwht<4>(v);
           emit_unit(v, jh);
         }
         signal(j, &doneB[chunk]);
@@ -687,7 +693,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
 #pragma unroll
         for (int kk = 0; kk < 16; ++kk) v[kk] = S[(jh * 16 + kk) * FB + f];
       }
-      wht_regs<4>(v);
+      pwht<4>(v);
       if constexpr (M == 4) {
         named_bar_sync(bar_id, GT);
         discard_tile();
@@ -721,7 +727,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
           const int uu = gtid + GT * p;
           const int f2 = uu % FB, jl = uu / FB;
           const uint32_t phi = (uint32_t)m.tile * FB + (uint32_t)f2;
-          wht_regs<R2>(&v[p * (1 << R2)]);
+          pwht<R2>(&v[p * (1 << R2)]);
           EpiUnit<R2, HALF> e;
           e.init((uint32_t)x0 + phi_u_of<XB>(phi), ((uint32_t)jl << R) | phi_zl_of<XB>(phi), R + 4, t,
                  a.gshift);

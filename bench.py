@@ -43,6 +43,9 @@ def _args():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
+                   help="N > 1: NCCL all-to-all then per-rank decomposition, or the fused "
+                        "peer-pull kernel (TMA loads of the owners' row blocks over NVLink)")
     return p.parse_args()
 
 
@@ -200,6 +203,10 @@ def main():
         A = ptdr.generate_dense(n, SEED, "general", device=dev)
         out = torch.empty(coeffs_total, dtype=torch.complex128, device=dev)
         ws = ptdr.alloc_workspace(n, "general", 1, dev)
+    elif a.exchange == "peer":
+        shard = ptdr.generate_dense(n, SEED, "general", row0=rank * (N // world), nrows=N // world, device=dev)
+        out = torch.empty(coeffs_total // world, dtype=torch.complex128, device=dev)
+        ws = ptdr.alloc_workspace(n, "general", world, dev)
     else:
         send = ptdr.generate_sendblocks(n, SEED, rank, world, device=dev)
         recv = torch.empty_like(send)
@@ -208,6 +215,10 @@ def main():
     g1.record(stream)
     torch.cuda.synchronize()
     gen_ms = g0.elapsed_time(g1)
+    peer_ptrs, peer_close = None, None
+    if world > 1 and a.exchange == "peer":
+        peer_ptrs, peer_close = pdist.open_peer_shards(shard)
+        dist.barrier()
 
     ev_kernel = []
 
@@ -217,6 +228,14 @@ def main():
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
             ptdr.decompose(A, "general", out=out, workspace=ws, stream=stream)
+            if record:
+                e1.record(stream)
+                ev_kernel.append((e0, e1))
+        elif peer_ptrs is not None:
+            if record:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            pdist.decompose_peer_sharded(shard, n, peer_ptrs, out=out, workspace=ws, stream=stream)
             if record:
                 e1.record(stream)
                 ev_kernel.append((e0, e1))
@@ -299,7 +318,9 @@ def main():
                        "input_bytes": 16 * coeffs_total,
                        "l2": "inputs 16 GiB >> 126 MB L2 (no flush needed)",
                        "parallelism": "single GPU" if world == 1 else
-                       f"X-mask shards over {world} GPUs, 1 NCCL all-to-all"},
+                       (f"X-mask shards over {world} GPUs, fused peer-pull (TMA over NVLink)"
+                        if peer_ptrs is not None else
+                        f"X-mask shards over {world} GPUs, 1 NCCL all-to-all")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_kind": peak_kind, "kernel": "dense_pipe_kernel (PTDR_PIPE_CFG=%s)" % os.environ.get("PTDR_PIPE_CFG", "default"),
@@ -353,6 +374,10 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
+        if peer_close is not None:
+            torch.cuda.synchronize()
+            dist.barrier()
+            peer_close()
         dist.destroy_process_group()
     return 0
 

@@ -138,6 +138,30 @@ ptdr_status ptdr_decompose_xshard_async(const ptdr_c128* A_local, int n, int ran
                                         ptdr_c128* out_local, void* workspace, size_t ws_bytes,
                                         void* stream);
 
+/* Multi-GPU, per rank, GENERAL, fused exchange ("peer pull"):
+ * instead of an all-to-all, the phase-A tiles of rank `rank`'s X-masks are loaded by TMA
+ * straight from the row-block shard of the rank that owns the rows, over NVLink.
+ * shards: HOST array of `world` device pointers (2, 4 or 8 ranks), shards[r] = rows
+ * [r R, (r+1) R) of A, row-major with row pitch 2^n (R = 2^n / world), each readable from
+ * this GPU (its own allocation, or a peer's opened with ptdr_ipc_open).  The shards must
+ * stay unmodified until the call's work on `stream` completes (and on the peers' side
+ * until every rank has finished: the caller synchronises, e.g. with a barrier).
+ * out_local: same layout as ptdr_decompose_xshard_async.  workspace: as for
+ * ptdr_workspace_bytes(n, GENERAL, world).  Requires n - log2(world) >= 11 (EUNSUPPORTED
+ * otherwise).  Bitwise identical to the all-to-all path. */
+ptdr_status ptdr_decompose_peer_async(const ptdr_c128* const* shards, int n, int rank, int world,
+                                      ptdr_c128* out_local, void* workspace, size_t ws_bytes,
+                                      void* stream);
+/* CUDA IPC of a shard allocation between the ranks' processes (thin wrappers of
+ * cudaIpcGetMemHandle / cudaIpcOpenMemHandle / cudaIpcCloseMemHandle): the handle is an
+ * opaque blob of ptdr_ipc_handle_size() bytes naming the whole allocation that contains
+ * dev_ptr, and *offset is dev_ptr's byte offset inside it; the peer adds the offset to
+ * the pointer ptdr_ipc_open returns.  The caller exchanges handle and offset. */
+size_t ptdr_ipc_handle_size(void);
+ptdr_status ptdr_ipc_get_handle(const void* dev_ptr, void* handle, uint64_t* offset);
+ptdr_status ptdr_ipc_open(const void* handle, void** dev_ptr);
+ptdr_status ptdr_ipc_close(void* dev_ptr);
+
 /* Multi-GPU, per rank, DIAGONAL / TRIDIAGONAL (replicated band,
  * z-sharded output, no communication).  Every rank holds the whole band (input layout as
  * for ptdr_decompose_async) and writes the z-slice z in [rank 2^(n-g), (rank+1) 2^(n-g))

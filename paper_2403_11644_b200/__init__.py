@@ -78,6 +78,14 @@ def lib():
         L.ptdr_padded_workspace_bytes.restype = sz
         L.ptdr_decompose_padded_async.argtypes = [vp, u64, u64, i32, vp, vp, sz, vp]
         L.ptdr_decompose_padded_async.restype = i32
+        L.ptdr_decompose_peer_async.argtypes = [ctypes.POINTER(vp), i32, i32, i32, vp, vp, sz, vp]
+        L.ptdr_decompose_peer_async.restype = i32
+        L.ptdr_ipc_handle_size.restype = sz
+        L.ptdr_ipc_get_handle.argtypes = [vp, vp, ctypes.POINTER(u64)]
+        L.ptdr_ipc_open.argtypes = [vp, ctypes.POINTER(vp)]
+        L.ptdr_ipc_close.argtypes = [vp]
+        for name in ("ptdr_ipc_get_handle", "ptdr_ipc_open", "ptdr_ipc_close"):
+            getattr(L, name).restype = i32
         L.ptdr_generate_dense_async.argtypes = [i32, u64, i32, u64, u64, vp, vp]
         L.ptdr_generate_band_async.argtypes = [i32, u64, i32, vp, vp]
         L.ptdr_generate_sendblocks_async.argtypes = [i32, u64, i32, i32, vp, vp]
@@ -316,6 +324,49 @@ def decompose_padded(A, structure="general", out=None, workspace=None, stream=No
                                              ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
                                              _stream_ptr(stream)), "ptdr_decompose_padded_async")
     return out
+
+
+def decompose_peer(shard_ptrs, n: int, rank: int, world: int, out=None, workspace=None, stream=None,
+                   device=None):
+    """Per-rank decomposition reading every rank's row-block shard directly (TMA over
+    NVLink; ptdr_decompose_peer_async).  shard_ptrs: device addresses (ints) of the
+    `world` shards, in rank order, all readable from this GPU."""
+    import torch
+
+    if len(shard_ptrs) != world:
+        raise ValueError("one shard pointer per rank")
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if out is None:
+        out = torch.empty((1 << (2 * n)) // world, dtype=torch.complex128, device=dev)
+    _require_cuda_c128(out, "out")
+    if workspace is None:
+        workspace = alloc_workspace(n, "general", world, dev)
+    arr = (ctypes.c_void_p * world)(*[ctypes.c_void_p(int(p)) for p in shard_ptrs])
+    _check(lib().ptdr_decompose_peer_async(arr, n, rank, world, ctypes.c_void_p(out.data_ptr()),
+                                           ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
+                                           _stream_ptr(stream)), "ptdr_decompose_peer_async")
+    return out
+
+
+def ipc_handle(tensor):
+    """(opaque CUDA IPC handle of the allocation holding `tensor`, byte offset of the tensor)."""
+    size = int(lib().ptdr_ipc_handle_size())
+    buf = ctypes.create_string_buffer(size)
+    off = ctypes.c_uint64()
+    _check(lib().ptdr_ipc_get_handle(ctypes.c_void_p(tensor.data_ptr()), buf, ctypes.byref(off)),
+           "ptdr_ipc_get_handle")
+    return buf.raw, int(off.value)
+
+
+def ipc_open(handle: bytes) -> int:
+    """Map a peer allocation; returns its base device address (add the peer's offset)."""
+    p = ctypes.c_void_p()
+    _check(lib().ptdr_ipc_open(ctypes.c_char_p(handle), ctypes.byref(p)), "ptdr_ipc_open")
+    return int(p.value)
+
+
+def ipc_close(ptr: int):
+    _check(lib().ptdr_ipc_close(ctypes.c_void_p(ptr)), "ptdr_ipc_close")
 
 
 def decompose_zshard(band, structure, rank: int, world: int, out=None, workspace=None, stream=None):

@@ -1,5 +1,6 @@
 // abi.cu -- the C ABI of libptdr.so (include/ptdr.h): validation, workspace
 // layout and dispatch to the kernels.  No torch types, no exceptions across the ABI.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -311,6 +312,89 @@ ptdr_status ptdr_decompose_xshard_async(const ptdr_c128* A_local, int n, int ran
   ptdr_status r = launch_mode(MODE_GENERAL, a, p, reinterpret_cast<cudaStream_t>(stream), &nl);
   g_last_launches = nl;
   return r;
+}
+
+// ---- fused exchange: peer-pull X-mask decomposition --------------------
+ptdr_status ptdr_decompose_peer_async(const ptdr_c128* const* shards, int n, int rank, int world,
+                                      ptdr_c128* out_local, void* workspace, size_t ws_bytes, void* stream) {
+  g_last_launches = 0;
+  if (world < 2 || world > 8 || (world & (world - 1))) return fail(PTDR_EINVAL, "world must be 2, 4 or 8");
+  if (rank < 0 || rank >= world) return fail(PTDR_EINVAL, "rank out of range");
+  if (!valid_n(n, PTDR_GENERAL)) return fail(PTDR_EINVAL, "invalid n");
+  if (!shards || !out_local) return fail(PTDR_EINVAL, "null pointer");
+  const int g = __builtin_ctz((unsigned)world);
+  const uint64_t N = 1ull << n, R = N >> g;
+  for (int r = 0; r < world; ++r)
+    if (!shards[r] || ((uintptr_t)shards[r] & 15)) return fail(PTDR_EINVAL, "null or misaligned shard pointer");
+  if ((uintptr_t)out_local & 15) return fail(PTDR_EINVAL, "misaligned out");
+  DensePlan p = plan_for(MODE_GENERAL, n, R);
+  if (p.kind != 2 || p.pipe_cfg == kPipeNone || R < 128)
+    return fail(PTDR_EUNSUPPORTED, "peer-pull needs the TMA pipeline: n - log2(world) >= 11");
+  const size_t need = ptdr_workspace_bytes(n, PTDR_GENERAL, world);
+  if (need > 0 && (!workspace || ((uintptr_t)workspace & 255)))
+    return fail(PTDR_EINVAL, "workspace missing or not 256-byte aligned");
+  if (ws_bytes < need) return fail(PTDR_ENOMEM, "workspace too small");
+  DenseArgs a = base_args(reinterpret_cast<const double2*>(shards[rank]), reinterpret_cast<double2*>(out_local),
+                          n, workspace);
+  a.ld = N;                 // shard rows are full matrix rows
+  a.colmask = N - 1;
+  a.gshift = n - g;
+  a.nv = n;
+  a.x_base = (uint64_t)rank * R;
+  a.nchunks = p.nchunks;
+  a.scratch = reinterpret_cast<double2*>(reinterpret_cast<char*>(workspace) + p.ctr_bytes);
+  a.peer_shift = n - g;
+  a.peer_rowmask = R - 1;
+  a.npeers = world;
+  for (int r = 0; r < world; ++r) a.peer_ptrs[r] = reinterpret_cast<const double2*>(shards[r]);
+  int nl = 0;
+  ptdr_status st = launch_mode(MODE_GENERAL, a, p, reinterpret_cast<cudaStream_t>(stream), &nl);
+  g_last_launches = nl;
+  return st;
+}
+
+size_t ptdr_ipc_handle_size(void) { return sizeof(cudaIpcMemHandle_t); }
+
+typedef CUresult (*PFN_memGetAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+ptdr_status ptdr_ipc_get_handle(const void* dev_ptr, void* handle, uint64_t* offset) {
+  if (!dev_ptr || !handle || !offset) return fail(PTDR_EINVAL, "null pointer");
+  // the handle names the whole allocation: report where dev_ptr sits inside it
+  static PFN_memGetAddressRange range_fn = nullptr;
+  if (!range_fn) {
+    void* fp = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fp, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return fail(PTDR_ECUDA, "cuMemGetAddressRange unavailable");
+    range_fn = reinterpret_cast<PFN_memGetAddressRange>(fp);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range_fn(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+    return fail(PTDR_EINVAL, "dev_ptr is not a device allocation");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+  memcpy(handle, &h, sizeof(h));
+  *offset = (uint64_t)(reinterpret_cast<CUdeviceptr>(dev_ptr) - base);
+  return PTDR_OK;
+}
+
+ptdr_status ptdr_ipc_open(const void* handle, void** dev_ptr) {
+  if (!handle || !dev_ptr) return fail(PTDR_EINVAL, "null pointer");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  cudaError_t e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+  return PTDR_OK;
+}
+
+ptdr_status ptdr_ipc_close(void* dev_ptr) {
+  if (!dev_ptr) return PTDR_OK;
+  cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcCloseMemHandle");
+  return PTDR_OK;
 }
 
 ptdr_status ptdr_decompose_zshard_async(const ptdr_c128* band, int n, int structure, int rank, int world,

@@ -5,14 +5,14 @@
 
 namespace ptdr {
 
-cudaError_t pipe_cfg1(int mode, const CUtensorMap& map, const DenseArgs& a, int M, cudaStream_t st);
-cudaError_t pipe_cfg2(int mode, const CUtensorMap& map, const DenseArgs& a, int M, cudaStream_t st);
-cudaError_t pipe_cfg3(int mode, const CUtensorMap& map, const DenseArgs& a, int M, cudaStream_t st);
-cudaError_t pipe_cfg4(int mode, const CUtensorMap& map, const DenseArgs& a, int M, cudaStream_t st);
-cudaError_t pipe_cfg5(int mode, const CUtensorMap& map, const DenseArgs& a, int M, cudaStream_t st);
-cudaError_t pipe_cfg6(int mode, const CUtensorMap& map, const DenseArgs& a, int M, cudaStream_t st);
-cudaError_t pipe_cfg7(int mode, const CUtensorMap& map, const DenseArgs& a, int M, cudaStream_t st);
-cudaError_t pipe_cfg8(int mode, const CUtensorMap& map, const DenseArgs& a, int M, cudaStream_t st);
+cudaError_t pipe_cfg1(int mode, const TmapSet& map, const DenseArgs& a, int M, cudaStream_t st);
+cudaError_t pipe_cfg2(int mode, const TmapSet& map, const DenseArgs& a, int M, cudaStream_t st);
+cudaError_t pipe_cfg3(int mode, const TmapSet& map, const DenseArgs& a, int M, cudaStream_t st);
+cudaError_t pipe_cfg4(int mode, const TmapSet& map, const DenseArgs& a, int M, cudaStream_t st);
+cudaError_t pipe_cfg5(int mode, const TmapSet& map, const DenseArgs& a, int M, cudaStream_t st);
+cudaError_t pipe_cfg6(int mode, const TmapSet& map, const DenseArgs& a, int M, cudaStream_t st);
+cudaError_t pipe_cfg7(int mode, const TmapSet& map, const DenseArgs& a, int M, cudaStream_t st);
+cudaError_t pipe_cfg8(int mode, const TmapSet& map, const DenseArgs& a, int M, cudaStream_t st);
 
 static unsigned long long* g_trace = nullptr;
 static unsigned long long* debug_trace_buffer() {
@@ -58,25 +58,38 @@ cudaError_t launch_dense_pipe(int mode, const DenseArgs& a_in, const DensePlan& 
   a.slot_elems = p.slot_elems;
   PFN_cuTensorMapEncodeTiled_v12000 enc = encode_fn();
   if (!enc) return cudaErrorNotSupported;
-  CUtensorMap map;
-  // zero padding: the tensor map covers only the stored rows_valid x
-  // cols_valid block; TMA fills every out-of-bounds element of a box with zeros.
-  const cuuint64_t ncols = a.cols_valid ? a.cols_valid : a.colmask + 1;
-  const cuuint64_t nrows = a.rows_valid ? a.rows_valid : 1ull << a.n;
-  cuuint64_t gdim[2] = {2 * ncols, nrows};
-  cuuint64_t gstride[1] = {a.ld * 16};
+  TmapSet map;
   const cuuint32_t W = (cuuint32_t)p.W;
   cuuint32_t box[2] = {2 * W, W};  // W complex128 x W rows
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double2*>(a.A), gdim, gstride,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  auto encode = [&](CUtensorMap* m, const double2* base, cuuint64_t ncols, cuuint64_t nrows) {
+    cuuint64_t gdim[2] = {2 * ncols, nrows};
+    cuuint64_t gstride[1] = {a.ld * 16};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double2*>(base), gdim, gstride, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  };
+  CUresult r = CUDA_SUCCESS;
+  if (a.peer_shift) {
+    // peer-pull: one map per rank's row-block shard [R rows][2^n columns] (row pitch a.ld)
+    if (a.npeers < 1 || a.npeers > kMaxPeers) return cudaErrorInvalidValue;
+    for (int g = 0; g < a.npeers && r == CUDA_SUCCESS; ++g)
+      r = encode(&map.m[g], a.peer_ptrs[g], a.colmask + 1, a.peer_rowmask + 1);
+  } else {
+    // zero padding: the tensor map covers only the stored rows_valid x
+    // cols_valid block; TMA fills every out-of-bounds element of a box with zeros.
+    const cuuint64_t ncols = a.cols_valid ? a.cols_valid : a.colmask + 1;
+    const cuuint64_t nrows = a.rows_valid ? a.rows_valid : 1ull << a.n;
+    r = encode(&map.m[0], a.A, ncols, nrows);
+  }
   if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
   {
     const char* nd = getenv("PTDR_NO_DISCARD");
     a.discard = (nd && nd[0] == '1') ? 0 : 1;
     const char* il = getenv("PTDR_INTERLEAVE");
     a.interleave = (il && il[0] == '1') ? 1 : 0;
+    const char* stc = getenv("PTDR_STATIC");
+    a.static_tickets = (stc && stc[0] == '1') ? 1 : 0;
   }
   cudaError_t e = cudaMemsetAsync(a.ctr, 0, p.ctr_bytes, st);
   if (e != cudaSuccess) return e;

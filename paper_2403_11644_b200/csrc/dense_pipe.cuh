@@ -43,6 +43,13 @@ __device__ __forceinline__ void pwht(double2* v) {
   if constexpr ((kDiag & 4) == 0) wht_regs<B>(v);
 }
 
+// Tensor maps of the A source: one (the local matrix or shard), or one per rank's row-block
+// shard in peer-pull mode (ptdr_decompose_peer_async).
+constexpr int kMaxPeers = 8;
+struct TmapSet {
+  CUtensorMap m[kMaxPeers];
+};
+
 struct TileMeta {
   int valid, phase, tile, seq;
   unsigned chunk, pad0, pad1, pad2;
@@ -323,7 +330,7 @@ __device__ __forceinline__ void xor_half_transpose(double2 (&v)[16], double2* X,
 // tile, so a phase-B tile is one contiguous bulk copy (fiber phi = tileB * FB + f).
 template <int LT, int XB, int GW, int NG, int NS, int NR, int M, int MODE>
 __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
-    dense_pipe_kernel(const __grid_constant__ CUtensorMap tmap, DenseArgs a) {
+    dense_pipe_kernel(const __grid_constant__ TmapSet maps, DenseArgs a) {
   using Cfg = PipeCfg<LT, XB, GW, NG, NS, NR>;
   constexpr int R = Cfg::R, TE = Cfg::TE, GT = Cfg::GT, W = Cfg::W;
   constexpr bool HALF = (MODE == MODE_HERM_HALF || MODE == MODE_SYM_HALF);
@@ -369,7 +376,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
   // ------------------------------------------------------------------ producer
   if (warp == 0) {
     if (lane == 0) {
-      prefetch_tmap(&tmap);
+      for (int pm = 0; pm < (a.peer_shift ? a.npeers : 1); ++pm) prefetch_tmap(&maps.m[pm]);
       const uint64_t pol = policy_evict_first();
       const uint32_t total = C << (M + 1);
       // Decoded ticket: (tk, phase, chunk, tile) and its dependency counter, whose value is
@@ -431,7 +438,10 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
             uint32_t row0 = HALF ? insert0_32(iv0, t) : iv0;
             if constexpr ((kDiag & 2) != 0) row0 &= 255u;
             const uint32_t col0 = (row0 ^ x0) & cm;
-            tma_load_2d(dst + rb * W * W, &tmap, (int)(col0 * 2u), (int)row0, &full[s], pol);
+            // peer-pull: the 128 rows of a tile lie in one rank's shard (R >= 128)
+            const CUtensorMap* tm = a.peer_shift ? &maps.m[row0 >> a.peer_shift] : &maps.m[0];
+            const uint32_t rowc = a.peer_shift ? (row0 & (uint32_t)a.peer_rowmask) : row0;
+            tma_load_2d(dst + rb * W * W, tm, (int)(col0 * 2u), (int)rowc, &full[s], pol);
           }
         } else {
           if constexpr (kBDirect) {
@@ -459,16 +469,33 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
       int phP, phQ;
       const unsigned *depP, *depQ;
       unsigned dvP, dvQ;
-      const uint32_t b0 = atomicAdd(ticket, 2u);
+      // Ticket pairs: claimed from the shared counter (dynamic balance), or assigned
+      // statically round-robin (pair p -> CTA p mod gridDim; no hot-spot atomic: every
+      // ticket still waits only on smaller tickets, and each CTA takes its own in order,
+      // so the smallest unfinished ticket always progresses).
+      const bool stat = a.static_tickets != 0;
+      uint32_t pair = blockIdx.x;
+      auto claim = [&]() -> uint32_t {
+        if (stat) {
+          const uint32_t t2 = 2u * pair;
+          pair += gridDim.x;
+          return t2 < total ? t2 : total;
+        }
+        return atomicAdd(ticket, 2u);
+      };
+      const uint32_t b0 = claim();
       decode_into(b0, tkP, phP, chP, tlP, depP, dvP);
       decode_into(b0 + 1, tkQ, phQ, chQ, tlQ, depQ, dvQ);
-      uint32_t nb = (b0 + 1 < total) ? atomicAdd(ticket, 2u) : total;
+      uint32_t nb = (b0 + 1 < total) ? claim() : total;
       for (;;) {
         if (process(tkP, phP, chP, tlP, depP, dvP)) break;
         decode_into(nb, tkP, phP, chP, tlP, depP, dvP);
+        trace_stamp(a.trace, k - 1, 9);
         if (process(tkQ, phQ, chQ, tlQ, depQ, dvQ)) break;
         decode_into(nb + 1, tkQ, phQ, chQ, tlQ, depQ, dvQ);
-        nb = (nb + 1 < total) ? atomicAdd(ticket, 2u) : total;
+        trace_stamp(a.trace, k - 1, 9);
+        nb = (nb + 1 < total) ? claim() : total;
+        trace_stamp(a.trace, k - 1, 10);
       }
     }
     return;
@@ -742,7 +769,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
 
 // ------------------------------------------------------------------ launch template
 template <int LT, int XB, int GW, int NG, int NS, int NR, int M, int MODE>
-static cudaError_t launch_pipe_impl(const CUtensorMap& map, const DenseArgs& a, cudaStream_t st) {
+static cudaError_t launch_pipe_impl(const TmapSet& map, const DenseArgs& a, cudaStream_t st) {
   using Cfg = PipeCfg<LT, XB, GW, NG, NS, NR>;
   constexpr auto kern = dense_pipe_kernel<LT, XB, GW, NG, NS, NR, M, MODE>;
   static std::once_flag once;
@@ -756,7 +783,7 @@ static cudaError_t launch_pipe_impl(const CUtensorMap& map, const DenseArgs& a, 
 }
 
 template <int LT, int XB, int GW, int NG, int NS, int NR, int MODE>
-static cudaError_t launch_pipe_m(const CUtensorMap& map, const DenseArgs& a, int M, cudaStream_t st) {
+static cudaError_t launch_pipe_m(const TmapSet& map, const DenseArgs& a, int M, cudaStream_t st) {
   switch (M) {
     case 4: return launch_pipe_impl<LT, XB, GW, NG, NS, NR, 4, MODE>(map, a, st);
     case 5: return launch_pipe_impl<LT, XB, GW, NG, NS, NR, 5, MODE>(map, a, st);
@@ -768,7 +795,7 @@ static cudaError_t launch_pipe_m(const CUtensorMap& map, const DenseArgs& a, int
 }
 
 template <int LT, int XB, int GW, int NG, int NS, int NR>
-static cudaError_t launch_pipe_cfg(int mode, const CUtensorMap& map, const DenseArgs& a, int M,
+static cudaError_t launch_pipe_cfg(int mode, const TmapSet& map, const DenseArgs& a, int M,
                                    cudaStream_t st) {
   switch (mode) {
     case MODE_GENERAL: return launch_pipe_m<LT, XB, GW, NG, NS, NR, MODE_GENERAL>(map, a, M, st);
@@ -779,7 +806,7 @@ static cudaError_t launch_pipe_cfg(int mode, const CUtensorMap& map, const Dense
 }
 
 #define PTDR_DEFINE_PIPE_CFG(NAME, LT, XB, GW, NG, NS, NR)                                     \
-  cudaError_t NAME(int mode, const CUtensorMap& map, const DenseArgs& a, int M, cudaStream_t st) { \
+  cudaError_t NAME(int mode, const TmapSet& map, const DenseArgs& a, int M, cudaStream_t st) {     \
     return launch_pipe_cfg<LT, XB, GW, NG, NS, NR>(mode, map, a, M, st);                       \
   }
 

@@ -101,3 +101,56 @@ def gather_band_sharded(local: torch.Tensor, n: int, blocks: int, group=None) ->
     NL = (1 << n) // world
     stacked = torch.stack([p.view(blocks, NL) for p in parts], dim=1)  # [blocks][world][NL]
     return stacked.reshape(blocks << n)
+
+
+# ---- dense, fused exchange: peer pull over NVLink -----------------------
+def _exchange_objects(obj, group=None):
+    world = dist.get_world_size(group)
+    objs = [None] * world
+    dist.all_gather_object(objs, obj, group=group)
+    return objs
+
+
+def peer_pointers(blobs, rank: int, local_ptr: int, open_fn):
+    """Device addresses of every rank's shard from the gathered (handle, offset) blobs: the
+    local shard as is, peers mapped through `open_fn(handle) -> base` plus their offset.
+    Returns (pointers in rank order, bases to close)."""
+    ptrs, opened = [], []
+    for r, (handle, offset) in enumerate(blobs):
+        if r == rank:
+            ptrs.append(int(local_ptr))
+        else:
+            base = open_fn(handle)
+            opened.append(base)
+            ptrs.append(base + int(offset))
+    return ptrs, opened
+
+
+def open_peer_shards(shard: torch.Tensor, group=None):
+    """CUDA IPC exchange of the ranks' row-block shards.  Returns (device pointers of all
+    shards in rank order, close()).  Collective over `group`."""
+    from . import ipc_close, ipc_handle, ipc_open
+
+    rank = dist.get_rank(group)
+    blobs = _exchange_objects(ipc_handle(shard), group)
+    ptrs, opened = peer_pointers(blobs, rank, shard.data_ptr(), ipc_open)
+
+    def close():
+        for b in opened:
+            ipc_close(b)
+
+    return ptrs, close
+
+
+def decompose_peer_sharded(shard: torch.Tensor, n: int, ptrs, group=None, out=None, workspace=None,
+                           stream=None) -> torch.Tensor:
+    """Fused exchange + decomposition: rank h's phase-A tiles read the rows they need
+    directly from the owning rank's shard (TMA over NVLink), no all-to-all, no receive
+    buffer.  Every shard must be complete before the call (barrier) and stay unmodified
+    until every rank has finished (the caller's barrier after synchronising)."""
+    from . import decompose_peer
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    return decompose_peer(ptrs, n, rank, world, out=out, workspace=workspace, stream=stream,
+                          device=shard.device)

@@ -154,3 +154,50 @@ def test_band_zshard_gather(world, n, structure):
     assert np.array_equal(pdist.assemble_zshards(parts, n, blocks), want)
     allidx = np.concatenate([pdist.zshard_index(r, n, world, blocks) for r in range(world)])
     assert np.array_equal(np.sort(allidx), np.arange(blocks << n))
+
+
+def _peer_blob_worker(rank, world, port, result_q):
+    """Host logic of the peer-pull setup: the (handle, offset) blobs gathered over a real
+    process group come back in rank order and map to base + offset (fake handles, no GPU)."""
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2403_11644_b200 import dist as pdist
+
+        mine = (bytes([rank]) * 64, 4096 * rank + 16)
+        blobs = pdist._exchange_objects(mine)
+        bases = {}
+
+        def fake_open(handle):
+            r = handle[0]
+            bases[r] = 0x7000_0000_0000 + (r << 32)
+            return bases[r]
+
+        ptrs, opened = pdist.peer_pointers(blobs, rank, 0xDEAD0000, fake_open)
+        result_q.put((rank, ptrs, sorted(bases)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_peer_handle_exchange(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_blob_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ptrs, opened in res:
+        assert len(ptrs) == world
+        assert opened == [r for r in range(world) if r != rank]       # never maps itself
+        for r, pt in enumerate(ptrs):
+            want = 0xDEAD0000 if r == rank else 0x7000_0000_0000 + (r << 32) + 4096 * r + 16
+            assert pt == want

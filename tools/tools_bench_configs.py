@@ -33,6 +33,24 @@ def time_it(fn, iters=10, warm=3):
     return t[len(t) // 2]
 
 
+def oracle_rate(fn, n_out, seconds=2.0):
+    """The CPU oracle timed beside the kernel (all host cores): coefficients/s on seeded
+    random strings of the same workload, bounded to ~`seconds`."""
+    import time
+
+    import numpy as np
+
+    import oracle
+
+    rng = np.random.default_rng(3)
+    batch = max(oracle.threads(), 8)
+    done, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < seconds:
+        fn(rng.integers(0, n_out, batch, dtype=np.uint64))
+        done += batch
+    return {"oracle_coeffs_per_s": done / (time.perf_counter() - t0), "oracle_cores": oracle.threads()}
+
+
 def dense(name, n, seed, variant):
     A = ptdr.generate_dense(n, seed, variant, device="cuda")
     out = torch.empty(1 << (2 * n), dtype=torch.complex128, device="cuda")
@@ -41,9 +59,14 @@ def dense(name, n, seed, variant):
     coeffs = 1 << (2 * n)
     bpc = 32 if variant == "general" else 24
     gbs = bpc * coeffs / (ms * 1e-3) / 1e9
+    import oracle
+    import ptdr_inputs
+
+    vnum = ptdr_inputs.VARIANTS.get(variant, variant)
+    orc = oracle_rate(lambda qs: oracle.coeffs_generated(n, seed, vnum, qs), coeffs)
     print(json.dumps({"config": name, "n": n, "structure": variant, "ms": ms,
                       "coeffs_per_s": coeffs / (ms * 1e-3), "alg_bytes_per_coeff": bpc,
-                      "hbm_gbs": gbs, "frac_of_measured": gbs / PEAK}), flush=True)
+                      "hbm_gbs": gbs, "frac_of_measured": gbs / PEAK, **orc}), flush=True)
     del A, out, ws
     torch.cuda.empty_cache()
 
@@ -56,9 +79,28 @@ def band(name, n, seed, variant):
     coeffs = out.numel()
     alg = (B.numel() + out.numel()) * 16
     gbs = alg / (ms * 1e-3) / 1e9
+    import numpy as np
+
+    import oracle
+    import ptdr_inputs
+    from paper_2403_11644_b200 import q_of
+
+    if variant == "tridiagonal":
+        sub, main, sup = ptdr_inputs.band(n, seed, "tridiagonal")
+
+        def orc_fn(idx):
+            qs = np.array([q_of((1 << int(b)) - 1, int(z), n) for b, z in zip(idx >> n, idx & ((1 << n) - 1))],
+                          dtype=np.uint64)
+            return oracle.coeffs_tridiagonal(sub, main, sup, qs)
+    else:
+        d = ptdr_inputs.band(n, seed, "diagonal")
+
+        def orc_fn(idx):
+            return oracle.coeffs_diagonal(d, np.array([q_of(0, int(z), n) for z in idx], dtype=np.uint64))
+    orc = oracle_rate(orc_fn, coeffs, seconds=3.0)
     print(json.dumps({"config": name, "n": n, "structure": variant, "ms": ms,
                       "coeffs_per_s": coeffs / (ms * 1e-3), "alg_bytes": alg, "hbm_gbs": gbs,
-                      "frac_of_measured": gbs / PEAK, "launches": ptdr.last_launch_count()}),
+                      "frac_of_measured": gbs / PEAK, "launches": ptdr.last_launch_count(), **orc}),
           flush=True)
     # 8 GPUs, replicated band + z-sharded output: ranks are independent (no communication),
     # so the 8-GPU step time is the max over ranks of each rank's own time (ranks 0 and 7 here)

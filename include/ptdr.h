@@ -138,6 +138,19 @@ ptdr_status ptdr_decompose_xshard_async(const ptdr_c128* A_local, int n, int ran
                                         ptdr_c128* out_local, void* workspace, size_t ws_bytes,
                                         void* stream);
 
+/* Matrix-free input ("no need to store the input matrix ... from a
+ * function"): the GENERAL matrix of the seeded generator (ptdr_generate_dense_async,
+ * variant 0, seed `seed`) is decomposed without being stored -- phase A of the pipeline
+ * computes A[i][i ^ x] itself.  world = 1: out_local = all 4^n coefficients in q order;
+ * world = 2^g > 1: rank `rank`'s X-mask shard in the layout of ptdr_decompose_xshard_async,
+ * with no communication at all (needs n - g >= 11).  Bitwise identical to decomposing the
+ * stored matrix.  workspace >= ptdr_generated_workspace_bytes(n, world) ((size_t)-1 if
+ * invalid); small n (no pipeline) generates into the workspace first. */
+size_t ptdr_generated_workspace_bytes(int n, int world);
+ptdr_status ptdr_decompose_generated_async(int n, uint64_t seed, int rank, int world,
+                                           ptdr_c128* out_local, void* workspace, size_t ws_bytes,
+                                           void* stream);
+
 /* Multi-GPU, per rank, GENERAL, fused exchange ("peer pull"):
  * instead of an all-to-all, the phase-A tiles of rank `rank`'s X-masks are loaded by TMA
  * straight from the row-block shard of the rank that owns the rows, over NVLink.

@@ -86,6 +86,10 @@ def lib():
         L.ptdr_ipc_close.argtypes = [vp]
         for name in ("ptdr_ipc_get_handle", "ptdr_ipc_open", "ptdr_ipc_close"):
             getattr(L, name).restype = i32
+        L.ptdr_generated_workspace_bytes.argtypes = [i32, i32]
+        L.ptdr_generated_workspace_bytes.restype = sz
+        L.ptdr_decompose_generated_async.argtypes = [i32, u64, i32, i32, vp, vp, sz, vp]
+        L.ptdr_decompose_generated_async.restype = i32
         L.ptdr_generate_dense_async.argtypes = [i32, u64, i32, u64, u64, vp, vp]
         L.ptdr_generate_band_async.argtypes = [i32, u64, i32, vp, vp]
         L.ptdr_generate_sendblocks_async.argtypes = [i32, u64, i32, i32, vp, vp]
@@ -323,6 +327,27 @@ def decompose_padded(A, structure="general", out=None, workspace=None, stream=No
                                              ctypes.c_void_p(out.data_ptr()),
                                              ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
                                              _stream_ptr(stream)), "ptdr_decompose_padded_async")
+    return out
+
+
+def decompose_generated(n: int, seed: int, rank: int = 0, world: int = 1, out=None, workspace=None,
+                        stream=None, device=None):
+    """Matrix-free decomposition of the seeded GENERAL matrix (ptdr_decompose_generated_async):
+    the entries are computed inside the kernel, A is never stored."""
+    import torch
+
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if out is None:
+        out = torch.empty((1 << (2 * n)) // world, dtype=torch.complex128, device=dev)
+    _require_cuda_c128(out, "out")
+    if workspace is None:
+        nb = int(lib().ptdr_generated_workspace_bytes(n, world))
+        if nb == ctypes.c_size_t(-1).value:
+            raise PtdrError(PTDR_EINVAL, f"invalid (n={n}, world={world})")
+        workspace = torch.empty(max(nb, 1), dtype=torch.uint8, device=dev)
+    _check(lib().ptdr_decompose_generated_async(n, seed, rank, world, ctypes.c_void_p(out.data_ptr()),
+                                                ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
+                                                _stream_ptr(stream)), "ptdr_decompose_generated_async")
     return out
 
 

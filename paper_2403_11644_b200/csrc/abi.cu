@@ -314,6 +314,66 @@ ptdr_status ptdr_decompose_xshard_async(const ptdr_c128* A_local, int n, int ran
   return r;
 }
 
+// ---- matrix-free input ------------------------------------
+// GENERAL entries from the counter-based generator (variant 0),
+// produced inside phase A of the pipeline: A is never stored.  world > 1: rank's X-mask
+// shard (output layout of ptdr_decompose_xshard_async), no communication at all.
+static bool generated_pipe(int n, int world) {
+  const uint64_t R = (1ull << n) / (uint64_t)world;
+  const DensePlan p = plan_for(MODE_GENERAL, n, R);
+  return p.kind == 2 && p.pipe_cfg != kPipeNone && (p.pipe_cfg == 1 || p.pipe_cfg == 4);
+}
+
+size_t ptdr_generated_workspace_bytes(int n, int world) {
+  if (!valid_n(n, PTDR_GENERAL) || world < 1 || (world & (world - 1)) || (uint64_t)world > (1ull << n))
+    return (size_t)-1;
+  if (world > 1) return generated_pipe(n, world) ? ptdr_workspace_bytes(n, PTDR_GENERAL, world) : (size_t)-1;
+  if (generated_pipe(n, 1)) return ptdr_workspace_bytes(n, PTDR_GENERAL, 1);
+  // small n: the matrix is generated into the workspace, then decomposed as stored
+  return ((((size_t)16 << (2 * n)) + 255) / 256) * 256 + ptdr_workspace_bytes(n, PTDR_GENERAL, 1);
+}
+
+ptdr_status ptdr_decompose_generated_async(int n, uint64_t seed, int rank, int world, ptdr_c128* out_local,
+                                           void* workspace, size_t ws_bytes, void* stream) {
+  g_last_launches = 0;
+  const size_t need = ptdr_generated_workspace_bytes(n, world);
+  if (need == (size_t)-1)
+    return fail(PTDR_EINVAL, "invalid n / world (world > 1 needs n - log2(world) >= 11)");
+  if (rank < 0 || rank >= world) return fail(PTDR_EINVAL, "rank out of range");
+  if (!out_local || ((uintptr_t)out_local & 15)) return fail(PTDR_EINVAL, "null or misaligned out");
+  if (need > 0 && (!workspace || ((uintptr_t)workspace & 255)))
+    return fail(PTDR_EINVAL, "workspace missing or not 256-byte aligned");
+  if (ws_bytes < need) return fail(PTDR_ENOMEM, "workspace too small");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int g = __builtin_ctz((unsigned)world);
+  const uint64_t N = 1ull << n, R = N >> g;
+  if (!generated_pipe(n, world)) {  // world == 1, small n
+    const size_t ab = ((((size_t)16 << (2 * n)) + 255) / 256) * 256;
+    double2* A = reinterpret_cast<double2*>(workspace);
+    cudaError_t e = launch_generate_dense(n, seed, 0, 0, N, A, st);
+    if (e != cudaSuccess) return cuda_fail(e, "generator launch");
+    ptdr_status r = ptdr_decompose_async(reinterpret_cast<const ptdr_c128*>(A), n, PTDR_GENERAL, out_local,
+                                         reinterpret_cast<char*>(workspace) + ab, ws_bytes - ab, stream);
+    g_last_launches += 1;
+    return r;
+  }
+  DensePlan p = plan_for(MODE_GENERAL, n, R);
+  DenseArgs a = base_args(reinterpret_cast<const double2*>(out_local), reinterpret_cast<double2*>(out_local), n,
+                          workspace);  // A unused (no loads); any valid address for the tensor map
+  a.ld = N;
+  a.colmask = N - 1;
+  a.gshift = n - g;
+  a.nv = n;
+  a.x_base = (uint64_t)rank * R;
+  a.nchunks = p.nchunks;
+  a.scratch = reinterpret_cast<double2*>(reinterpret_cast<char*>(workspace) + p.ctr_bytes);
+  a.gen_seed = seed;
+  int nl = 0;
+  ptdr_status r = launch_mode(MODE_GEN, a, p, st, &nl);
+  g_last_launches = nl;
+  return r;
+}
+
 // ---- fused exchange: peer-pull X-mask decomposition --------------------
 ptdr_status ptdr_decompose_peer_async(const ptdr_c128* const* shards, int n, int rank, int world,
                                       ptdr_c128* out_local, void* workspace, size_t ws_bytes, void* stream) {

@@ -20,7 +20,8 @@ namespace ptdr {
 // MODE: 0 GENERAL, 1 HERMITIAN mirrored (full-length vectors built from the upper
 // triangle), 2 REAL_SYMMETRIC mirrored, 3 HERMITIAN half-length, 4 REAL_SYMMETRIC
 // half-length.  See DESIGN.md "Hermitian / real-symmetric path".
-enum { MODE_GENERAL = 0, MODE_HERM_MIRROR = 1, MODE_SYM_MIRROR = 2, MODE_HERM_HALF = 3, MODE_SYM_HALF = 4 };
+enum { MODE_GENERAL = 0, MODE_HERM_MIRROR = 1, MODE_SYM_MIRROR = 2, MODE_HERM_HALF = 3, MODE_SYM_HALF = 4,
+       MODE_GEN = 8 /* matrix-free GENERAL (pipeline only): entries generated in phase A */ };
 
 struct DenseArgs {
   const double2* A;
@@ -44,6 +45,7 @@ struct DenseArgs {
   u64 peer_rowmask;    //   at local row i & peer_rowmask
   int npeers;          //   shards (host side: tensor maps are built from peer_ptrs)
   const double2* peer_ptrs[8];
+  u64 gen_seed;        // MODE_GEN: seed of the counter-based generator
   u64 rows_valid;      // zero padding: rows / columns of A actually stored;
   u64 cols_valid;      // 0 = all (the TMA tensor map fills the rest with zeros)
   unsigned long long* trace;  // pipeline debug timeline (nullptr unless PTDR_TRACE=1)

@@ -24,6 +24,7 @@
 #include "dense_impl.cuh"
 #include "dense_plan.h"
 #include "internal.h"
+#include "philox.cuh"
 #include "sm100_ptx.cuh"
 
 namespace ptdr {
@@ -134,7 +135,7 @@ struct EpiUnit {
 template <int MODE>
 __device__ __forceinline__ void emit_one(const DenseArgs& a, uint32_t q, uint32_t p, uint32_t dt,
                                          double2 w) {
-  if constexpr (MODE == MODE_GENERAL) {
+  if constexpr (MODE == MODE_GENERAL || MODE == MODE_GEN) {
     const bool sw = (p & 1u) != 0;
     const double s = (p & 2u) ? -a.scale : a.scale;
     const double re = sw ? -w.y : w.x;
@@ -159,7 +160,7 @@ __device__ __forceinline__ void emit_one(const DenseArgs& a, uint32_t q, uint32_
 // All 2^NB registers of a unit, visited in Gray-code order so that consecutive outputs
 // differ in one z bit: q and p are updated with one add each (q += +-D[b], p += +-P[b]).
 template <int MODE, int NB, int I = 0>
-__device__ __forceinline__ void emit_gray(const DenseArgs& a, const EpiUnit<NB, (MODE >= 3)>& e,
+__device__ __forceinline__ void emit_gray(const DenseArgs& a, const EpiUnit<NB, (MODE == 3 || MODE == 4)>& e,
                                           const double2* w, uint32_t q, uint32_t p) {
   if constexpr (I < (1 << NB)) {
     constexpr int J = I ^ (I >> 1);
@@ -180,7 +181,7 @@ __device__ __forceinline__ void emit_gray(const DenseArgs& a, const EpiUnit<NB, 
 }
 
 template <int MODE, int NB>
-__device__ __forceinline__ void emit_all(const DenseArgs& a, const EpiUnit<NB, (MODE >= 3)>& e,
+__device__ __forceinline__ void emit_all(const DenseArgs& a, const EpiUnit<NB, (MODE == 3 || MODE == 4)>& e,
                                          const double2* w) {
   emit_gray<MODE, NB, 0>(a, e, w, e.q0, e.p0);
 }
@@ -427,7 +428,9 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
         meta[s].tile = (int)tlX;
         meta[s].chunk = chX;
         meta[s].seq = k;
-        if (phX == 0) {
+        if (phX == 0 && MODE == MODE_GEN) {
+          mbar_arrive(&full[s]);  // matrix-free: the consumers generate the tile's entries
+        } else if (phX == 0) {
           mbar_arrive_expect_tx(&full[s], (uint32_t)Cfg::TB);
           const uint32_t x0 = (uint32_t)a.x_base + (chX << XB);
           const int t = HALF ? 31 - __clz(x0) : 0;
@@ -620,11 +623,22 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
       //      sits in SMEM row r at column (r mod W) ^ u (XOR transpose in the read)
       {
         const int u = gtid & (W - 1), jh = gtid >> XB;
+        if constexpr (MODE == MODE_GEN) {
+          // matrix-free: A[i][i ^ x] from the counter-based
+          // generator, bit-identical to what ptdr_generate_dense_async stores
+          const u64 x = a.x_base + ((u64)m.chunk << XB) + (u64)u;
 #pragma unroll
-        for (int kk = 0; kk < 16; ++kk) {
-          const int r = jh * 16 + kk;
-          v[kk] = S[r * W + ((r & (W - 1)) ^ u)];
-          if (MODE == MODE_SYM_HALF) v[kk].y = 0.0;
+          for (int kk = 0; kk < 16; ++kk) {
+            const u64 i = ((u64)m.tile << R) + (u64)(jh * 16 + kk);
+            v[kk] = gauss_pair(a.gen_seed, (i << a.n) + (i ^ x), 0u);
+          }
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < 16; ++kk) {
+            const int r = jh * 16 + kk;
+            v[kk] = S[r * W + ((r & (W - 1)) ^ u)];
+            if (MODE == MODE_SYM_HALF) v[kk].y = 0.0;
+          }
         }
         pwht<4>(v);
         __syncwarp();  // rows of this jh are read and written only by this warp
@@ -801,6 +815,10 @@ static cudaError_t launch_pipe_cfg(int mode, const TmapSet& map, const DenseArgs
     case MODE_GENERAL: return launch_pipe_m<LT, XB, GW, NG, NS, NR, MODE_GENERAL>(map, a, M, st);
     case MODE_HERM_HALF: return launch_pipe_m<LT, XB, GW, NG, NS, NR, MODE_HERM_HALF>(map, a, M, st);
     case MODE_SYM_HALF: return launch_pipe_m<LT, XB, GW, NG, NS, NR, MODE_SYM_HALF>(map, a, M, st);
+    case MODE_GEN:
+      // matrix-free: instantiated for the 3-stage in-place configurations only
+      if constexpr (NR == 0 && LT == 12) return launch_pipe_m<LT, XB, GW, NG, NS, NR, MODE_GEN>(map, a, M, st);
+      return cudaErrorInvalidValue;
     default: return cudaErrorInvalidValue;
   }
 }

@@ -148,6 +148,19 @@ def anti(name, n):
                       "launches": ptdr.last_launch_count()}), flush=True)
 
 
+def generated(name, n):
+    """Matrix-free: entries computed in phase A, A never stored."""
+    out = torch.empty(4 ** n, dtype=torch.complex128, device="cuda")
+    ws = torch.empty(int(ptdr.lib().ptdr_generated_workspace_bytes(n, 1)), dtype=torch.uint8, device="cuda")
+    ms = time_it(lambda: ptdr.decompose_generated(n, 4, out=out, workspace=ws), iters=5, warm=2)
+    print(json.dumps({"config": name, "n": n, "ms": ms, "coeffs_per_s": 4 ** n / (ms * 1e-3),
+                      "hbm_gbs_16B": 16 * 4 ** n / (ms * 1e-3) / 1e9,
+                      "frac_of_measured_16B": 16 * 4 ** n / (ms * 1e-3) / 1e9 / PEAK,
+                      "launches": ptdr.last_launch_count()}), flush=True)
+    del out, ws
+    torch.cuda.empty_cache()
+
+
 def inverse(name, n):
     """Inverse transform: coefficients -> A, round trip checked."""
     A = ptdr.generate_dense(n, 4, "general", device="cuda")
@@ -182,6 +195,7 @@ if __name__ == "__main__":
         band_s("n24band_s2", 24, 2)
         band_s("n22band_s5", 22, 5)
         inverse("n15_inverse", 15)
+        generated("n15_matrix_free", 15)
     if "all" in which or "big" in which:
         dense("n15", 15, 4, "general")
         dense("n15_hermitian", 15, 4, "hermitian")

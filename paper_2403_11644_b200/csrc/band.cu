@@ -539,7 +539,7 @@ static BandPlan make_band_plan(int n, int s) {
     p.seg_lam[k] = segs[k].lam;
   }
   const size_t tb = p.blocks.size() * sizeof(BandBlockDev) + p.refs.size() * sizeof(BandSegRef) +
-                    segs.size() * sizeof(int4);
+                    segs.size() * sizeof(int4) + (size_t)n * (s > 0 ? s : 1) * sizeof(int);
   p.table_bytes = (tb + 255) / 256 * 256;
   p.ws_bytes = p.table_bytes + (size_t)p.seg_elems * 16;
   return p;
@@ -562,27 +562,108 @@ __global__ void band_gather_kernel(const double2* diags, int n, int s, const Ban
   }
 }
 
-// Expansion: out[b][z] = 2^-n i^{popcount(x_b & z)} sum_k (-1)^{popcount(l_k & z_lo)} W_k[z_hi].
-__global__ void __launch_bounds__(256) band_expand_kernel(const BandBlockDev* blocks, const BandSegRef* refs,
-                                                          const double2* segs, int nblocks, int n,
-                                                          double scale, double2* out) {
+// Gather in diagonal order: every stored band element A[i][i+d] belongs to exactly one
+// segment -- x = i ^ (i+d), l = i mod 2^{t+1}, h = i >> (t+1) -- so each diagonal is read
+// once, coalesced (the per-segment gather above reads a 32 B sector per element).
+// xblock[t * s + e] = block index of x = 2^{t+1} - 1 - e (-1 if x is not in the support).
+__global__ void band_gather_diag_kernel(const double2* diags, int n, int s, const BandBlockDev* blocks,
+                                        const BandSegRef* refs, const int* xblock, double2* segs) {
   const u64 N = 1ull << n;
-  for (int b = blockIdx.y; b < nblocks; b += gridDim.y) {
+  const u64 total = (u64)(2 * s + 1) * N;
+  for (u64 id = (u64)blockIdx.x * blockDim.x + threadIdx.x; id < total; id += (u64)gridDim.x * blockDim.x) {
+    const int d = (int)(id >> n) - s;
+    const u64 i = id & (N - 1);
+    const long long j = (long long)i + d;
+    if (j < 0 || j >= (long long)N) continue;
+    const double2 v = ld_stream(diags + id);
+    if (d == 0) {  // x = 0: block 0, one segment of length 2^n
+      segs[refs[blocks[0].first].off + i] = v;
+      continue;
+    }
+    const u64 x = i ^ (u64)j;
+    const int t = 63 - __clzll(x);
+    const u64 e = ((2ull << t) - 1ull) - x;
+    const BandBlockDev B = blocks[xblock[t * s + (int)e]];
+    const u64 l = i & ((2ull << t) - 1ull);
+    for (int k = 0; k < B.nL; ++k) {
+      const BandSegRef r = refs[B.first + k];
+      if (r.l == l) {
+        segs[r.off + (i >> (t + 1))] = v;
+        break;
+      }
+    }
+  }
+}
+
+// Expansion: out[b][z] = 2^-n i^{popcount(x_b & z)} sum_k (-1)^{popcount(l_k & z_lo)} W_k[z_hi].
+// One CTA row per block b (blockIdx.y): its segment references are staged in SMEM once;
+// every warp then produces 256 consecutive outputs, 8 per lane (z = base + lane + 32 j), so
+// 8 independent accumulations keep their loads in flight (W values are shared by runs of
+// 2^{t+1} consecutive z: L1 broadcast) and each store instruction writes 512 B.
+// Warps walk the output in address order (group g = 256 consecutive outputs of block
+// g >> (n-8)), like the tridiagonal expansion: the chip's write front stays within a few
+// tens of MiB, which keeps HBM row-buffer locality (a grid with one CTA row per block
+// spreads the front over all blocks and ran 2.5x slower).
+__global__ void __launch_bounds__(256, 4) band_expand_kernel(const BandBlockDev* blocks, const BandSegRef* refs,
+                                                             const double2* segs, int nblocks, int n,
+                                                             double scale, double2* out) {
+  const u64 N = 1ull << n;
+  const unsigned lane = threadIdx.x & 31;
+  const int gshift = n - 8;  // groups per block = 2^(n-8); z < 2^28 fits 32 bits
+  const u64 groups = (u64)nblocks << gshift;
+  for (u64 gi = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; gi < groups;
+       gi += ((u64)gridDim.x * blockDim.x) >> 5) {
+    const int b = (int)(gi >> gshift);
     const BandBlockDev B = blocks[b];
     const int sh = B.t + 1;
-    const u64 lomask = (1ull << sh) - 1ull;
-    for (u64 z = (u64)blockIdx.x * blockDim.x + threadIdx.x; z < N; z += (u64)gridDim.x * blockDim.x) {
-      const u64 zlo = z & lomask, zhi = z >> sh;
-      double re = 0.0, im = 0.0;
-      for (int k = 0; k < B.nL; ++k) {
-        const BandSegRef r = refs[B.first + k];
-        const double2 w = __ldg(segs + r.off + zhi);
-        if (__popcll(r.l & zlo) & 1) { re -= w.x; im -= w.y; }
-        else { re += w.x; im += w.y; }
+    const unsigned lomask = (1u << sh) - 1u;
+    const unsigned z0 = ((unsigned)(gi & ((1ull << gshift) - 1ull)) << 8) + lane;
+    double re[8], im[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { re[j] = 0.0; im[j] = 0.0; }
+    for (int k = 0; k < B.nL; ++k) {
+      const BandSegRef r = refs[B.first + k];
+      const double2* W = segs + r.off;
+      const unsigned lm = (unsigned)r.l & lomask;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const unsigned z = z0 + 32u * j;
+        const double2 w = __ldg(W + (z >> sh));
+        const double sg = (__popc(lm & z) & 1) ? -1.0 : 1.0;
+        re[j] = fma(sg, w.x, re[j]);
+        im[j] = fma(sg, w.y, im[j]);
       }
-      const double2 c = rot_ipow(make_double2(re, im), __popcll(B.x & z));
-      st_stream(out + (u64)b * N + z, make_double2(c.x * scale, c.y * scale));
     }
+    double2* ob = out + (u64)b * N;
+    const unsigned xb = (unsigned)B.x;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const unsigned z = z0 + 32u * j;
+      const double2 c = rot_ipow(make_double2(re[j], im[j]), __popc(xb & z));
+      st_stream(ob + z, make_double2(c.x * scale, c.y * scale));
+    }
+  }
+}
+
+// n < 8 (fewer than 256 outputs per block): one output per thread.
+__global__ void band_expand_small_kernel(const BandBlockDev* blocks, const BandSegRef* refs, const double2* segs,
+                                         int nblocks, int n, double scale, double2* out) {
+  const u64 N = 1ull << n;
+  for (u64 id = (u64)blockIdx.x * blockDim.x + threadIdx.x; id < (u64)nblocks * N;
+       id += (u64)gridDim.x * blockDim.x) {
+    const BandBlockDev B = blocks[id >> n];
+    const u64 z = id & (N - 1);
+    const int sh = B.t + 1;
+    const u64 zlo = z & ((1ull << sh) - 1ull), zhi = z >> sh;
+    double re = 0.0, im = 0.0;
+    for (int k = 0; k < B.nL; ++k) {
+      const BandSegRef r = refs[B.first + k];
+      const double2 w = segs[r.off + zhi];
+      if (__popcll(r.l & zlo) & 1) { re -= w.x; im -= w.y; }
+      else { re += w.x; im += w.y; }
+    }
+    const double2 c = rot_ipow(make_double2(re, im), __popcll(B.x & z));
+    out[id] = make_double2(c.x * scale, c.y * scale);
   }
 }
 
@@ -619,13 +700,31 @@ cudaError_t launch_band_s(const double2* diags, int n, int s, double2* out, void
   std::vector<int4> gat(nseg);
   for (int k = 0; k < nseg; ++k) gat[k] = make_int4(p.seg_t[k], p.seg_d[k], p.seg_lam[k], 0);
   memcpy(host.data() + nb * sizeof(BandBlockDev) + nseg * sizeof(BandSegRef), gat.data(), nseg * sizeof(int4));
+  // x -> block table for the diagonal-order gather
+  const int sw = s > 0 ? s : 1;
+  std::vector<int> xb((size_t)n * sw, -1);
+  for (int bi = 0; bi < nb; ++bi) {
+    const BandBlockDev& B = p.blocks[bi];
+    if (B.t < 0) continue;
+    const unsigned long long e = ((2ull << B.t) - 1ull) - B.x;
+    if (e < (unsigned long long)sw) xb[(size_t)B.t * sw + e] = bi;
+  }
+  const size_t xb_off = nb * sizeof(BandBlockDev) + nseg * sizeof(BandSegRef) + nseg * sizeof(int4);
+  memcpy(host.data() + xb_off, xb.data(), xb.size() * sizeof(int));
+  const int* dxb = reinterpret_cast<const int*>(base + xb_off);
   // pageable source: the call returns once the bytes are staged, so `host` may go
   cudaError_t e = cudaMemcpyAsync(base, host.data(), p.table_bytes, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return e;
   const int sms = device_sm_count();
-  {
+  if (s >= 1) {
+    const u64 total = (u64)(2 * s + 1) << n;
+    u64 g = (total + 255) / 256;
+    if (g > (u64)sms * 16) g = (u64)sms * 16;
+    band_gather_diag_kernel<<<(unsigned)g, 256, 0, st>>>(diags, n, s, dblocks, drefs, dxb, segs);
+    *nl += 1;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  } else {
     dim3 grid((unsigned)(sms * 4 > 1 ? sms * 4 : 1), (unsigned)(nseg < 65535 ? nseg : 65535));
-    // long segments dominate; short ones use a few threads of their row of blocks
     band_gather_kernel<<<grid, 256, 0, st>>>(diags, n, s, drefs, dgat, nseg, segs);
     *nl += 1;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -640,10 +739,15 @@ cudaError_t launch_band_s(const double2* diags, int n, int s, double2* out, void
   }
   {
     const u64 N = 1ull << n;
-    u64 gx = (N + 255) / 256;
-    if (gx > (u64)sms * 8) gx = (u64)sms * 8;
-    dim3 grid((unsigned)gx, (unsigned)(nb < 65535 ? nb : 65535));
-    band_expand_kernel<<<grid, 256, 0, st>>>(dblocks, drefs, segs, nb, n, ldexp(1.0, -n), out);
+    if (n >= 8) {
+      u64 g = (((u64)nb << (n - 8)) + 7) / 8;
+      if (g > (u64)sms * 16) g = (u64)sms * 16;
+      band_expand_kernel<<<(unsigned)g, 256, 0, st>>>(dblocks, drefs, segs, nb, n, ldexp(1.0, -n), out);
+    } else {
+      u64 g = ((u64)nb * N + 255) / 256;
+      if (g > (u64)sms * 16) g = (u64)sms * 16;
+      band_expand_small_kernel<<<(unsigned)g, 256, 0, st>>>(dblocks, drefs, segs, nb, n, ldexp(1.0, -n), out);
+    }
     *nl += 1;
     e = cudaGetLastError();
   }

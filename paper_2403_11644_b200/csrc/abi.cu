@@ -75,15 +75,16 @@ static bool pipe_mode(int mode) {
 }
 
 static DensePlan plan_for(int mode, int nv, uint64_t x_count) {
-  return make_dense_plan(nv, x_count, pipe_mode(mode) ? pipe_choice() : kPipeNone);
+  return make_dense_plan(nv, x_count, pipe_mode(mode) ? pipe_choice() : kPipeNone, kSingleMax);
 }
 // The workspace is the max over every kernel choice so the env switches never need more.
 static size_t plan_ws(int nv, uint64_t x_count) {
   size_t m = 0;
-  for (int cfg = kPipeNone; cfg <= kPipeCfgCount; ++cfg) {
-    const size_t b = make_dense_plan(nv, x_count, cfg).ws_bytes();
-    if (b > m) m = b;
-  }
+  for (int cfg = kPipeNone; cfg <= kPipeCfgCount; ++cfg)
+    for (int smax : {7, kSingleMax}) {
+      const size_t b = make_dense_plan(nv, x_count, cfg, smax).ws_bytes();
+      if (b > m) m = b;
+    }
   return m;
 }
 
@@ -298,7 +299,6 @@ ptdr_status ptdr_decompose_xshard_async(const ptdr_c128* A_local, int n, int ran
   const uint64_t N = 1ull << n, R = N >> g;
   if (overlaps(A_local, N * R * 16, out_local, N * R * 16)) return fail(PTDR_EUNSUPPORTED, "out overlaps A");
   DensePlan p = plan_for(MODE_GENERAL, n, R);
-  if (p.kind == 1) { p.kind = 0; p.nchunks = R / 16; }  // narrow shards: direct kernel
   DenseArgs a = base_args(reinterpret_cast<const double2*>(A_local), reinterpret_cast<double2*>(out_local),
                           n, workspace);
   a.ld = R;

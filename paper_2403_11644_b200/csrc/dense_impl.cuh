@@ -165,16 +165,20 @@ template <int MODE>
 struct LoadS {
   const DenseArgs* a;
   u64 xfirst;
+  int t;  // half-length modes: index bit removed (top bit of the tile's X-masks)
   __device__ __forceinline__ double2 operator()(int f, int j) const {
-    return load_v<MODE>(*a, (u64)j, xfirst + (u64)f);
+    u64 row = (u64)j;
+    if constexpr (MODE == MODE_HERM_HALF || MODE == MODE_SYM_HALF) row = insert0(row, t);
+    return load_v<MODE>(*a, row, xfirst + (u64)f);
   }
 };
 template <int MODE>
 struct StoreS {
   const DenseArgs* a;
   u64 xfirst;
+  int t;
   __device__ __forceinline__ void operator()(int f, int j, double2 v) const {
-    emit<MODE>(*a, xfirst + (u64)f, (u64)j, v, 0);
+    emit<MODE>(*a, xfirst + (u64)f, (u64)j, v, t);
   }
 };
 
@@ -253,9 +257,13 @@ __global__ void __launch_bounds__(kThreads, 2) dense_single_kernel(DenseArgs a) 
   const u64 ntiles = nx / F;
   for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const u64 xfirst = a.x_base + tile * F;
-    LoadS<MODE> ld{&a, xfirst};
-    StoreS<MODE> st{&a, xfirst};
-    fiber_tile<R>(S, ld, st);
+    // the F X-masks of a tile share their top bit (tiles are F-aligned, x_base a power of
+    // two >= F in the half-length modes)
+    const int t = top_bit_for<MODE>(xfirst);
+    LoadS<MODE> ld{&a, xfirst, t};
+    StoreS<MODE> st{&a, xfirst, t};
+    if constexpr (R <= 8) fiber_tile<R>(S, ld, st);
+    else fiber_tile3<R>(S, ld, st);
     __syncthreads();
   }
 }

@@ -66,11 +66,17 @@ cudaError_t launch_dense_mode_impl(const DenseArgs& a_in, const DensePlan& p, cu
     return cudaErrorInvalidValue;
   }
   if (p.kind == 1) {
-    if constexpr (MODE <= MODE_SYM_MIRROR) {
+    {
       const u64 nx = a.nchunks * 16;
       *nlaunch += 1;
-      if (p.R == 6) return launch_single<6, MODE>(a, nx / (kTileElems >> 6), st);
-      if (p.R == 7) return launch_single<7, MODE>(a, nx / (kTileElems >> 7), st);
+      switch (p.R) {
+        case 6: return launch_single<6, MODE>(a, nx / (kTileElems >> 6), st);
+        case 7: return launch_single<7, MODE>(a, nx / (kTileElems >> 7), st);
+        case 8: return launch_single<8, MODE>(a, nx / (kTileElems >> 8), st);
+        case 9: return launch_single<9, MODE>(a, nx / (kTileElems >> 9), st);
+        case 10: return launch_single<10, MODE>(a, nx / (kTileElems >> 10), st);
+        default: break;
+      }
     }
     return cudaErrorInvalidValue;
   }

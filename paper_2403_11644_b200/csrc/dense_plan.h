@@ -75,11 +75,22 @@ inline bool pipe_fits(int cfg, int nv, uint64_t x_count) {
 // pipe_cfg: requested dense_pipe configuration (0 = v1 kernels); falls back when it does
 // not fit (phase-B length M = nv - (LT - XB) must be in [4, 8], x_count a multiple of the
 // chunk width).
-inline DensePlan make_dense_plan(int nv, uint64_t x_count, int pipe_cfg = kPipeNone) {
+// Whole-vector (single-phase) tiles for nv <= kSingleMax: a 4096-element tile holds
+// 4096 / 2^nv complete vectors (n = 10: 4 X-masks), one pass over HBM and no inter-CTA
+// dependencies -- at these sizes the two-phase pipeline is latency-bound.
+constexpr int kSingleMax = 10;
+
+inline DensePlan make_dense_plan(int nv, uint64_t x_count, int pipe_cfg = kPipeNone,
+                                 int single_max = kSingleMax) {
   DensePlan p;
   p.nv = nv;
   if (nv <= 5) { p.kind = 0; p.nchunks = x_count >= 16 ? x_count / 16 : 1; return p; }
-  if (nv <= 7) { p.kind = 1; p.R = nv; p.M = 0; p.nchunks = x_count / 16; return p; }
+  if (nv <= single_max) {
+    if (x_count % (4096u >> nv) == 0 && x_count >= 16) {
+      p.kind = 1; p.R = nv; p.M = 0; p.nchunks = x_count / 16; return p;
+    }
+    if (nv <= 7) { p.kind = 0; p.nchunks = x_count >= 16 ? x_count / 16 : 1; return p; }  // tiny shards
+  }
   p.kind = 2;
   if (pipe_cfg != kPipeNone && !pipe_fits(pipe_cfg, nv, x_count))
     pipe_cfg = pipe_fits(pipe_fallback(pipe_cfg), nv, x_count) ? pipe_fallback(pipe_cfg) : kPipeNone;

@@ -139,6 +139,55 @@ __device__ __forceinline__ void fiber_tile(double2* S, const Ld& ld, const St& s
   }
 }
 
+// fiber_tile3<K> (K = 9, 10): F = 4096 / 2^K fibres of length 2^K in three register stages
+// (bits 0-3, 4-7, 8..K-1) with two SMEM exchanges; element (f, j) lives at S[j F + f], so
+// lanes always run along f and then the low bits of j (conflict-free, and the loads/stores
+// of consecutive lanes touch consecutive fibres).  Used for whole-vector tiles at n = 9, 10.
+template <int K, class Ld, class St>
+__device__ __forceinline__ void fiber_tile3(double2* S, const Ld& ld, const St& st) {
+  static_assert(K == 9 || K == 10, "three-stage tile");
+  constexpr int F = kTileElems >> K;
+  constexpr int K3 = K - 8;        // bits of the third stage
+  constexpr int U3 = 16 >> K3;     // third-stage units per thread
+  const int tid = threadIdx.x;
+  double2 v[16];
+  {  // stage 1: bits 0-3
+    const int f = tid % F, jh = tid / F;
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) v[kk] = ld(f, jh * 16 + kk);
+    wht_regs<4>(v);
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) S[(jh * 16 + kk) * F + f] = v[kk];
+  }
+  __syncthreads();
+  {  // stage 2: bits 4-7
+    const int f = tid % F, rest = tid / F;
+    const int jl = rest & 15, jt = rest >> 4;
+#pragma unroll
+    for (int m = 0; m < 16; ++m) v[m] = S[((jt * 16 + m) * 16 + jl) * F + f];
+    wht_regs<4>(v);
+#pragma unroll
+    for (int m = 0; m < 16; ++m) S[((jt * 16 + m) * 16 + jl) * F + f] = v[m];
+  }
+  __syncthreads();
+  // stage 3: bits 8..K-1
+#pragma unroll
+  for (int p = 0; p < U3; ++p) {
+    const int uu = tid + kThreads * p;
+    const int f = uu % F, jlow = uu / F;
+#pragma unroll
+    for (int q = 0; q < (1 << K3); ++q) v[p * (1 << K3) + q] = S[(q * 256 + jlow) * F + f];
+  }
+#pragma unroll
+  for (int p = 0; p < U3; ++p) {
+    const int uu = tid + kThreads * p;
+    const int f = uu % F, jlow = uu / F;
+    wht_regs<K3>(&v[p * (1 << K3)]);
+#pragma unroll
+    for (int q = 0; q < (1 << K3); ++q) st(f, q * 256 + jlow, v[p * (1 << K3) + q]);
+  }
+}
+
 // Global-memory access helpers with cache hints.
 __device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }   // read-once input
 __device__ __forceinline__ double ld_stream_re(const double2* p) { return __ldcs(reinterpret_cast<const double*>(p)); }

@@ -435,16 +435,22 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
           const uint32_t x0 = (uint32_t)a.x_base + (chX << XB);
           const int t = HALF ? 31 - __clz(x0) : 0;
           const uint32_t cm = (uint32_t)a.colmask & ~(uint32_t)(W - 1);
+          // peer-pull: all rows of a tile lie in one rank's shard (R >= rows per tile), so
+          // the tensor map and the row mask are chosen once per tile
+          const CUtensorMap* tm = &maps.m[0];
+          uint32_t rmask = 0xFFFFFFFFu;
+          if (a.peer_shift) {
+            const uint32_t r0 = (tlX << R);
+            tm = &maps.m[r0 >> a.peer_shift];
+            rmask = (uint32_t)a.peer_rowmask;
+          }
 #pragma unroll
           for (int rb = 0; rb < (1 << (R - XB)); ++rb) {
             const uint32_t iv0 = (tlX << R) + (uint32_t)rb * W;
             uint32_t row0 = HALF ? insert0_32(iv0, t) : iv0;
             if constexpr ((kDiag & 2) != 0) row0 &= 255u;
             const uint32_t col0 = (row0 ^ x0) & cm;
-            // peer-pull: the 128 rows of a tile lie in one rank's shard (R >= 128)
-            const CUtensorMap* tm = a.peer_shift ? &maps.m[row0 >> a.peer_shift] : &maps.m[0];
-            const uint32_t rowc = a.peer_shift ? (row0 & (uint32_t)a.peer_rowmask) : row0;
-            tma_load_2d(dst + rb * W * W, tm, (int)(col0 * 2u), (int)rowc, &full[s], pol);
+            tma_load_2d(dst + rb * W * W, tm, (int)(col0 * 2u), (int)(row0 & rmask), &full[s], pol);
           }
         } else {
           if constexpr (kBDirect) {

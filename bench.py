@@ -221,6 +221,7 @@ def main():
         dist.barrier()
 
     ev_kernel = []
+    ev_xchg = []
 
     def step(record):
         if world == 1:
@@ -240,8 +241,13 @@ def main():
                 e1.record(stream)
                 ev_kernel.append((e0, e1))
         else:
+            if record:
+                x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                x0.record(stream)
             pdist.exchange(send, None, recv)
             if record:
+                x1.record(stream)
+                ev_xchg.append((x0, x1))
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
             ptdr.decompose_xshard(recv.view(N, N // world), n, rank, world, out=out, workspace=ws,
@@ -275,10 +281,11 @@ def main():
     clk = clocks.stop() if rank == 0 else None
     elapsed_ms = t0.elapsed_time(t1)
     kern_ms = [e0.elapsed_time(e1) for e0, e1 in ev_kernel]
+    xmean = statistics.mean([x0.elapsed_time(x1) for x0, x1 in ev_xchg]) if ev_xchg else 0.0
     if world > 1:
-        tt = torch.tensor([elapsed_ms, statistics.mean(kern_ms)], dtype=torch.float64, device=dev)
+        tt = torch.tensor([elapsed_ms, statistics.mean(kern_ms), xmean], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        elapsed_ms, kmean = tt.tolist()
+        elapsed_ms, kmean, xmean = tt.tolist()
     else:
         kmean = statistics.mean(kern_ms)
     ms_per_step = elapsed_ms / a.steps
@@ -324,9 +331,18 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_kind": peak_kind, "kernel": "dense_pipe_kernel (PTDR_PIPE_CFG=%s)" % os.environ.get("PTDR_PIPE_CFG", "default"),
-                         "kernel_ms": kmean, "algorithmic_bytes_per_launch": alg_bytes},
+                         "kernel_ms": kmean, "algorithmic_bytes_per_launch": alg_bytes,
+                         "hbm_passes": 1, "l2_round_trips": 1,
+                         "note": "32 B/coefficient (16 B read of A + 16 B write); the partial "
+                                 "transforms make one round trip through an L2-resident scratch "
+                                 "(DESIGN.md section 7)"},
             "hbm_gbs_step": 32 * coeffs_total / (ms_per_step * 1e-3) / 1e9 / world,
             "gpu_launches": launches,
+            "nvlink": (None if not ev_xchg else {
+                "exchange_ms": xmean,
+                "bytes_sent_per_rank": 16 * coeffs_total // world * (world - 1) // world,
+                "gbs_per_rank": 16 * coeffs_total // world * (world - 1) // world / (xmean * 1e-3) / 1e9,
+                "peak_per_direction_gbs": 770.0, "peak_kind": "measured peer copy (B200_PROFILING.md)"}),
             "generator_ms": gen_ms,
             "parseval_rel": parseval,
             "clocks": clk,

@@ -384,6 +384,47 @@ def main():
                        "api": "ptdr_plan_decompose_host_async, depth 2 (pinned host buffers)"}
         del host_in, host_out, hin, houts
 
+    # ---- end to end at N > 1: every rank uploads its row block from pinned host memory,
+    # the step runs (exchange + decomposition, or the peer-pull kernel), and every rank
+    # downloads its coefficient shard; wall time between barriers, max over ranks.
+    if world > 1 and not a.no_e2e:
+        try:
+            src = shard if peer_ptrs is not None else send
+            host_in = torch.empty(src.shape, dtype=src.dtype, pin_memory=True)
+            host_in.copy_(src)
+            host_out = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+            K = max(2, a.e2e_steps)
+            torch.cuda.synchronize()
+            dist.barrier()
+            s0 = time.perf_counter()
+            for _ in range(K):
+                src.copy_(host_in, non_blocking=True)
+                if peer_ptrs is not None:
+                    torch.cuda.synchronize()
+                    dist.barrier()          # every shard uploaded before any rank reads it
+                    pdist.decompose_peer_sharded(shard, n, peer_ptrs, out=out, workspace=ws, stream=stream)
+                    torch.cuda.synchronize()
+                    dist.barrier()          # every rank done reading before the next upload
+                else:
+                    pdist.decompose_sharded(send, n, out=out, recv=recv, workspace=ws, stream=stream)
+                host_out.copy_(out, non_blocking=True)
+            torch.cuda.synchronize()
+            dist.barrier()
+            tt = torch.tensor([(time.perf_counter() - s0) / K], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_s = tt.item()
+            if rank == 0:
+                line["e2e"] = {"value": coeffs_total / e2e_s, "unit": UNIT,
+                               "h2d_bytes_per_step": 16 * coeffs_total,
+                               "d2h_bytes_per_step": 16 * coeffs_total, "steps": K, "s_per_step": e2e_s,
+                               "api": "pinned host row blocks -> " + ("decompose_peer_sharded" if peer_ptrs
+                                                                     is not None else "decompose_sharded")
+                                      + " -> pinned host shards (all ranks)"}
+            del host_in, host_out
+        except Exception as exc:  # never lose the bench line over the e2e leg
+            if rank == 0:
+                line["e2e"] = {"error": repr(exc)[:200]}
+
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(n, a.cpu_seconds)
     if rank == 0:

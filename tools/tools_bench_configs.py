@@ -48,7 +48,9 @@ def oracle_rate(fn, n_out, seconds=2.0):
     while time.perf_counter() - t0 < seconds:
         fn(rng.integers(0, n_out, batch, dtype=np.uint64))
         done += batch
-    return {"oracle_coeffs_per_s": done / (time.perf_counter() - t0), "oracle_cores": oracle.threads()}
+    rate = done / (time.perf_counter() - t0)
+    return {"oracle_coeffs_per_s": rate, "oracle_cores": oracle.threads(),
+            "oracle_projected_full_s": n_out / rate}
 
 
 def dense(name, n, seed, variant):

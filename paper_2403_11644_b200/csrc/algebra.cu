@@ -98,6 +98,130 @@ __global__ void xscatter_small_kernel(const double2* __restrict__ V, double2* __
   }
 }
 
+// ---- two-pass inverse (9 <= n <= 16): 32 B of HBM traffic per coefficient per pass ---------
+// Pass 1: a tile = 16 X-masks (x bits 0-3) x 256 Z-masks (z bits 0-7) with the other bits
+// fixed; in q order that is 16 runs of 256 consecutive coefficients (one run per value of z
+// bits 4-7), read coalesced.  Conjugate phase, WHT over z bits 0-7 per X-mask (the contig8
+// register/SMEM scheme), stored as U[x >> 5][z][x & 31] (32 X-masks contiguous, so pass 2
+// reads 512 B runs).  Pass 2: fibres = (32 consecutive X-masks) x (Z-masks with equal low 8
+// bits), WHT over z bits 8..n-1, then the XOR scatter A[i][i ^ x] with i = z: for one i the
+// 32 X-masks hit one aligned 32-column window (512 B per warp store).
+__device__ __forceinline__ int inv_slot(int f, int j) { return f * 273 + (j >> 4) * 17 + (j & 15); }
+constexpr int kInvSmem = 16 * 273 * 16;
+
+__global__ void __launch_bounds__(256, 2) inv_pass1_kernel(const double2* __restrict__ c, double2* __restrict__ U,
+                                                           int n) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* T = reinterpret_cast<double2*>(smem_raw);
+  const u64 N = 1ull << n;
+  const u64 xtiles = N >> 4;
+  const u64 tiles = xtiles * (N >> 8);
+  const int tid = threadIdx.x;
+  // this thread's (x bits 0-3, z bits 0-3) = the decode of q bits 0-7 = tid
+  const u64 zl4 = compact_even((u64)tid >> 1) & 15ull;
+  const u64 xl4 = (compact_even((u64)tid) & 15ull) ^ zl4;
+  for (u64 tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const u64 xt = (tile % xtiles) << 4, zt = (tile / xtiles) << 8;
+    const u64 x = xt | xl4;
+    double2 v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {  // all 16 loads in flight before any use
+      const u64 z = zt | ((u64)r << 4) | zl4;
+      v[r] = ld_stream(c + (spread_bits(x ^ z) | (spread_bits(z) << 1)));
+    }
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const u64 z = zt | ((u64)r << 4) | zl4;
+      T[inv_slot((int)xl4, (r << 4) | (int)zl4)] = rot_ipow(v[r], 4 - (__popcll(x & z) & 3));
+    }
+    __syncthreads();
+    {
+      const int f = tid >> 4, jl = tid & 15;
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) v[kk] = T[inv_slot(f, jl + 16 * kk)];
+      wht_regs<4>(v);
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) T[inv_slot(f, jl + 16 * kk)] = v[kk];
+    }
+    __syncthreads();
+    {
+      const int f = tid >> 4, kh = tid & 15;
+#pragma unroll
+      for (int jl = 0; jl < 16; ++jl) v[jl] = T[inv_slot(f, jl + 16 * kh)];
+      wht_regs<4>(v);
+#pragma unroll
+      for (int jl = 0; jl < 16; ++jl) T[inv_slot(f, jl + 16 * kh)] = v[jl];
+    }
+    __syncthreads();
+    {
+      const int f = tid & 15, jg = tid >> 4;
+      const u64 xo = xt + (u64)f;
+#pragma unroll 4
+      for (int kk = 0; kk < 16; ++kk) {
+        const int j = jg + 16 * kk;
+        st_stream(U + ((((xo >> 5) << n) + zt + (u64)j) << 5) + (xo & 31ull), T[inv_slot(f, j)]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int K>
+struct InvLd {
+  const double2* U;
+  u64 xbase, zbase;
+  int n, xw;
+  __device__ __forceinline__ double2 operator()(int f, int j) const {
+    const u64 x = xbase + (u64)(f % xw), z = zbase + (u64)(f / xw) + ((u64)j << 8);
+    return ld_stream(U + ((((x >> 5) << n) + z) << 5) + (x & 31ull));
+  }
+};
+template <int K>
+struct InvSt {
+  double2* A;
+  u64 xbase, zbase;
+  int n, xw;
+  __device__ __forceinline__ void operator()(int f, int j, double2 v) const {
+    const u64 x = xbase + (u64)(f % xw), z = zbase + (u64)(f / xw) + ((u64)j << 8);
+    st_stream(A + (z << n) + (z ^ x), v);  // A[i][i ^ x], i = z
+  }
+};
+
+template <int K>
+__global__ void __launch_bounds__(kThreads, 2) inv_pass2_kernel(const double2* __restrict__ U, double2* __restrict__ A,
+                                                               int n) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* S = reinterpret_cast<double2*>(smem_raw);
+  constexpr int F = kTileElems >> K;
+  constexpr int XW = F < 32 ? F : 32;  // X-masks per tile
+  constexpr int ZS = F / XW;           // low-z values per tile
+  const u64 N = 1ull << n;
+  const u64 xtiles = N / XW, ztiles = 256 / ZS;
+  for (u64 tile = blockIdx.x; tile < xtiles * ztiles; tile += gridDim.x) {
+    const u64 xbase = (tile % xtiles) * XW, zbase = (tile / xtiles) * ZS;
+    InvLd<K> ld{U, xbase, zbase, n, XW};
+    InvSt<K> st{A, xbase, zbase, n, XW};
+    fiber_tile<K>(S, ld, st);
+    __syncthreads();
+  }
+}
+
+template <int K>
+static cudaError_t launch_inv_pass2(const double2* U, double2* A, int n, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(inv_pass2_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kTileBytes);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  u64 tiles = (1ull << (2 * n)) / kTileElems;
+  u64 g = (u64)device_sm_count() * 2;
+  if (g > tiles) g = tiles;
+  inv_pass2_kernel<K><<<(unsigned)g, kThreads, kTileBytes, st>>>(U, A, n);
+  return cudaGetLastError();
+}
+
 size_t reconstruct_workspace_bytes(int n) { return (size_t)16 << (2 * n); }
 
 cudaError_t launch_reconstruct(const double2* c, int n, double2* A, void* ws, cudaStream_t st, int* nl) {
@@ -105,6 +229,31 @@ cudaError_t launch_reconstruct(const double2* c, int n, double2* A, void* ws, cu
   double2* U = reinterpret_cast<double2*>(ws);
   const int sms = device_sm_count();
   cudaError_t e;
+  if (n >= 9 && n <= 16) {
+    static bool attr1 = false;
+    if (!attr1) {
+      if ((e = cudaFuncSetAttribute(inv_pass1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kInvSmem)) !=
+          cudaSuccess)
+        return e;
+      attr1 = true;
+    }
+    u64 g = (N * N) >> 12;
+    if (g > (u64)sms * 2) g = (u64)sms * 2;
+    inv_pass1_kernel<<<(unsigned)g, 256, kInvSmem, st>>>(c, U, n);
+    *nl += 1;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    *nl += 1;
+    switch (n - 8) {
+      case 1: return launch_inv_pass2<1>(U, A, n, st);
+      case 2: return launch_inv_pass2<2>(U, A, n, st);
+      case 3: return launch_inv_pass2<3>(U, A, n, st);
+      case 4: return launch_inv_pass2<4>(U, A, n, st);
+      case 5: return launch_inv_pass2<5>(U, A, n, st);
+      case 6: return launch_inv_pass2<6>(U, A, n, st);
+      case 7: return launch_inv_pass2<7>(U, A, n, st);
+      default: return launch_inv_pass2<8>(U, A, n, st);
+    }
+  }
   if (n >= 6) {
     static bool attr = false;
     if (!attr) {

@@ -40,7 +40,7 @@ def test_reconstruct_vs_kronecker(gpu, n):
     assert np.max(np.abs(got - want)) <= TOL * np.max(np.abs(want)) * 4 ** n
 
 
-@pytest.mark.parametrize("n", [1, 3, 5, 6, 8, 10, 11])
+@pytest.mark.parametrize("n", [1, 3, 5, 6, 8, 9, 10, 11])
 def test_reconstruct_inverts_oracle(gpu, n):
     """reconstruct(oracle coefficients of A) == A (Theorem 1 uniqueness, l.98-121)."""
     A = ptdr_inputs.dense(n, 60 + n, "general")
@@ -49,7 +49,7 @@ def test_reconstruct_inverts_oracle(gpu, n):
     assert np.max(np.abs(got - A)) <= 1e-12 * np.max(np.abs(A)) * n
 
 
-@pytest.mark.parametrize("n", [13, 15])
+@pytest.mark.parametrize("n", [12, 13, 14, 15])
 def test_round_trip_large(gpu, n):
     """Full-size round trip A -> decompose -> reconstruct on the device (a property that
     holds at any size), at the bench configuration n = 15."""

@@ -115,6 +115,14 @@ ptdr_status ptdr_decompose_async(const ptdr_c128* A, int n, int structure, ptdr_
 ptdr_status ptdr_decompose_host(const ptdr_c128* A_host, int n, int structure,
                                 ptdr_c128* out_host);
 
+/* Batched small matrices (serving many decompositions per launch): A = [batch][2^n][2^n]
+ * dense matrices of one structure stored back to back, out = [batch][4^n] coefficient
+ * arrays in q order; 1 <= n <= 10 (the whole-vector and direct kernels: no workspace, one
+ * launch -- two for HERMITIAN / REAL_SYMMETRIC at n >= 9 -- for the whole batch).  Each
+ * matrix's result is bitwise identical to ptdr_decompose_async on it alone. */
+ptdr_status ptdr_decompose_batched_async(const ptdr_c128* A, int n, int structure, uint64_t batch,
+                                         ptdr_c128* out, void* stream);
+
 /* Zero padding ("we can use a zero padding to make any size of matrix
  * fit this constraint"): A is an m x m matrix of a dense structure stored row-major with
  * row pitch lda >= m (elements); it is decomposed as the top-left block of a 2^n x 2^n

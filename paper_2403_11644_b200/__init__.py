@@ -90,6 +90,8 @@ def lib():
         L.ptdr_generated_workspace_bytes.restype = sz
         L.ptdr_decompose_generated_async.argtypes = [i32, u64, i32, i32, vp, vp, sz, vp]
         L.ptdr_decompose_generated_async.restype = i32
+        L.ptdr_decompose_batched_async.argtypes = [vp, i32, i32, u64, vp, vp]
+        L.ptdr_decompose_batched_async.restype = i32
         L.ptdr_generate_dense_async.argtypes = [i32, u64, i32, u64, u64, vp, vp]
         L.ptdr_generate_band_async.argtypes = [i32, u64, i32, vp, vp]
         L.ptdr_generate_sendblocks_async.argtypes = [i32, u64, i32, i32, vp, vp]
@@ -298,6 +300,28 @@ def decompose_xshard(A_local, n: int, rank: int, world: int, out=None, workspace
                                            ctypes.c_void_p(workspace.data_ptr()),
                                            workspace.numel(), _stream_ptr(stream))
     _check(st, "ptdr_decompose_xshard_async")
+    return out
+
+
+def decompose_batched(A, structure="general", out=None, stream=None):
+    """A batch of small dense matrices [batch, 2^n, 2^n] (n <= 10) in one launch
+    (ptdr_decompose_batched_async) -> [batch, 4^n] coefficients."""
+    import torch
+
+    _require_cuda_c128(A, "A")
+    if A.dim() != 3 or A.shape[1] != A.shape[2]:
+        raise ValueError("A must be [batch, 2^n, 2^n]")
+    B, N = A.shape[0], A.shape[1]
+    n = N.bit_length() - 1
+    if (1 << n) != N:
+        raise ValueError("2^n x 2^n matrices")
+    s = _structure(structure)
+    if out is None:
+        out = torch.empty((B, 4 ** n), dtype=torch.complex128, device=A.device)
+    _require_cuda_c128(out, "out")
+    _check(lib().ptdr_decompose_batched_async(ctypes.c_void_p(A.data_ptr()), n, s, B,
+                                              ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)),
+           "ptdr_decompose_batched_async")
     return out
 
 

@@ -143,13 +143,20 @@ static DenseArgs base_args(const double2* A, double2* out, int n, void* ws) {
 }
 
 static ptdr_status run_dense(const double2* A, int n, int s, double2* out, void* ws,
-                             cudaStream_t st, int* nl, uint64_t lda = 0, uint64_t m = 0) {
+                             cudaStream_t st, int* nl, uint64_t lda = 0, uint64_t m = 0,
+                             uint64_t batch = 0) {
   const uint64_t N = 1ull << n;
+  auto batched = [&](DenseArgs& a) {
+    a.batch = batch;
+    a.bstride_in = N * N;
+    a.bstride_out = N * N;
+  };
   if (s == PTDR_GENERAL || n <= 8) {
     const int mode = s == PTDR_GENERAL ? MODE_GENERAL
                      : s == PTDR_HERMITIAN ? MODE_HERM_MIRROR : MODE_SYM_MIRROR;
     DensePlan p = plan_for(mode, n, N);
     DenseArgs a = base_args(A, out, n, ws);
+    batched(a);
     if (m) {  // zero-padded view (TMA pipeline only, see ptdr_decompose_padded_async)
       a.ld = lda;
       a.rows_valid = m;
@@ -168,6 +175,7 @@ static ptdr_status run_dense(const double2* A, int n, int s, double2* out, void*
   {
     DensePlan p = plan_for(MODE_HERM_MIRROR, n, w);
     DenseArgs a = base_args(A, out, n, ws);
+    batched(a);
     a.nv = n;
     a.x_base = 0;
     a.nchunks = p.nchunks;
@@ -178,6 +186,7 @@ static ptdr_status run_dense(const double2* A, int n, int s, double2* out, void*
   {
     DensePlan p = plan_for(hmode, n - 1, N - w);
     DenseArgs a = base_args(A, out, n, ws);
+    batched(a);
     a.nv = n - 1;
     a.x_base = w;
     a.nchunks = p.nchunks;
@@ -647,6 +656,39 @@ ptdr_status ptdr_decompose_padded_async(const ptdr_c128* A, uint64_t m, uint64_t
                              reinterpret_cast<char*>(workspace) + pad_b, ws_bytes - pad_b, stream);
     nl = 1 + g_last_launches;
   }
+  g_last_launches = nl;
+  return r;
+}
+
+// ---- batched small matrices -----------------------------------------------------------
+ptdr_status ptdr_decompose_batched_async(const ptdr_c128* A, int n, int structure, uint64_t batch,
+                                         ptdr_c128* out, void* stream) {
+  g_last_launches = 0;
+  if (!is_dense(structure)) return fail(PTDR_EINVAL, "batched decomposition is for the dense structures");
+  if (n < 1 || n > kSingleMax) return fail(PTDR_EINVAL, "batched decomposition needs 1 <= n <= 10");
+  if (!A || !out) return fail(PTDR_EINVAL, "null pointer");
+  if (((uintptr_t)A & 15) || ((uintptr_t)out & 15)) return fail(PTDR_EINVAL, "misaligned pointer");
+  if (batch == 0) return PTDR_OK;
+  const size_t bytes = ((size_t)16 << (2 * n)) * batch;
+  if (overlaps(A, bytes, out, bytes)) return fail(PTDR_EUNSUPPORTED, "out overlaps A");
+  {
+    // every launch of the call must be a direct or whole-vector kernel (no workspace)
+    const uint64_t N = 1ull << n;
+    bool two_phase;
+    if (structure == PTDR_GENERAL || n <= 8) {
+      const int mode = structure == PTDR_GENERAL ? MODE_GENERAL
+                       : structure == PTDR_HERMITIAN ? MODE_HERM_MIRROR : MODE_SYM_MIRROR;
+      two_phase = plan_for(mode, n, N).kind == 2;
+    } else {
+      const int hmode = structure == PTDR_HERMITIAN ? MODE_HERM_HALF : MODE_SYM_HALF;
+      const uint64_t w = herm_mirror_width(n, hmode);
+      two_phase = plan_for(MODE_HERM_MIRROR, n, w).kind == 2 || plan_for(hmode, n - 1, N - w).kind == 2;
+    }
+    if (two_phase) return fail(PTDR_EUNSUPPORTED, "this n would need the two-phase pipeline");
+  }
+  int nl = 0;
+  ptdr_status r = run_dense(reinterpret_cast<const double2*>(A), n, structure, reinterpret_cast<double2*>(out), nullptr,
+                            reinterpret_cast<cudaStream_t>(stream), &nl, 0, 0, batch);
   g_last_launches = nl;
   return r;
 }

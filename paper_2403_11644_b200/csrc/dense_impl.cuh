@@ -46,6 +46,9 @@ struct DenseArgs {
   int npeers;          //   shards (host side: tensor maps are built from peer_ptrs)
   const double2* peer_ptrs[8];
   u64 gen_seed;        // MODE_GEN: seed of the counter-based generator
+  u64 batch;           // batched small-n launches (direct / whole-vector kernels): matrices,
+  u64 bstride_in;      //   element stride between consecutive inputs
+  u64 bstride_out;     //   and between consecutive outputs (0 batch = 1)
   u64 rows_valid;      // zero padding: rows / columns of A actually stored;
   u64 cols_valid;      // 0 = all (the TMA tensor map fills the rest with zeros)
   unsigned long long* trace;  // pipeline debug timeline (nullptr unless PTDR_TRACE=1)
@@ -255,13 +258,18 @@ __global__ void __launch_bounds__(kThreads, 2) dense_single_kernel(DenseArgs a) 
   constexpr int F = kTileElems >> R;
   const u64 nx = a.nchunks * 16;
   const u64 ntiles = nx / F;
-  for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  const u64 nb = a.batch ? a.batch : 1;
+  for (u64 tg = blockIdx.x; tg < ntiles * nb; tg += gridDim.x) {
+    const u64 b = tg / ntiles, tile = tg - b * ntiles;
+    DenseArgs ab = a;  // matrix b of a batch
+    ab.A += b * a.bstride_in;
+    ab.out += b * a.bstride_out;
     const u64 xfirst = a.x_base + tile * F;
     // the F X-masks of a tile share their top bit (tiles are F-aligned, x_base a power of
     // two >= F in the half-length modes)
     const int t = top_bit_for<MODE>(xfirst);
-    LoadS<MODE> ld{&a, xfirst, t};
-    StoreS<MODE> st{&a, xfirst, t};
+    LoadS<MODE> ld{&ab, xfirst, t};
+    StoreS<MODE> st{&ab, xfirst, t};
     if constexpr (R <= 8) fiber_tile<R>(S, ld, st);
     else fiber_tile3<R>(S, ld, st);
     __syncthreads();
@@ -270,10 +278,15 @@ __global__ void __launch_bounds__(kThreads, 2) dense_single_kernel(DenseArgs a) 
 
 // Direct evaluation for nv <= 5 (at most 32 terms per coefficient): thread per (x, z).
 template <int MODE>
-__global__ void dense_direct_kernel(DenseArgs a, u64 nx) {
-  const u64 N = 1ull << a.n;
-  const u64 id = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  if (id >= nx * N) return;
+__global__ void dense_direct_kernel(DenseArgs a0, u64 nx) {
+  const u64 N = 1ull << a0.n;
+  const u64 gid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  const u64 per = nx * N;
+  if (gid >= per * (a0.batch ? a0.batch : 1)) return;
+  const u64 b = gid / per, id = gid - b * per;
+  DenseArgs a = a0;
+  a.A += b * a0.bstride_in;
+  a.out += b * a0.bstride_out;
   const u64 x = a.x_base + id / N, z = id % N;
   double2 s = make_double2(0.0, 0.0);
   for (u64 i = 0; i < N; ++i) {

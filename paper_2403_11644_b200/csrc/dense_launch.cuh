@@ -45,7 +45,8 @@ static cudaError_t launch_single(const DenseArgs& a, u64 ntiles, cudaStream_t st
   cudaError_t e = prep_kernel<kern>(&bps);
   if (e != cudaSuccess) return e;
   u64 grid = (u64)device_sm_count() * (u64)bps;
-  if (grid > ntiles) grid = ntiles;
+  const u64 all = ntiles * (a.batch ? a.batch : 1);
+  if (grid > all) grid = all;
   kern<<<(unsigned)grid, kThreads, kTileBytes, st>>>(a);
   return cudaGetLastError();
 }
@@ -57,7 +58,7 @@ cudaError_t launch_dense_mode_impl(const DenseArgs& a_in, const DensePlan& p, cu
   if (p.kind == 0) {
     if constexpr (MODE <= MODE_SYM_MIRROR) {
       const u64 nx = a.nchunks * 16 > (1ull << a.n) ? (1ull << a.n) : a.nchunks * 16;
-      const u64 total = nx << a.n;
+      const u64 total = (nx << a.n) * (a.batch ? a.batch : 1);
       const unsigned blocks = (unsigned)((total + 255) / 256);
       dense_direct_kernel<MODE><<<blocks, 256, 0, st>>>(a, nx);
       *nlaunch += 1;

@@ -178,6 +178,20 @@ def generated(name, n):
     torch.cuda.empty_cache()
 
 
+def batched(name, n, batch):
+    """Batched small matrices: one launch for the whole batch (amortises launch latency)."""
+    A = torch.randn((batch, 1 << n, 1 << n), dtype=torch.complex128, device="cuda")
+    out = torch.empty((batch, 4 ** n), dtype=torch.complex128, device="cuda")
+    ms = time_it(lambda: ptdr.decompose_batched(A, "general", out=out))
+    coeffs = batch * 4 ** n
+    print(json.dumps({"config": name, "n": n, "batch": batch, "ms": ms, "coeffs_per_s": coeffs / (ms * 1e-3),
+                      "hbm_gbs": 32 * coeffs / (ms * 1e-3) / 1e9,
+                      "frac_of_measured": 32 * coeffs / (ms * 1e-3) / 1e9 / PEAK,
+                      "launches": ptdr.last_launch_count()}), flush=True)
+    del A, out
+    torch.cuda.empty_cache()
+
+
 def inverse(name, n):
     """Inverse transform: coefficients -> A, round trip checked."""
     A = ptdr.generate_dense(n, 4, "general", device="cuda")
@@ -212,6 +226,8 @@ if __name__ == "__main__":
         band_s("n24band_s2", 24, 2)
         band_s("n22band_s5", 22, 5)
         inverse("n15_inverse", 15)
+        batched("n6_batch16384", 6, 16384)
+        batched("n10_batch64", 10, 64)
         generated("n15_matrix_free", 15)
     if "all" in which or "big" in which:
         dense("n15", 15, 4, "general")

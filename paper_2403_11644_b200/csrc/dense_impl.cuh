@@ -39,8 +39,6 @@ struct DenseArgs {
   int L;
   int nslot;
   int discard;         // pipeline: discard consumed scratch lines from L2 (no write-back)
-  int interleave;      // pipeline: steady-state tickets alternate B(c) / A(c+L+1) tiles
-  int static_tickets;  // pipeline: ticket pairs assigned round-robin instead of by atomic
   int peer_shift;      // peer-pull mode (> 0): row i lives in shard i >> peer_shift
   u64 peer_rowmask;    //   at local row i & peer_rowmask
   int npeers;          //   shards (host side: tensor maps are built from peer_ptrs)

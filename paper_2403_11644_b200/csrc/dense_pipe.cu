@@ -86,10 +86,6 @@ cudaError_t launch_dense_pipe(int mode, const DenseArgs& a_in, const DensePlan& 
   {
     const char* nd = getenv("PTDR_NO_DISCARD");
     a.discard = (nd && nd[0] == '1') ? 0 : 1;
-    const char* il = getenv("PTDR_INTERLEAVE");
-    a.interleave = (il && il[0] == '1') ? 1 : 0;
-    const char* stc = getenv("PTDR_STATIC");
-    a.static_tickets = (stc && stc[0] == '1') ? 1 : 0;
   }
   cudaError_t e = cudaMemsetAsync(a.ctr, 0, p.ctr_bytes, st);
   if (e != cudaSuccess) return e;

@@ -188,7 +188,7 @@ __device__ __forceinline__ void emit_all(const DenseArgs& a, const EpiUnit<NB, (
 
 // Ticket order of dense_impl.cuh's decode_ticket, 32-bit, NA = NB = 2^M.
 __device__ __forceinline__ void decode_ticket32(uint32_t t, int M, uint32_t C, uint32_t L, int& phase,
-                                                uint32_t& chunk, uint32_t& tile, int interleave = 0) {
+                                                uint32_t& chunk, uint32_t& tile) {
   const uint32_t NA = 1u << M;
   const uint32_t lp1 = (L + 1u < C) ? L + 1u : C;
   const uint32_t pro = lp1 << M;
@@ -200,10 +200,7 @@ __device__ __forceinline__ void decode_ticket32(uint32_t t, int M, uint32_t C, u
   const uint32_t steady = C > L + 1u ? C - L - 1u : 0u;
   if (t < (steady << (M + 1))) {
     const uint32_t c = t >> (M + 1), o = t & (2u * NA - 1u);
-    if (interleave) {
-      if (o & 1u) { phase = 0; chunk = c + L + 1u; tile = o >> 1; }
-      else { phase = 1; chunk = c; tile = o >> 1; }
-    } else if (o < NA) { phase = 1; chunk = c; tile = o; }
+    if (o < NA) { phase = 1; chunk = c; tile = o; }
     else { phase = 0; chunk = c + L + 1u; tile = o - NA; }
     return;
   }
@@ -247,12 +244,6 @@ struct PipeCfg {
 // Fiber index of the phase-B tiles: phi encodes (u, zl) with bits [0,1]=u0,u1 [2,3]=zl0,zl1
 // [4, XB+2)=u2.. [XB+2, ..)=zl2.., so 2^k consecutive fibers form a (u, zl) square of
 // 4^(k/2) consecutive q (coalesced epilogue stores).
-// Phase-B tiles: consumers load the scratch straight into registers (L2 hits) instead of a
-// TMA bulk copy into the stage (saves 2 x 64 KiB of SMEM traffic per tile).
-#ifndef PTDR_B_DIRECT
-#define PTDR_B_DIRECT 0
-#endif
-constexpr bool kBDirect = PTDR_B_DIRECT != 0;
 
 template <int XB>
 __device__ __forceinline__ uint32_t phi_of(uint32_t u, uint32_t zl) {
@@ -389,7 +380,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
         depX = nullptr;
         dvX = 0;
         if (tk < total) {
-          decode_ticket32(tk, M, C, (uint32_t)a.L, phX, chX, tlX, a.interleave);
+          decode_ticket32(tk, M, C, (uint32_t)a.L, phX, chX, tlX);
           if (phX == 1) depX = &doneA[chX];
           else if (chX >= nslot) depX = &doneB[chX - nslot];
           if (depX) dvX = ld_relaxed(depX);
@@ -453,18 +444,11 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
             tma_load_2d(dst + rb * W * W, tm, (int)(col0 * 2u), (int)(row0 & rmask), &full[s], pol);
           }
         } else {
-          if constexpr (kBDirect) {
-            // phase-B consumers read the (L2-resident) scratch themselves; the stage is
-            // only their exchange buffer
-            mbar_arrive(&full[s]);
-          } else {
-            // scratch written by other CTAs' generic stores, read by the async proxy
-            fence_proxy_async_global();
-            mbar_arrive_expect_tx(&full[s], (uint32_t)Cfg::TB);
-            const double2* src =
-                a.scratch + (size_t)(chX % nslot) * a.slot_elems + ((size_t)tlX << LT);
-            bulk_load(dst, src, (uint32_t)Cfg::TB, &full[s], pol);
-          }
+          // scratch written by other CTAs' generic stores, read by the async proxy
+          fence_proxy_async_global();
+          mbar_arrive_expect_tx(&full[s], (uint32_t)Cfg::TB);
+          const double2* src = a.scratch + (size_t)(chX % nslot) * a.slot_elems + ((size_t)tlX << LT);
+          bulk_load(dst, src, (uint32_t)Cfg::TB, &full[s], pol);
         }
         trace_stamp(a.trace, k, 3);
         ++k;
@@ -478,20 +462,8 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
       int phP, phQ;
       const unsigned *depP, *depQ;
       unsigned dvP, dvQ;
-      // Ticket pairs: claimed from the shared counter (dynamic balance), or assigned
-      // statically round-robin (pair p -> CTA p mod gridDim; no hot-spot atomic: every
-      // ticket still waits only on smaller tickets, and each CTA takes its own in order,
-      // so the smallest unfinished ticket always progresses).
-      const bool stat = a.static_tickets != 0;
-      uint32_t pair = blockIdx.x;
-      auto claim = [&]() -> uint32_t {
-        if (stat) {
-          const uint32_t t2 = 2u * pair;
-          pair += gridDim.x;
-          return t2 < total ? t2 : total;
-        }
-        return atomicAdd(ticket, 2u);
-      };
+      // Ticket pairs from the shared counter (dynamic balance across CTAs).
+      auto claim = [&]() -> uint32_t { return atomicAdd(ticket, 2u); };
       const uint32_t b0 = claim();
       decode_into(b0, tkP, phP, chP, tlP, depP, dvP);
       decode_into(b0 + 1, tkQ, phQ, chQ, tlQ, depQ, dvQ);
@@ -733,13 +705,8 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
         if (gtid == 0) trace_stamp(a.trace, k, 7);
         continue;
       }
-      if constexpr (kBDirect) {
 #pragma unroll
-        for (int kk = 0; kk < 16; ++kk) v[kk] = __ldcg(yt + (jh * 16 + kk) * FB + f);
-      } else {
-#pragma unroll
-        for (int kk = 0; kk < 16; ++kk) v[kk] = S[(jh * 16 + kk) * FB + f];
-      }
+      for (int kk = 0; kk < 16; ++kk) v[kk] = S[(jh * 16 + kk) * FB + f];
       pwht<4>(v);
       if constexpr (M == 4) {
         named_bar_sync(bar_id, GT);

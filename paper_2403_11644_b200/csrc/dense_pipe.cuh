@@ -345,7 +345,9 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
   unsigned* ticket = a.ctr;
   unsigned* doneA = a.ctr + 1;
   unsigned* doneB = a.ctr + 1 + C;
-  const uint32_t nslot = (uint32_t)a.nslot;
+  const uint32_t nslot = (uint32_t)a.nslot;           // a power of two (dense_plan.h)
+  const uint32_t slot_mask = nslot - 1u;
+  const int slot_shift = __ffsll((long long)a.slot_elems) - 1;  // slot_elems = W << nv
   const unsigned done_target = 1u << M;  // one completion signal per tile
 
   if (threadIdx.x == 0) {
@@ -414,11 +416,9 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
         trace_stamp(a.trace, k, 2);
         if (PTDR_ENABLE_TRACE && a.trace && blockIdx.x == 0 && k < kTraceTiles) a.trace[k * 16 + 8] = phX;
         double2* dst = stage0 + (size_t)s * TE;
-        meta[s].valid = 1;
-        meta[s].phase = phX;
-        meta[s].tile = (int)tlX;
+        // one 16-byte and one 4-byte shared store instead of five
+        *reinterpret_cast<int4*>(&meta[s]) = make_int4(1, phX, (int)tlX, k);
         meta[s].chunk = chX;
-        meta[s].seq = k;
         if (phX == 0 && MODE == MODE_GEN) {
           mbar_arrive(&full[s]);  // matrix-free: the consumers generate the tile's entries
         } else if (phX == 0) {
@@ -447,7 +447,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
           // scratch written by other CTAs' generic stores, read by the async proxy
           fence_proxy_async_global();
           mbar_arrive_expect_tx(&full[s], (uint32_t)Cfg::TB);
-          const double2* src = a.scratch + (size_t)(chX % nslot) * a.slot_elems + ((size_t)tlX << LT);
+          const double2* src = a.scratch + ((size_t)(chX & slot_mask) << slot_shift) + ((size_t)tlX << LT);
           bulk_load(dst, src, (uint32_t)Cfg::TB, &full[s], pol);
         }
         trace_stamp(a.trace, k, 3);
@@ -555,7 +555,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
     }
     double2* S = stage0 + (size_t)s * TE;
     const uint32_t chunk = m.chunk;
-    double2* Y = a.scratch + (size_t)(chunk % nslot) * a.slot_elems;
+    double2* Y = a.scratch + ((size_t)(chunk & slot_mask) << slot_shift);
     double2 v[16];
     if (m.phase == 0 && NR > 0) {
       // ---- phase A, early release: read the stage once, release it, exchange through X

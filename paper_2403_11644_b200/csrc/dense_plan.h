@@ -132,6 +132,13 @@ inline DensePlan make_dense_plan(int nv, uint64_t x_count, int pipe_cfg = kPipeN
     ns = budget;
   }
   if (ns > nchunks) ns = nchunks;
+  if (pipe_cfg != kPipeNone) {
+    // a power of two, so the pipeline maps chunks to slots with a mask (its single producer
+    // thread is on the critical path: no integer division per tile)
+    uint64_t p2 = 1;
+    while (p2 < ns) p2 <<= 1;
+    ns = p2;
+  }
   p.nslot = (int)ns;
   p.ctr_bytes = ((4 * (1 + 2 * nchunks)) + 255) / 256 * 256;
   p.scratch_bytes = (size_t)p.nslot * p.slot_elems * 16;

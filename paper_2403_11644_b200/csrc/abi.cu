@@ -8,6 +8,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "../../include/ptdr.h"
@@ -33,6 +35,20 @@ int device_sm_count() {
     g_sm_count[dev] = v;
   }
   return g_sm_count[dev];
+}
+
+cudaError_t ensure_smem_attr(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::map<const void*, unsigned long long> done;  // bit d: device d configured
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(mu);
+  unsigned long long& bits = done[fn];
+  if (dev >= 0 && dev < 64 && (bits >> dev) & 1ull) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess && dev >= 0 && dev < 64) bits |= 1ull << dev;
+  return e;
 }
 
 static ptdr_status fail(ptdr_status s, const std::string& msg) {

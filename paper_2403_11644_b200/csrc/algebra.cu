@@ -208,12 +208,9 @@ __global__ void __launch_bounds__(kThreads, 2) inv_pass2_kernel(const double2* _
 
 template <int K>
 static cudaError_t launch_inv_pass2(const double2* U, double2* A, int n, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(inv_pass2_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kTileBytes);
+  {
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(inv_pass2_kernel<K>), kTileBytes);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   u64 tiles = (1ull << (2 * n)) / kTileElems;
   u64 g = (u64)device_sm_count() * 2;
@@ -230,13 +227,7 @@ cudaError_t launch_reconstruct(const double2* c, int n, double2* A, void* ws, cu
   const int sms = device_sm_count();
   cudaError_t e;
   if (n >= 9 && n <= 16) {
-    static bool attr1 = false;
-    if (!attr1) {
-      if ((e = cudaFuncSetAttribute(inv_pass1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kInvSmem)) !=
-          cudaSuccess)
-        return e;
-      attr1 = true;
-    }
+    if ((e = ensure_smem_attr(reinterpret_cast<const void*>(inv_pass1_kernel), kInvSmem)) != cudaSuccess) return e;
     u64 g = (N * N) >> 12;
     if (g > (u64)sms * 2) g = (u64)sms * 2;
     inv_pass1_kernel<<<(unsigned)g, 256, kInvSmem, st>>>(c, U, n);
@@ -255,13 +246,7 @@ cudaError_t launch_reconstruct(const double2* c, int n, double2* A, void* ws, cu
     }
   }
   if (n >= 6) {
-    static bool attr = false;
-    if (!attr) {
-      if ((e = cudaFuncSetAttribute(q2x_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536)) !=
-          cudaSuccess)
-        return e;
-      attr = true;
-    }
+    if ((e = ensure_smem_attr(reinterpret_cast<const void*>(q2x_kernel), 65536)) != cudaSuccess) return e;
     u64 g = (N * N) >> 12;
     if (g > (u64)sms * 3) g = (u64)sms * 3;
     q2x_kernel<<<(unsigned)g, 256, 65536, st>>>(c, U, n);

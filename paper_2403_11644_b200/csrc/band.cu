@@ -273,12 +273,9 @@ __global__ void __launch_bounds__(kThreads, 2) seg_pass_kernel(const __grid_cons
 
 // Runs all passes for all families (at most 3 launches for lam <= 24).
 cudaError_t run_families(const WhtFamily* fam, int nfam, cudaStream_t st, int* nl) {
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(seg_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kBandSmem);
+  {
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(seg_pass_kernel), kBandSmem);
     if (e != cudaSuccess) return e;
-    attr_done = true;
   }
   int maxlam = 0;
   for (int f = 0; f < nfam; ++f) maxlam = fam[f].lam > maxlam ? fam[f].lam : maxlam;

@@ -2,6 +2,7 @@
 // Each dense_mode<k>.cu instantiates it for one MODE so the ~50 kernel
 // instantiations compile in parallel translation units.
 #pragma once
+#include <atomic>
 #include <mutex>
 
 #include "dense_impl.cuh"
@@ -12,16 +13,25 @@ namespace ptdr {
 
 template <auto kernel>
 static cudaError_t prep_kernel(int* blocks_per_sm) {
-  // cached per kernel (function-local statics are per template instance)
-  static std::once_flag once;
-  static cudaError_t err = cudaSuccess;
-  static int bps = 0;
-  std::call_once(once, [&]() {
-    err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileBytes);
-    if (err == cudaSuccess)
-      err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kernel, kThreads, kTileBytes);
-    if (err == cudaSuccess && bps < 1) err = cudaErrorInvalidConfiguration;
-  });
+  // the shared-memory attribute once per (kernel, device); the occupancy (identical on every
+  // B200) queried after it
+  static std::atomic<int> cached[64];  // per device; 0 = not queried yet
+  int dev = 0;
+  cudaError_t err = cudaGetDevice(&dev);
+  if (err != cudaSuccess) return err;
+  if (dev >= 0 && dev < 64) {
+    const int c = cached[dev].load(std::memory_order_relaxed);
+    if (c > 0) {
+      *blocks_per_sm = c;
+      return cudaSuccess;
+    }
+  }
+  err = ensure_smem_attr(reinterpret_cast<const void*>(kernel), kTileBytes);
+  if (err != cudaSuccess) return err;
+  int bps = 0;
+  err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kernel, kThreads, kTileBytes);
+  if (err == cudaSuccess && bps < 1) err = cudaErrorInvalidConfiguration;
+  if (err == cudaSuccess && dev >= 0 && dev < 64) cached[dev].store(bps, std::memory_order_relaxed);
   *blocks_per_sm = bps;
   return err;
 }

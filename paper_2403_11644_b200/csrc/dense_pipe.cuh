@@ -759,11 +759,7 @@ template <int LT, int XB, int GW, int NG, int NS, int NR, int M, int MODE>
 static cudaError_t launch_pipe_impl(const TmapSet& map, const DenseArgs& a, cudaStream_t st) {
   using Cfg = PipeCfg<LT, XB, GW, NG, NS, NR>;
   constexpr auto kern = dense_pipe_kernel<LT, XB, GW, NG, NS, NR, M, MODE>;
-  static std::once_flag once;
-  static cudaError_t err = cudaSuccess;
-  std::call_once(once, [&]() {
-    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
-  });
+  const cudaError_t err = ensure_smem_attr(reinterpret_cast<const void*>(kern), Cfg::SMEM);
   if (err != cudaSuccess) return err;
   kern<<<device_sm_count(), Cfg::THREADS, Cfg::SMEM, st>>>(map, a);
   return cudaGetLastError();

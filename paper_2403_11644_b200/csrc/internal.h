@@ -12,6 +12,10 @@ struct DensePlan;
 
 int device_sm_count();  // SMs of the current device (cached per device)
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) for `fn` on the current device, once per
+// (function, device), thread-safe (a function attribute is per device context).
+cudaError_t ensure_smem_attr(const void* fn, int bytes);
+
 cudaError_t launch_dense_mode0(const DenseArgs& a, const DensePlan& p, cudaStream_t st, int* nl);
 cudaError_t launch_dense_mode1(const DenseArgs& a, const DensePlan& p, cudaStream_t st, int* nl);
 cudaError_t launch_dense_mode2(const DenseArgs& a, const DensePlan& p, cudaStream_t st, int* nl);

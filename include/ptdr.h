@@ -118,7 +118,8 @@ ptdr_status ptdr_decompose_host(const ptdr_c128* A_host, int n, int structure,
 /* Batched small matrices (serving many decompositions per launch): A = [batch][2^n][2^n]
  * dense matrices of one structure stored back to back, out = [batch][4^n] coefficient
  * arrays in q order; 1 <= n <= 10 (the whole-vector and direct kernels: no workspace, one
- * launch -- two for HERMITIAN / REAL_SYMMETRIC at n >= 9 -- for the whole batch).  Each
+ * launch -- two for HERMITIAN / REAL_SYMMETRIC at n >= 9 -- for the whole batch; batch = 0
+ * is a no-op and accepts null pointers).  Each
  * matrix's result is bitwise identical to ptdr_decompose_async on it alone. */
 ptdr_status ptdr_decompose_batched_async(const ptdr_c128* A, int n, int structure, uint64_t batch,
                                          ptdr_c128* out, void* stream);

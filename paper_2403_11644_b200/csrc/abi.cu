@@ -682,9 +682,9 @@ ptdr_status ptdr_decompose_batched_async(const ptdr_c128* A, int n, int structur
   g_last_launches = 0;
   if (!is_dense(structure)) return fail(PTDR_EINVAL, "batched decomposition is for the dense structures");
   if (n < 1 || n > kSingleMax) return fail(PTDR_EINVAL, "batched decomposition needs 1 <= n <= 10");
+  if (batch == 0) return PTDR_OK;  // empty batch: nothing to read or write (pointers may be null)
   if (!A || !out) return fail(PTDR_EINVAL, "null pointer");
   if (((uintptr_t)A & 15) || ((uintptr_t)out & 15)) return fail(PTDR_EINVAL, "misaligned pointer");
-  if (batch == 0) return PTDR_OK;
   const size_t bytes = ((size_t)16 << (2 * n)) * batch;
   if (overlaps(A, bytes, out, bytes)) return fail(PTDR_EUNSUPPORTED, "out overlaps A");
   {

@@ -38,3 +38,11 @@ def test_batched_rejects_large_n(gpu):
     with pytest.raises(ptdr.PtdrError) as e:
         ptdr.decompose_batched(A)
     assert e.value.status == ptdr.PTDR_EINVAL
+
+
+def test_batched_empty_batch_is_a_noop(gpu):
+    torch = _torch()
+    A = torch.zeros((0, 64, 64), dtype=torch.complex128, device="cuda")
+    out = ptdr.decompose_batched(A)
+    assert out.shape == (0, 4 ** 6)
+    assert ptdr.last_launch_count() == 0

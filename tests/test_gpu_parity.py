@@ -209,3 +209,15 @@ def test_error_paths(gpu):
     assert e.value.status == ptdr.PTDR_ENOMEM
     with pytest.raises(TypeError):
         ptdr.decompose(A.cpu())                          # no CPU fallback
+
+
+@pytest.mark.parametrize("n", [1, 6, 11, 13])
+@pytest.mark.parametrize("variant", ["general", "hermitian", "real_symmetric"])
+def test_zero_matrix_gives_exact_zeros(gpu, n, variant):
+    """Degenerate input: A = 0 decomposes to exactly 0 on every path (no stale scratch,
+    no uninitialised output)."""
+    torch = _torch()
+    A = torch.zeros((1 << n, 1 << n), dtype=torch.complex128, device="cuda")
+    out = torch.full((4 ** n,), complex(float("nan"), float("nan")), dtype=torch.complex128, device="cuda")
+    ptdr.decompose(A, variant, out=out)
+    assert torch.count_nonzero(torch.view_as_real(out)).item() == 0

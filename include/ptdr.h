@@ -115,6 +115,14 @@ ptdr_status ptdr_decompose_async(const ptdr_c128* A, int n, int structure, ptdr_
 ptdr_status ptdr_decompose_host(const ptdr_c128* A_host, int n, int structure,
                                 ptdr_c128* out_host);
 
+/* Selected coefficients of a dense GENERAL-storage matrix: out[k] = coefficient of the string
+ * with index qs[k] (q order, < 4^n), evaluated directly by Algorithm 2 (compute_coeff,
+ * l.302-313) in O(2^n) per string -- no workspace, no full transform.  A: device
+ * [2^n][2^n]; qs: device uint64 [count]; out: device [count].  Indices out of range
+ * of q are undefined (not checked on the device). */
+ptdr_status ptdr_coefficients_async(const ptdr_c128* A, int n, const uint64_t* qs, uint64_t count,
+                                    ptdr_c128* out, void* stream);
+
 /* Batched small matrices (serving many decompositions per launch): A = [batch][2^n][2^n]
  * dense matrices of one structure stored back to back, out = [batch][4^n] coefficient
  * arrays in q order; 1 <= n <= 10 (the whole-vector and direct kernels: no workspace, one

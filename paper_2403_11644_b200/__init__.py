@@ -90,6 +90,8 @@ def lib():
         L.ptdr_generated_workspace_bytes.restype = sz
         L.ptdr_decompose_generated_async.argtypes = [i32, u64, i32, i32, vp, vp, sz, vp]
         L.ptdr_decompose_generated_async.restype = i32
+        L.ptdr_coefficients_async.argtypes = [vp, i32, vp, u64, vp, vp]
+        L.ptdr_coefficients_async.restype = i32
         L.ptdr_decompose_batched_async.argtypes = [vp, i32, i32, u64, vp, vp]
         L.ptdr_decompose_batched_async.restype = i32
         L.ptdr_generate_dense_async.argtypes = [i32, u64, i32, u64, u64, vp, vp]
@@ -300,6 +302,22 @@ def decompose_xshard(A_local, n: int, rank: int, world: int, out=None, workspace
                                            ctypes.c_void_p(workspace.data_ptr()),
                                            workspace.numel(), _stream_ptr(stream))
     _check(st, "ptdr_decompose_xshard_async")
+    return out
+
+
+def coefficients(A, qs, out=None, stream=None):
+    """Coefficients of the strings qs (q order) of a dense matrix by Algorithm 2 directly
+    (ptdr_coefficients_async); qs: CUDA int64/uint64 tensor or anything torch.as_tensor takes."""
+    import torch
+
+    _require_cuda_c128(A, "A")
+    n = n_of(A, 0)
+    q = torch.as_tensor(qs, dtype=torch.int64, device=A.device).contiguous()
+    if out is None:
+        out = torch.empty(q.numel(), dtype=torch.complex128, device=A.device)
+    _check(lib().ptdr_coefficients_async(ctypes.c_void_p(A.data_ptr()), n, ctypes.c_void_p(q.data_ptr()), q.numel(),
+                                         ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)),
+           "ptdr_coefficients_async")
     return out
 
 

@@ -676,6 +676,20 @@ ptdr_status ptdr_decompose_padded_async(const ptdr_c128* A, uint64_t m, uint64_t
   return r;
 }
 
+// ---- selected coefficients (Algorithm 2 per string) ------------------------------------
+ptdr_status ptdr_coefficients_async(const ptdr_c128* A, int n, const uint64_t* qs, uint64_t count,
+                                    ptdr_c128* out, void* stream) {
+  g_last_launches = 0;
+  if (n < 1 || n > 16) return fail(PTDR_EINVAL, "invalid n (1..16)");
+  if (count == 0) return PTDR_OK;
+  if (!A || !qs || !out) return fail(PTDR_EINVAL, "null pointer");
+  if (((uintptr_t)A & 15) || ((uintptr_t)out & 15) || ((uintptr_t)qs & 7)) return fail(PTDR_EINVAL, "misaligned");
+  cudaError_t e = launch_coeffs(reinterpret_cast<const double2*>(A), n, qs, count, reinterpret_cast<double2*>(out),
+                                reinterpret_cast<cudaStream_t>(stream));
+  g_last_launches = 1;
+  return e == cudaSuccess ? PTDR_OK : cuda_fail(e, "coefficients launch");
+}
+
 // ---- batched small matrices -----------------------------------------------------------
 ptdr_status ptdr_decompose_batched_async(const ptdr_c128* A, int n, int structure, uint64_t batch,
                                          ptdr_c128* out, void* stream) {

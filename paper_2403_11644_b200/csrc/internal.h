@@ -47,6 +47,10 @@ cudaError_t launch_axpby(double2* out, double2 mu, const double2* x, double2 nu,
 cudaError_t launch_block_diag(const double2* blocks, int n, int k, double2* out, cudaStream_t st);
 cudaError_t launch_herm_augment(const double2* a, int n, double2* out, cudaStream_t st);
 
+// selected coefficients (coeffs.cu)
+cudaError_t launch_coeffs(const double2* A, int n, const uint64_t* qs, uint64_t count, double2* out,
+                          cudaStream_t st);
+
 // generators (generate.cu)
 cudaError_t launch_generate_dense(int n, uint64_t seed, int variant, uint64_t row0,
                                   uint64_t nrows, double2* A, cudaStream_t st);

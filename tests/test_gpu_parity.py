@@ -221,3 +221,30 @@ def test_zero_matrix_gives_exact_zeros(gpu, n, variant):
     out = torch.full((4 ** n,), complex(float("nan"), float("nan")), dtype=torch.complex128, device="cuda")
     ptdr.decompose(A, variant, out=out)
     assert torch.count_nonzero(torch.view_as_real(out)).item() == 0
+
+
+@pytest.mark.parametrize("n", [1, 3, 8, 12])
+def test_selected_coefficients_vs_oracle(gpu, n):
+    """ptdr_coefficients_async (Algorithm 2 per string on the GPU) vs the oracle."""
+    torch = _torch()
+    A = _dense(n, 300 + n, "general")
+    rng = np.random.default_rng(300 + n)
+    qs = np.unique(np.concatenate([rng.integers(0, 4 ** n, 300), _edge_qs(n)])).astype(np.int64)
+    got = ptdr.coefficients(torch.from_numpy(A).cuda(), torch.from_numpy(qs).cuda()).cpu().numpy()
+    want = oracle.coeffs_dense(A, qs.astype(np.uint64))
+    _assert_close(got, want, np.max(np.abs(A)), f"coefficients n={n}")
+
+
+def test_selected_coefficients_n15_match_transform(gpu):
+    """At the bench size: the direct per-string evaluation agrees with the full transform."""
+    torch = _torch()
+    n = 15
+    A = ptdr.generate_dense(n, 4, "general")
+    full = ptdr.decompose(A)
+    rng = np.random.default_rng(15)
+    qs = torch.from_numpy(rng.integers(0, 4 ** n, 512).astype(np.int64)).cuda()
+    got = ptdr.coefficients(A, qs)
+    err = torch.max(torch.abs(got - full[qs])).item()
+    assert err <= TOL * 6.0, err
+    del A, full
+    torch.cuda.empty_cache()

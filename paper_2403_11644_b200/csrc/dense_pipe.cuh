@@ -529,9 +529,14 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
   const int gtid = threadIdx.x - 128 - g * GT;
   const int wig = gtid >> 5;  // warp index within the group
   // per-warp completion signal of the group's j-th tile (see the signaler)
+  auto fresh_lane = []() {
+    int l;
+    asm volatile("mov.u32 %0, %%laneid;" : "=r"(l));
+    return l;
+  };
   auto signal = [&](int j, unsigned* counter) {
     __syncwarp();
-    if (lane == 0) {
+    if (fresh_lane() == 0) {
       const int d = j % SIGD;
       if (j >= SIGD) mbar_wait(&sigfree[g * SIGD + d], (uint32_t)((j / SIGD) - 1) & 1u);
       if (wig == 0) sigptr[g * SIGD + d] = counter;
@@ -539,9 +544,19 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
     }
   };
   const int bar_id = 1 + g;
+  // The thread's index inside the group, re-read from %tid.x in every tile: index values
+  // derived from a loop-invariant gtid were kept live across the whole loop and spilled, and
+  // their per-tile local reloads queued behind the group's global stores in the LSU.
+  auto fresh_gtid = [&]() {
+    int t;
+    asm volatile("mov.u32 %0, %%tid.x;" : "=r"(t));
+    return t - 128 - g * GT;
+  };
   int j = 0;
   for (int k = g;; k += NG, ++j) {
     const int s = k % NS;
+    const int gtid = fresh_gtid();
+    const int lane = fresh_lane();
     // stages are shared round-robin by the groups, so a parity wait alone could match an
     // older phase: first wait until the producer has published tile k in this stage
     if (gtid == 0) trace_stamp(a.trace, k, 4);

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "engine.cuh"
+#include "sm100_ptx.cuh"
 #include "internal.h"
 #include "wht_passes.h"
 
@@ -592,52 +593,150 @@ __global__ void band_gather_diag_kernel(const double2* diags, int n, int s, cons
   }
 }
 
+// One segment's contribution to a lane's 8 outputs z = z0 + 32 j (z0 = base + lane, base a
+// multiple of 256, so bits 5-7 of z0 are zero).  Wg = W + (base >> SH): the sample of output z
+// is Wg[(lane + 32 j) >> SH], which for SH >= 5 does not depend on the lane, so only 256 >> SH
+// distinct values (one for SH >= 8) are loaded instead of one per output.  The signs
+// (-1)^{popcount(lm & z)} = (-1)^{popcount(lm & z0)} (-1)^{popcount(((lm >> 5) & 7) & j)} come
+// from one byte-table lookup per segment (bit j of T), and are applied as fma(+-1, w, acc):
+// exactly acc +- w.
+#ifndef PTDR_BAND_PF
+#define PTDR_BAND_PF 1
+#endif
+constexpr int kBandPrefetchDist = PTDR_BAND_PF;  // groups ahead (grid strides) for the L1 prefetch
+
+template <int SH>
+__device__ __forceinline__ void band_accum(const double2* __restrict__ Wg, unsigned z0, unsigned lane, unsigned lm,
+                                           double (&re)[8], double (&im)[8]) {
+  constexpr int D = SH >= 8 ? 1 : (SH >= 5 ? (256 >> SH) : 8);  // loads per lane
+  double2 w[D];
+#pragma unroll
+  for (int m = 0; m < D; ++m) {
+    const unsigned idx = SH >= 5 ? (unsigned)m : ((lane + 32u * m) >> SH);
+#if defined(PTDR_DIAG) && (PTDR_DIAG & 8)
+    w[m] = make_double2((double)(size_t)Wg, (double)idx);  // diagnostics: no W loads
+#else
+    w[m] = __ldg(Wg + idx);
+#endif
+  }
+  // byte m of {0x963C5AF0 : 0x66CCAA00} has bit j = parity(m & j)
+  const unsigned T = __byte_perm(0x66CCAA00u, 0x963C5AF0u, (lm >> 5) & 7u) ^ (0u - (__popc(lm & z0) & 1u));
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const double2 v = w[SH >= 8 ? 0 : (SH >= 5 ? (j >> (SH - 5)) : j)];
+    const double sg = __hiloint2double((int)(((T << (31 - j)) & 0x80000000u) | 0x3ff00000u), 0);
+    re[j] = fma(sg, v.x, re[j]);
+    im[j] = fma(sg, v.y, im[j]);
+  }
+}
+
 // Expansion: out[b][z] = 2^-n i^{popcount(x_b & z)} sum_k (-1)^{popcount(l_k & z_lo)} W_k[z_hi].
-// One CTA row per block b (blockIdx.y): its segment references are staged in SMEM once;
-// every warp then produces 256 consecutive outputs, 8 per lane (z = base + lane + 32 j), so
-// 8 independent accumulations keep their loads in flight (W values are shared by runs of
-// 2^{t+1} consecutive z: L1 broadcast) and each store instruction writes 512 B.
-// Warps walk the output in address order (group g = 256 consecutive outputs of block
-// g >> (n-8)), like the tridiagonal expansion: the chip's write front stays within a few
-// tens of MiB, which keeps HBM row-buffer locality (a grid with one CTA row per block
-// spreads the front over all blocks and ran 2.5x slower).
-__global__ void __launch_bounds__(256, 4) band_expand_kernel(const BandBlockDev* blocks, const BandSegRef* refs,
+// Every warp produces 256 consecutive outputs of one block, 8 per lane (z = base + lane + 32 j),
+// so each store instruction writes 512 B.  Warps walk the output in address order (group g =
+// 256 consecutive outputs of block g >> (n-8)), like the tridiagonal expansion: the chip's
+// write front stays within a few tens of MiB, which keeps HBM row-buffer locality (a grid with
+// one CTA row per block spreads the front over all blocks and ran 2.5x slower).  The kernel is
+// issue-bound rather than load-bound (a version without any W loads wrote at 6.4 TB/s, and an
+// L2 prefetch of the next group's W ranges changed nothing), so the per-output work is
+// integer-light: shift-specialised loads, table-driven signs, and an i^p phase applied with
+// sign-bit arithmetic on the scale.
+__global__ void __launch_bounds__(256, 2) band_expand_kernel(const BandBlockDev* blocks, const BandSegRef* refs,
                                                              const double2* segs, int nblocks, int n,
                                                              double scale, double2* out) {
   const u64 N = 1ull << n;
   const unsigned lane = threadIdx.x & 31;
   const int gshift = n - 8;  // groups per block = 2^(n-8); z < 2^28 fits 32 bits
   const u64 groups = (u64)nblocks << gshift;
+  const int scale_hi = __double2hiint(scale), scale_lo = __double2loint(scale);
   for (u64 gi = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; gi < groups;
        gi += ((u64)gridDim.x * blockDim.x) >> 5) {
     const int b = (int)(gi >> gshift);
-    const BandBlockDev B = blocks[b];
-    const int sh = B.t + 1;
+    const unsigned xb = (unsigned)__ldg(&blocks[b].x);
+    const int bt = __ldg(&blocks[b].t), nL = __ldg(&blocks[b].nL), first = __ldg(&blocks[b].first);
+    const int sh = bt + 1;
     const unsigned lomask = (1u << sh) - 1u;
     const unsigned z0 = ((unsigned)(gi & ((1ull << gshift) - 1ull)) << 8) + lane;
+    {
+      // L1 prefetch of the W samples of a later group of this warp: its loads then hit L1 instead
+      // of waiting an L2 / DRAM round trip (lane kk: segment kk's sample, or lines of it)
+      const u64 gn = gi + kBandPrefetchDist * (((u64)gridDim.x * blockDim.x) >> 5);
+      if (gn < groups) {
+        const int bn = (int)(gn >> gshift);
+        const int shn = __ldg(&blocks[bn].t) + 1, nLn = __ldg(&blocks[bn].nL), fn = __ldg(&blocks[bn].first);
+        const unsigned zb = (unsigned)(gn & ((1ull << gshift) - 1ull)) << 8;
+        if (shn >= 8) {
+          if ((int)lane < nLn) prefetch_l1(segs + __ldg(&refs[fn + (int)lane].off) + (zb >> shn));
+        } else {
+          const unsigned cnt = 256u >> shn;  // samples per segment, 8 per 128 B line
+          for (int kk = 0; kk < nLn; ++kk)
+            if (lane * 8u < cnt) prefetch_l1(segs + __ldg(&refs[fn + kk].off) + (zb >> shn) + lane * 8u);
+        }
+      }
+    }
     double re[8], im[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) { re[j] = 0.0; im[j] = 0.0; }
-    for (int k = 0; k < B.nL; ++k) {
-      const BandSegRef r = refs[B.first + k];
-      const double2* W = segs + r.off;
-      const unsigned lm = (unsigned)r.l & lomask;
+    int k = 0;
+    if (sh >= 8) {
+      // one sample per segment: issue all of them (up to 8) before using any, so a group
+      // waits one memory latency instead of one per segment
+      constexpr int KB = 8;
+      double2 wk[KB];
+      unsigned lmk[KB];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const unsigned z = z0 + 32u * j;
-        const double2 w = __ldg(W + (z >> sh));
-        const double sg = (__popc(lm & z) & 1) ? -1.0 : 1.0;
-        re[j] = fma(sg, w.x, re[j]);
-        im[j] = fma(sg, w.y, im[j]);
+      for (int kk = 0; kk < KB; ++kk) {
+        if (kk < nL) {
+          const unsigned long long rl = __ldg(&refs[first + kk].l), roff = __ldg(&refs[first + kk].off);
+          lmk[kk] = (unsigned)rl & lomask;
+#if defined(PTDR_DIAG) && (PTDR_DIAG & 8)
+          wk[kk] = make_double2((double)roff, 1.0);
+#else
+          wk[kk] = __ldg(segs + roff + ((z0 - lane) >> sh));
+#endif
+        }
+      }
+#pragma unroll
+      for (int kk = 0; kk < KB; ++kk) {
+        if (kk < nL) {
+          const unsigned lm = lmk[kk];
+          const unsigned T = __byte_perm(0x66CCAA00u, 0x963C5AF0u, (lm >> 5) & 7u) ^ (0u - (__popc(lm & z0) & 1u));
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const double sg = __hiloint2double((int)(((T << (31 - j)) & 0x80000000u) | 0x3ff00000u), 0);
+            re[j] = fma(sg, wk[kk].x, re[j]);
+            im[j] = fma(sg, wk[kk].y, im[j]);
+          }
+        }
+      }
+      k = KB;
+    }
+    for (; k < nL; ++k) {
+      const unsigned long long rl = __ldg(&refs[first + k].l), roff = __ldg(&refs[first + k].off);
+      const double2* Wg = segs + roff + ((z0 - lane) >> sh);
+      const unsigned lm = (unsigned)rl & lomask;
+      switch (sh < 8 ? sh : 8) {
+        case 0: band_accum<0>(Wg, z0, lane, lm, re, im); break;
+        case 1: band_accum<1>(Wg, z0, lane, lm, re, im); break;
+        case 2: band_accum<2>(Wg, z0, lane, lm, re, im); break;
+        case 3: band_accum<3>(Wg, z0, lane, lm, re, im); break;
+        case 4: band_accum<4>(Wg, z0, lane, lm, re, im); break;
+        case 5: band_accum<5>(Wg, z0, lane, lm, re, im); break;
+        case 6: band_accum<6>(Wg, z0, lane, lm, re, im); break;
+        case 7: band_accum<7>(Wg, z0, lane, lm, re, im); break;
+        default: band_accum<8>(Wg, z0, lane, lm, re, im); break;
       }
     }
     double2* ob = out + (u64)b * N;
-    const unsigned xb = (unsigned)B.x;
+    const unsigned p0 = (unsigned)__popc(xb & z0), mx = (xb >> 5) & 7u;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const unsigned z = z0 + 32u * j;
-      const double2 c = rot_ipow(make_double2(re[j], im[j]), __popc(xb & z));
-      st_stream(ob + z, make_double2(c.x * scale, c.y * scale));
+      // i^p (re + i im): p odd swaps the parts; Re is negated for p in {1, 2}, Im for p in {2, 3}
+      const unsigned p = (p0 + (unsigned)__popc(mx & (unsigned)j)) & 3u;
+      const bool odd = (p & 1u) != 0;
+      const double a = odd ? im[j] : re[j], c = odd ? re[j] : im[j];
+      const double sa = __hiloint2double(scale_hi ^ (int)(((p ^ (p >> 1)) & 1u) << 31), scale_lo);
+      const double sc = __hiloint2double(scale_hi ^ (int)((p & 2u) << 30), scale_lo);
+      st_stream(ob + z0 + 32u * j, make_double2(a * sa, c * sc));
     }
   }
 }

@@ -14,6 +14,7 @@
 #include <cstdint>
 
 #include "engine.cuh"
+#include "sm100_ptx.cuh"
 #include "internal.h"
 #include "wht_passes.h"
 
@@ -109,60 +110,94 @@ __global__ void xscatter_small_kernel(const double2* __restrict__ V, double2* __
 __device__ __forceinline__ int inv_slot(int f, int j) { return f * 273 + (j >> 4) * 17 + (j & 15); }
 constexpr int kInvSmem = 16 * 273 * 16;
 
-__global__ void __launch_bounds__(256, 2) inv_pass1_kernel(const double2* __restrict__ c, double2* __restrict__ U,
+// Tiles stream through a ring of kInvStages SMEM buffers filled by the bulk-copy (TMA) engine:
+// a tile's 16 runs are 16 contiguous 4 KiB copies completing on the buffer's mbarrier, issued
+// two tiles ahead, so the loads of the next tiles are in flight while the current tile is
+// transformed and stored (one CTA per SM).  The first WHT stage reads the raw q-order copy
+// (its element for (x bits 0-3 = f, z bits 0-7 = jl + 16 kk) sits at kk * 256 + qlo(f, jl)),
+// applies the conjugate phase, and after a barrier writes the padded transpose layout into
+// the same buffer.  (Register loads with two CTAs per SM: 8.9 ms at n = 15; 16 B cp.async
+// into a double buffer: 12.7 ms.)
+constexpr int kInvStages = 3;
+
+__global__ void __launch_bounds__(256, 1) inv_pass1_kernel(const double2* __restrict__ c, double2* __restrict__ U,
                                                            int n) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* T = reinterpret_cast<double2*>(smem_raw);
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  double2* Tb = reinterpret_cast<double2*>(smem_raw);
+  constexpr int TE = kInvSmem / 16;  // elements per buffer (padded layout; the raw copy uses 4096)
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + kInvStages * kInvSmem);
   const u64 N = 1ull << n;
   const u64 xtiles = N >> 4;
   const u64 tiles = xtiles * (N >> 8);
   const int tid = threadIdx.x;
-  // this thread's (x bits 0-3, z bits 0-3) = the decode of q bits 0-7 = tid
-  const u64 zl4 = compact_even((u64)tid >> 1) & 15ull;
-  const u64 xl4 = (compact_even((u64)tid) & 15ull) ^ zl4;
-  for (u64 tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+  if (tid == 0) {
+    for (int b = 0; b < kInvStages; ++b) mbar_init(&full[b], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint64_t pol = policy_evict_first();
+  // warp 0 issues tile t into buffer t % kInvStages (lane 0 arms the barrier, lanes 0-15 copy)
+  auto issue = [&](u64 t, int it) {
+    if (t >= tiles) return;
+    const int b = it % kInvStages;
+    const u64 xt = (t % xtiles) << 4, zt = (t / xtiles) << 8;
+    if (tid == 0) {
+      fence_proxy_async_smem();  // the buffer was last written by generic stores
+      mbar_arrive_expect_tx(&full[b], 4096u * 16u);
+    }
+    __syncwarp();
+    if (tid < 16) {
+      const u64 zr = zt | ((u64)tid << 4);
+      bulk_load(Tb + (size_t)b * TE + tid * 256, c + (spread_bits(xt ^ zr) | (spread_bits(zr) << 1)), 4096u, &full[b],
+                pol);
+    }
+  };
+  int it = 0;
+  if (tid < 32) {
+    issue(blockIdx.x, 0);
+    issue(blockIdx.x + gridDim.x, 1);
+  }
+  const int f = tid >> 4, jl = tid & 15;
+  const int qlo = (int)(spread_bits((u64)(f ^ jl)) | (spread_bits((u64)jl) << 1));
+  for (u64 tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+    const int b = it % kInvStages;
+    if (tid < 32) issue(tile + 2 * (u64)gridDim.x, it + 2);  // into the buffer freed last iteration
+    mbar_wait(&full[b], (uint32_t)(it / kInvStages) & 1u);
+    double2* T = Tb + (size_t)b * TE;
     const u64 xt = (tile % xtiles) << 4, zt = (tile / xtiles) << 8;
-    const u64 x = xt | xl4;
     double2 v[16];
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {  // all 16 loads in flight before any use
-      const u64 z = zt | ((u64)r << 4) | zl4;
-      v[r] = ld_stream(c + (spread_bits(x ^ z) | (spread_bits(z) << 1)));
-    }
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      const u64 z = zt | ((u64)r << 4) | zl4;
-      T[inv_slot((int)xl4, (r << 4) | (int)zl4)] = rot_ipow(v[r], 4 - (__popcll(x & z) & 3));
-    }
-    __syncthreads();
     {
-      const int f = tid >> 4, jl = tid & 15;
+      const u64 x = xt | (u64)f;
 #pragma unroll
-      for (int kk = 0; kk < 16; ++kk) v[kk] = T[inv_slot(f, jl + 16 * kk)];
+      for (int kk = 0; kk < 16; ++kk) {
+        const u64 z = zt | ((u64)kk << 4) | (u64)jl;
+        v[kk] = rot_ipow(T[kk * 256 + qlo], 4 - (__popcll(x & z) & 3));
+      }
       wht_regs<4>(v);
+      __syncthreads();  // every raw element is read before the padded layout overwrites it
 #pragma unroll
       for (int kk = 0; kk < 16; ++kk) T[inv_slot(f, jl + 16 * kk)] = v[kk];
     }
     __syncthreads();
     {
-      const int f = tid >> 4, kh = tid & 15;
+      const int kh = tid & 15;
 #pragma unroll
-      for (int jl = 0; jl < 16; ++jl) v[jl] = T[inv_slot(f, jl + 16 * kh)];
+      for (int j = 0; j < 16; ++j) v[j] = T[inv_slot(f, j + 16 * kh)];
       wht_regs<4>(v);
 #pragma unroll
-      for (int jl = 0; jl < 16; ++jl) T[inv_slot(f, jl + 16 * kh)] = v[jl];
+      for (int j = 0; j < 16; ++j) T[inv_slot(f, j + 16 * kh)] = v[j];
     }
     __syncthreads();
     {
-      const int f = tid & 15, jg = tid >> 4;
-      const u64 xo = xt + (u64)f;
+      const int fo = tid & 15, jg = tid >> 4;
+      const u64 xo = xt + (u64)fo;
 #pragma unroll 4
       for (int kk = 0; kk < 16; ++kk) {
         const int j = jg + 16 * kk;
-        st_stream(U + ((((xo >> 5) << n) + zt + (u64)j) << 5) + (xo & 31ull), T[inv_slot(f, j)]);
+        st_stream(U + ((((xo >> 5) << n) + zt + (u64)j) << 5) + (xo & 31ull), T[inv_slot(fo, j)]);
       }
     }
-    __syncthreads();
+    __syncthreads();  // buffer b is refilled by a later issue
   }
 }
 
@@ -227,10 +262,11 @@ cudaError_t launch_reconstruct(const double2* c, int n, double2* A, void* ws, cu
   const int sms = device_sm_count();
   cudaError_t e;
   if (n >= 9 && n <= 16) {
-    if ((e = ensure_smem_attr(reinterpret_cast<const void*>(inv_pass1_kernel), kInvSmem)) != cudaSuccess) return e;
+    constexpr int smem = kInvStages * kInvSmem + 64;
+    if ((e = ensure_smem_attr(reinterpret_cast<const void*>(inv_pass1_kernel), smem)) != cudaSuccess) return e;
     u64 g = (N * N) >> 12;
-    if (g > (u64)sms * 2) g = (u64)sms * 2;
-    inv_pass1_kernel<<<(unsigned)g, 256, kInvSmem, st>>>(c, U, n);
+    if (g > (u64)sms) g = (u64)sms;
+    inv_pass1_kernel<<<(unsigned)g, 256, smem, st>>>(c, U, n);
     *nl += 1;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     *nl += 1;

@@ -119,3 +119,24 @@ def test_band_n20_sampled(gpu):
     want = oracle.coeffs_band(diags, s, qs)
     got = out[torch.from_numpy(b * (1 << n) + z).cuda()].cpu().numpy()
     assert np.max(np.abs(got - want)) <= TOL * np.max(np.abs(diags))
+
+
+@pytest.mark.parametrize("n,s,full", [(9, 17, True), (10, 33, False), (12, 64, False)])
+def test_band_wide(gpu, n, s, full):
+    """Wide bands: blocks with more than 8 segments (|L_x| = #m * 2^popcount(e), e = 2^{t+1}-1-x
+    up to s-1) take the expansion's per-segment fallback after its batched first 8."""
+    torch = _torch()
+    rng = np.random.default_rng(3000 + n + s)
+    diags = _cplx(rng, (2 * s + 1, 1 << n))
+    out = ptdr.decompose_band(torch.from_numpy(diags).cuda(), s).cpu().numpy().reshape(-1, 1 << n)
+    xs = ptdr.band_xmasks(n, s)
+    if full:
+        bs = np.repeat(np.arange(len(xs)), 1 << n)
+        zs = np.tile(np.arange(1 << n), len(xs))
+    else:
+        bs = rng.integers(0, len(xs), 3000)
+        zs = rng.integers(0, 1 << n, 3000)
+    qs = np.array([q_of(int(xs[b]), int(z), n) for b, z in zip(bs, zs)], dtype=np.uint64)
+    want = oracle.coeffs_band(diags, s, qs)
+    err = np.max(np.abs(out[bs, zs] - want))
+    assert err <= TOL * np.max(np.abs(diags)), err

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <map>
 #include <mutex>
 #include <string>
@@ -23,31 +24,32 @@ namespace ptdr {
 static thread_local std::string g_last_error;
 static thread_local int g_last_launches = 0;
 
-static int g_sm_count[64] = {0};
+static std::atomic<int> g_sm_count[64] = {};
 
 int device_sm_count() {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
-  if (g_sm_count[dev] == 0) {
-    int v = 0;
-    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
-      v = 148;
-    g_sm_count[dev] = v;
+  int v = g_sm_count[dev].load(std::memory_order_relaxed);
+  if (v == 0) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    g_sm_count[dev].store(v, std::memory_order_relaxed);
   }
-  return g_sm_count[dev];
+  return v;
 }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device), raised again if
+// a later launch of the same kernel asks for more.
 cudaError_t ensure_smem_attr(const void* fn, int bytes) {
   static std::mutex mu;
-  static std::map<const void*, unsigned long long> done;  // bit d: device d configured
+  static std::map<std::pair<const void*, int>, int> done;  // (kernel, device) -> bytes set
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   std::lock_guard<std::mutex> g(mu);
-  unsigned long long& bits = done[fn];
-  if (dev >= 0 && dev < 64 && (bits >> dev) & 1ull) return cudaSuccess;
+  int& have = done[{fn, dev}];
+  if (have >= bytes) return cudaSuccess;
   e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e == cudaSuccess && dev >= 0 && dev < 64) bits |= 1ull << dev;
+  if (e == cudaSuccess) have = bytes;
   return e;
 }
 

@@ -33,7 +33,8 @@ namespace ptdr {
 //   bit 0: phase B computes but does not store the output (isolates the read side);
 //   bit 1: phase-A TMA loads come from the first 256 rows of A (L2-resident: isolates
 //          the write side);
-//   bit 2: no butterflies (pure data movement through the same pipeline).
+//   bit 2: no butterflies (pure data movement through the same pipeline);
+//   bit 4: phase A skips its SMEM exchange (STS + LDS); bit 5: phase B skips its exchange.
 #ifndef PTDR_DIAG
 #define PTDR_DIAG 0
 #endif
@@ -635,18 +636,22 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
         }
         pwht<4>(v);
         __syncwarp();  // rows of this jh are read and written only by this warp
+        if constexpr ((kDiag & 16) == 0) {
 #pragma unroll
-        for (int kk = 0; kk < 16; ++kk) S[(jh * 16 + kk) * W + u] = v[kk];
+          for (int kk = 0; kk < 16; ++kk) S[(jh * 16 + kk) * W + u] = v[kk];
+        }
       }
       named_bar_sync(bar_id, GT);
       constexpr int R2 = R - 4;
       constexpr int UA = (W * 16) / GT;  // (u, jl) units per thread, each 2^R2 registers
+      if constexpr ((kDiag & 16) == 0) {
 #pragma unroll
-      for (int p = 0; p < UA; ++p) {
-        const int uu = gtid + GT * p;
-        const int u = uu & (W - 1), jl = uu >> XB;
+        for (int p = 0; p < UA; ++p) {
+          const int uu = gtid + GT * p;
+          const int u = uu & (W - 1), jl = uu >> XB;
 #pragma unroll
-        for (int j = 0; j < (1 << R2); ++j) v[p * (1 << R2) + j] = S[(j * 16 + jl) * W + u];
+          for (int j = 0; j < (1 << R2); ++j) v[p * (1 << R2) + j] = S[(j * 16 + jl) * W + u];
+        }
       }
       fence_proxy_async_smem();
       __syncwarp();
@@ -736,16 +741,20 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
       } else {
         constexpr int R2 = M - 4;
         constexpr int UB = (FB * 16) / GT;  // (f, jl) units per thread, 2^R2 registers each
+        if constexpr ((kDiag & 32) == 0) {
 #pragma unroll
-        for (int kk = 0; kk < 16; ++kk) S[(jh * 16 + kk) * FB + f] = v[kk];
+          for (int kk = 0; kk < 16; ++kk) S[(jh * 16 + kk) * FB + f] = v[kk];
+        }
         named_bar_sync(bar_id, GT);
         discard_tile();
+        if constexpr ((kDiag & 32) == 0) {
 #pragma unroll
-        for (int p = 0; p < UB; ++p) {
-          const int uu = gtid + GT * p;
-          const int f2 = uu % FB, jl = uu / FB;
+          for (int p = 0; p < UB; ++p) {
+            const int uu = gtid + GT * p;
+            const int f2 = uu % FB, jl = uu / FB;
 #pragma unroll
-          for (int j = 0; j < (1 << R2); ++j) v[p * (1 << R2) + j] = S[(j * 16 + jl) * FB + f2];
+            for (int j = 0; j < (1 << R2); ++j) v[p * (1 << R2) + j] = S[(j * 16 + jl) * FB + f2];
+          }
         }
         fence_proxy_async_smem();
         __syncwarp();

@@ -334,8 +334,9 @@ def main():
                          "kernel_ms": kmean, "algorithmic_bytes_per_launch": alg_bytes,
                          "hbm_passes": 1, "l2_round_trips": 1,
                          "note": "32 B/coefficient (16 B read of A + 16 B write); the partial "
-                                 "transforms make one round trip through an L2-resident scratch "
-                                 "(DESIGN.md section 7)"},
+                                 "transforms make one round trip through an L2-resident scratch, "
+                                 "whose traffic alone (no arithmetic) takes 6.75-7.3 ms at n=15 "
+                                 "(profiles/r01/micro/roundtrip_bench.txt; DESIGN.md section 7)"},
             "hbm_gbs_step": 32 * coeffs_total / (ms_per_step * 1e-3) / 1e9 / world,
             "gpu_launches": launches,
             "nvlink": (None if not ev_xchg else {

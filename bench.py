@@ -146,24 +146,35 @@ def cpu_baseline(n, seconds, variant=0):
         elapsed = time.perf_counter() - t0
     return {"value": done / elapsed, "unit": UNIT, "cores": threads, "kind": "oracle",
             "sample": f"{done} seeded-random coefficients of the n={n} seed-{SEED} matrix "
-                      f"(entries generated on the fly), {elapsed:.1f} s"}
+                      f"(entries generated on the fly), {elapsed:.1f} s",
+            "coefficients": done, "seconds": elapsed}
 
 
 def run_reference(a):
+    """The reference arm: the oracle (there is no reference code, the reference is a paper)
+    timed on the host cores -- W untimed warm-up steps, then exactly K timed steps, each a
+    bounded sample of the workload (about cpu_seconds / K seconds of oracle work)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    cb = cpu_baseline(a.n, a.cpu_seconds)
-    steps = [cpu_baseline(a.n, max(1.0, a.cpu_seconds / max(1, a.steps)))["value"]
-             for _ in range(max(1, min(a.steps, 5)))]
-    v = statistics.median(steps)
+    per = max(0.5, a.cpu_seconds / max(1, a.steps))
+    for _ in range(max(0, a.warmup)):
+        cpu_baseline(a.n, min(per, 0.5))
+    runs = [cpu_baseline(a.n, per) for _ in range(max(1, a.steps))]
+    done = sum(r["coefficients"] for r in runs)
+    secs = sum(r["seconds"] for r in runs)
+    v = done / secs
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus,
-        "steps": len(steps), "warmup": 0, "ms_per_step": None, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "steps": len(runs), "warmup": max(0, a.warmup), "ms_per_step": secs * 1e3 / len(runs),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
         "config": {"workload": f"n{a.n}_dense_general_seed{SEED}", "n": a.n,
                    "structure": "general", "seed": SEED},
-        "cpu_baseline": {**cb, "value": v},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": runs[0]["cores"], "kind": "oracle",
+                         "sample": f"{done} seeded-random coefficients of the n={a.n} seed-{SEED} "
+                                   f"matrix (entries generated on the fly) in {len(runs)} steps, "
+                                   f"{secs:.1f} s"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -427,7 +438,8 @@ def main():
                 line["e2e"] = {"error": repr(exc)[:200]}
 
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(n, a.cpu_seconds)
+        cb = cpu_baseline(n, a.cpu_seconds)
+        line["cpu_baseline"] = {k: v for k, v in cb.items() if k not in ("coefficients", "seconds")}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -119,31 +119,43 @@ constexpr int kInvSmem = 16 * 273 * 16;
 // the same buffer.  (Register loads with two CTAs per SM: 8.9 ms at n = 15; 16 B cp.async
 // into a double buffer: 12.7 ms.)
 constexpr int kInvStages = 3;
+constexpr int kInvGroups = 2;  // 256-thread groups per CTA, each transforming its own tiles
 
-__global__ void __launch_bounds__(256, 1) inv_pass1_kernel(const double2* __restrict__ c, double2* __restrict__ U,
-                                                           int n) {
+__global__ void __launch_bounds__(256 * kInvGroups, 1) inv_pass1_kernel(const double2* __restrict__ c,
+                                                                        double2* __restrict__ U, int n) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   double2* Tb = reinterpret_cast<double2*>(smem_raw);
   constexpr int TE = kInvSmem / 16;  // elements per buffer (padded layout; the raw copy uses 4096)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + kInvStages * kInvSmem);
+  // tag[b] = the tile sequence number last issued into buffer b: the two groups consume a
+  // buffer alternately, so a parity wait alone could match the previous occupant's phase
+  volatile int* tag = reinterpret_cast<volatile int*>(full + kInvStages);
   const u64 N = 1ull << n;
   const u64 xtiles = N >> 4;
   const u64 tiles = xtiles * (N >> 8);
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    for (int b = 0; b < kInvStages; ++b) mbar_init(&full[b], 1);
+  const int g = threadIdx.x >> 8, tid = threadIdx.x & 255;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < kInvStages; ++b) {
+      mbar_init(&full[b], 1);
+      tag[b] = -1;
+    }
     fence_mbar_init();
   }
   __syncthreads();
   const uint64_t pol = policy_evict_first();
-  // warp 0 issues tile t into buffer t % kInvStages (lane 0 arms the barrier, lanes 0-15 copy)
-  auto issue = [&](u64 t, int it) {
+  // CTA-local tile sequence it = 0, 1, 2, ...: tile blockIdx.x + it * gridDim.x, buffer
+  // it % kInvStages, transformed by group it % kInvGroups.  The first warp of the group that
+  // finishes tile it refills its buffer with tile it + kInvStages (lane 0 arms the barrier,
+  // lanes 0-15 copy the 16 runs).
+  auto issue = [&](int it) {
+    const u64 t = blockIdx.x + (u64)it * gridDim.x;
     if (t >= tiles) return;
     const int b = it % kInvStages;
     const u64 xt = (t % xtiles) << 4, zt = (t / xtiles) << 8;
     if (tid == 0) {
       fence_proxy_async_smem();  // the buffer was last written by generic stores
       mbar_arrive_expect_tx(&full[b], 4096u * 16u);
+      tag[b] = it;
     }
     __syncwarp();
     if (tid < 16) {
@@ -152,16 +164,16 @@ __global__ void __launch_bounds__(256, 1) inv_pass1_kernel(const double2* __rest
                 pol);
     }
   };
-  int it = 0;
-  if (tid < 32) {
-    issue(blockIdx.x, 0);
-    issue(blockIdx.x + gridDim.x, 1);
-  }
+  if (threadIdx.x < 32)
+    for (int it = 0; it < kInvStages; ++it) issue(it);
+  const int bar = 1 + g;
   const int f = tid >> 4, jl = tid & 15;
   const int qlo = (int)(spread_bits((u64)(f ^ jl)) | (spread_bits((u64)jl) << 1));
-  for (u64 tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+  for (int it = g;; it += kInvGroups) {
+    const u64 tile = blockIdx.x + (u64)it * gridDim.x;
+    if (tile >= tiles) break;
     const int b = it % kInvStages;
-    if (tid < 32) issue(tile + 2 * (u64)gridDim.x, it + 2);  // into the buffer freed last iteration
+    while (tag[b] != it) __nanosleep(20);
     mbar_wait(&full[b], (uint32_t)(it / kInvStages) & 1u);
     double2* T = Tb + (size_t)b * TE;
     const u64 xt = (tile % xtiles) << 4, zt = (tile / xtiles) << 8;
@@ -174,11 +186,11 @@ __global__ void __launch_bounds__(256, 1) inv_pass1_kernel(const double2* __rest
         v[kk] = rot_ipow(T[kk * 256 + qlo], 4 - (__popcll(x & z) & 3));
       }
       wht_regs<4>(v);
-      __syncthreads();  // every raw element is read before the padded layout overwrites it
+      named_bar_sync(bar, 256);  // every raw element is read before the padded layout overwrites it
 #pragma unroll
       for (int kk = 0; kk < 16; ++kk) T[inv_slot(f, jl + 16 * kk)] = v[kk];
     }
-    __syncthreads();
+    named_bar_sync(bar, 256);
     {
       const int kh = tid & 15;
 #pragma unroll
@@ -187,7 +199,7 @@ __global__ void __launch_bounds__(256, 1) inv_pass1_kernel(const double2* __rest
 #pragma unroll
       for (int j = 0; j < 16; ++j) T[inv_slot(f, j + 16 * kh)] = v[j];
     }
-    __syncthreads();
+    named_bar_sync(bar, 256);
     {
       const int fo = tid & 15, jg = tid >> 4;
       const u64 xo = xt + (u64)fo;
@@ -197,7 +209,8 @@ __global__ void __launch_bounds__(256, 1) inv_pass1_kernel(const double2* __rest
         st_stream(U + ((((xo >> 5) << n) + zt + (u64)j) << 5) + (xo & 31ull), T[inv_slot(fo, j)]);
       }
     }
-    __syncthreads();  // buffer b is refilled by a later issue
+    named_bar_sync(bar, 256);  // buffer b is free: refill it with tile it + kInvStages
+    if (tid < 32) issue(it + kInvStages);
   }
 }
 
@@ -266,7 +279,7 @@ cudaError_t launch_reconstruct(const double2* c, int n, double2* A, void* ws, cu
     if ((e = ensure_smem_attr(reinterpret_cast<const void*>(inv_pass1_kernel), smem)) != cudaSuccess) return e;
     u64 g = (N * N) >> 12;
     if (g > (u64)sms) g = (u64)sms;
-    inv_pass1_kernel<<<(unsigned)g, 256, smem, st>>>(c, U, n);
+    inv_pass1_kernel<<<(unsigned)g, 256 * kInvGroups, smem, st>>>(c, U, n);
     *nl += 1;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     *nl += 1;

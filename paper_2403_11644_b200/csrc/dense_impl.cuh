@@ -39,6 +39,8 @@ struct DenseArgs {
   int L;
   int nslot;
   int discard;         // pipeline: discard consumed scratch lines from L2 (no write-back)
+  int pol_a, pol_s, pol_b;  // pipeline L2 policies (policy_of codes): A loads, scratch stores,
+                            //   scratch loads
   int peer_shift;      // peer-pull mode (> 0): row i lives in shard i >> peer_shift
   u64 peer_rowmask;    //   at local row i & peer_rowmask
   int npeers;          //   shards (host side: tensor maps are built from peer_ptrs)

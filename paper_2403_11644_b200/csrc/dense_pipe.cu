@@ -86,6 +86,20 @@ cudaError_t launch_dense_pipe(int mode, const DenseArgs& a_in, const DensePlan& 
   {
     const char* nd = getenv("PTDR_NO_DISCARD");
     a.discard = (nd && nd[0] == '1') ? 0 : 1;
+    // L2 policies of A loads / scratch stores / scratch loads (developer override PTDR_POL,
+    // three letters of f n l u = evict_first / normal / last / unchanged)
+    // Default f n n, measured: scratch stores with evict_normal beat
+    // evict_last by ~3 % (8.02-8.09 vs 8.31-8.34 ms at n = 15); A must stay evict_first.
+    a.pol_a = 0;
+    a.pol_s = 1;
+    a.pol_b = 1;
+    const char* pe = getenv("PTDR_POL");
+    if (pe && strlen(pe) >= 3) {
+      auto code = [](char c) { return c == 'n' ? 1 : c == 'l' ? 2 : c == 'u' ? 3 : 0; };
+      a.pol_a = code(pe[0]);
+      a.pol_s = code(pe[1]);
+      a.pol_b = code(pe[2]);
+    }
   }
   cudaError_t e = cudaMemsetAsync(a.ctr, 0, p.ctr_bytes, st);
   if (e != cudaSuccess) return e;

@@ -40,6 +40,17 @@ namespace ptdr {
 #endif
 constexpr int kDiag = PTDR_DIAG;
 // bit 2 (diagnostics): skip the radix butterflies (data movement only)
+// bit 6 (diagnostics): output stores without the streaming hint; bit 7: output stores with
+// an L2 evict-first policy (createpolicy) instead of .cs
+__device__ __forceinline__ void st_out(double2* p, double2 v) {
+  if constexpr ((kDiag & 64) != 0) {
+    *p = v;
+  } else if constexpr ((kDiag & 128) != 0) {
+    st_global_hint(p, v, policy_evict_first());
+  } else {
+    st_stream(p, v);
+  }
+}
 template <int B>
 __device__ __forceinline__ void pwht(double2* v) {
   if constexpr ((kDiag & 4) == 0) wht_regs<B>(v);
@@ -144,7 +155,7 @@ __device__ __forceinline__ void emit_one(const DenseArgs& a, uint32_t q, uint32_
     if constexpr ((kDiag & 1) != 0) {
       if (re == 12345.678) st_stream(a.out + q, make_double2(re * s, im * s));  // keeps the math live
     } else {
-      st_stream(a.out + q, make_double2(re * s, im * s));
+      st_out(a.out + q, make_double2(re * s, im * s));
     }
   } else {
     // half-length modes: alpha = 2^{1-n} {Re, -Im, -Re, Im}[p mod 4] for z_t = 0 and the
@@ -153,8 +164,8 @@ __device__ __forceinline__ void emit_one(const DenseArgs& a, uint32_t q, uint32_
     const uint32_t p1 = p + 1u;
     const double v0 = ((p & 1u) ? w.y : w.x) * ((((p ^ (p >> 1)) & 1u) != 0) ? -s : s);
     const double v1 = ((p1 & 1u) ? w.y : w.x) * ((((p1 ^ (p1 >> 1)) & 1u) != 0) ? -s : s);
-    st_stream(a.out + q, make_double2(v0, 0.0));
-    st_stream(a.out + (q + dt), make_double2(v1, 0.0));
+    st_out(a.out + q, make_double2(v0, 0.0));
+    st_out(a.out + (q + dt), make_double2(v1, 0.0));
   }
 }
 
@@ -372,7 +383,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
   if (warp == 0) {
     if (lane == 0) {
       for (int pm = 0; pm < (a.peer_shift ? a.npeers : 1); ++pm) prefetch_tmap(&maps.m[pm]);
-      const uint64_t pol = policy_evict_first();
+      const uint64_t pol = policy_of(a.pol_a), pol_sl = policy_of(a.pol_b);
       const uint32_t total = C << (M + 1);
       // Decoded ticket: (tk, phase, chunk, tile) and its dependency counter, whose value is
       // requested (dv) one tile before it is checked.
@@ -449,7 +460,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
           fence_proxy_async_global();
           mbar_arrive_expect_tx(&full[s], (uint32_t)Cfg::TB);
           const double2* src = a.scratch + ((size_t)(chX & slot_mask) << slot_shift) + ((size_t)tlX << LT);
-          bulk_load(dst, src, (uint32_t)Cfg::TB, &full[s], pol);
+          bulk_load(dst, src, (uint32_t)Cfg::TB, &full[s], pol_sl);
         }
         trace_stamp(a.trace, k, 3);
         ++k;
@@ -589,7 +600,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
       constexpr int R2 = R - 4;
       constexpr int UA = (W * 16) / GT;   // second-stage units per thread, 2^R2 registers each
       double2* X = xbuf + g * Cfg::XE;
-      const uint64_t pol_last = policy_evict_last();
+      const uint64_t pol_last = policy_of(a.pol_s);
       // unit (u, jl) -> Y[tileB][ih][f]
       auto store_unit = [&](const double2* w, int jl) {
         const uint32_t phi_lo = phi_of<XB>((uint32_t)u, (uint32_t)jl);
@@ -657,7 +668,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       if (gtid == 0) trace_stamp(a.trace, k, 6);
-      const uint64_t pol_last = policy_evict_last();
+      const uint64_t pol_last = policy_of(a.pol_s);
 #pragma unroll
       for (int p = 0; p < UA; ++p) {
         const int uu = gtid + GT * p;

@@ -104,10 +104,26 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_unchanged() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
+}
+
+// 0: evict_first, 1: evict_normal, 2: evict_last, 3: evict_unchanged
+__device__ __forceinline__ uint64_t policy_of(int code) {
+  return code == 1 ? policy_evict_normal()
+                   : code == 2 ? policy_evict_last() : code == 3 ? policy_evict_unchanged() : policy_evict_first();
 }
 
 __device__ __forceinline__ void st_global_hint(double2* p, double2 v, uint64_t policy) {

@@ -114,6 +114,13 @@ inline DensePlan make_dense_plan(int nv, uint64_t x_count, int pipe_cfg = kPipeN
   p.NB = 1 << p.M;
   const int period = p.NA + p.NB;
   int L = (3 * resident + 2 * period - 1) / (2 * period);  // ceil(1.5*resident/period)
+  if (pipe_cfg != kPipeNone) {
+    // TMA pipeline: look ahead as far as ~40 MiB of live partials (L2-resident scratch)
+    // allows; measured optimum at n = 12..16 and Hermitian n = 13.
+    const uint64_t slot_bytes = ((uint64_t)p.W << nv) * 16;
+    const uint64_t lmax = (40ull << 20) / slot_bytes;
+    L = (int)(lmax < 2 ? 2 : (lmax > 64 ? 64 : lmax));
+  }
   if (L < 1) L = 1;
   if (L > 64) L = 64;
   p.L = L;

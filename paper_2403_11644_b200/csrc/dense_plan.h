@@ -52,11 +52,17 @@ inline PipeGeom pipe_geom(int cfg) {
     default: return {0, 4, 0, 0, 0, 0};
   }
 }
-constexpr int kPipeDefault = 4;   // preferred configuration
-constexpr int kPipeFallback = 1;  // when the preferred one does not fit (nv, x_count)
-// Fallback of a configuration that does not fit (nv, x_count): the same pipeline style
-// with 16-wide chunks.
-inline int pipe_fallback(int cfg) { return pipe_geom(cfg).NR ? 8 : kPipeFallback; }
+// Preferred configuration: 16-wide chunks (256 B row windows, 256-row phase-A tiles).  With
+// the look-ahead sized by live scratch bytes and evict-normal scratch stores it beats the
+// 32-wide configuration 4 by 1-5 % at n = 12..15 and on the Hermitian / real-symmetric
+// paths (`profiles/r01/sweep_cfg_final.txt`).
+constexpr int kPipeDefault = 1;
+// Fallback of a configuration that does not fit (nv, x_count): the same pipeline style with
+// the other chunk width (configuration 1 needs nv >= 12; n = 11 runs configuration 4).
+inline int pipe_fallback(int cfg) {
+  if (pipe_geom(cfg).NR) return cfg == 8 ? 6 : 8;
+  return cfg == 1 ? 4 : 1;
+}
 
 // Tiles resident at once on a B200 (fixes L deterministically, independent of the device).
 constexpr int kNominalSMs = 148;

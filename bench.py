@@ -39,7 +39,7 @@ def _args():
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--n", type=int, default=15)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--e2e-steps", type=int, default=6)
+    p.add_argument("--e2e-steps", type=int, default=12)  # steady state: fill and drain amortised
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)

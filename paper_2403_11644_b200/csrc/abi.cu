@@ -77,14 +77,14 @@ static bool valid_n(int n, int s) {
 // Dense-path kernel selection.  PTDR_DENSE_V1=1 forces the dense_impl.cuh kernels;
 // PTDR_PIPE_CFG=<k> picks a dense_pipe configuration (see dense_plan.h).
 static int pipe_choice() {
-  static int v = -1;
-  if (v < 0) {
+  // read once (thread-safe static initialisation)
+  static const int v = []() {
     const char* e1 = getenv("PTDR_DENSE_V1");
     const char* ec = getenv("PTDR_PIPE_CFG");
-    if (e1 && e1[0] == '1') v = kPipeNone;
-    else if (ec && ec[0] >= '1' && ec[0] <= '0' + kPipeCfgCount) v = ec[0] - '0';
-    else v = kPipeDefault;
-  }
+    if (e1 && e1[0] == '1') return kPipeNone;
+    if (ec && ec[0] >= '1' && ec[0] <= '0' + kPipeCfgCount) return ec[0] - '0';
+    return kPipeDefault;
+  }();
   return v;
 }
 

@@ -447,15 +447,15 @@ typedef CUresult (*PFN_memGetAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
 ptdr_status ptdr_ipc_get_handle(const void* dev_ptr, void* handle, uint64_t* offset) {
   if (!dev_ptr || !handle || !offset) return fail(PTDR_EINVAL, "null pointer");
   // the handle names the whole allocation: report where dev_ptr sits inside it
-  static PFN_memGetAddressRange range_fn = nullptr;
-  if (!range_fn) {
+  static const PFN_memGetAddressRange range_fn = []() -> PFN_memGetAddressRange {
     void* fp = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fp, cudaEnableDefault, &q) != cudaSuccess ||
         q != cudaDriverEntryPointSuccess)
-      return fail(PTDR_ECUDA, "cuMemGetAddressRange unavailable");
-    range_fn = reinterpret_cast<PFN_memGetAddressRange>(fp);
-  }
+      return nullptr;
+    return reinterpret_cast<PFN_memGetAddressRange>(fp);
+  }();
+  if (!range_fn) return fail(PTDR_ECUDA, "cuMemGetAddressRange unavailable");
   CUdeviceptr base = 0;
   size_t size = 0;
   if (range_fn(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)

@@ -16,12 +16,12 @@ cudaError_t pipe_cfg8(int mode, const TmapSet& map, const DenseArgs& a, int M, c
 
 static unsigned long long* g_trace = nullptr;
 static unsigned long long* debug_trace_buffer() {
-  static int on = -1;
-  if (on < 0) {
+  // developer timeline (PTDR_TRACE=1): allocated once, thread-safe
+  static std::once_flag once;
+  std::call_once(once, []() {
     const char* e = getenv("PTDR_TRACE");
-    on = (e && e[0] == '1') ? 1 : 0;
-    if (on && cudaMalloc(&g_trace, (size_t)kTraceTiles * 16 * 8) != cudaSuccess) g_trace = nullptr;
-  }
+    if (e && e[0] == '1' && cudaMalloc(&g_trace, (size_t)kTraceTiles * 16 * 8) != cudaSuccess) g_trace = nullptr;
+  });
   return g_trace;
 }
 int debug_trace_copy(void* host, size_t bytes) {

@@ -13,8 +13,9 @@ namespace ptdr {
 //   nv <= 5   : direct kernel (one thread per coefficient)
 //   nv in 6,7 : single-phase tiles (whole vector in one tile)
 //   nv >= 8   : two phases: phase A transforms the low R index bits (gather fused),
-//               phase B the high M bits (+ epilogue); x-chunks of 16 X-masks flow
-//               through an L2-resident scratch ring of `nslot` chunk slots.
+//               phase B the high M bits (+ epilogue); x-chunks of W X-masks (16 in the
+//               default pipeline configuration) flow through an L2-resident scratch ring
+//               of `nslot` chunk slots.
 struct DensePlan {
   int nv = 0;
   int kind = 0;        // 0 direct, 1 single, 2 two-phase

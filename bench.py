@@ -365,36 +365,43 @@ def main():
     # decomposes it on the device and downloads all 4^n coefficients into pinned host
     # memory; with two device slots the upload of step k+1 overlaps the download of step k.
     if world == 1 and not a.no_e2e:
-        del ws
-        torch.cuda.empty_cache()
-        import numpy as np
+        def e2e_single():
+            nonlocal A, ws
+            del ws
+            torch.cuda.empty_cache()
+            import numpy as np
 
-        host_in = torch.empty((N, N), dtype=torch.complex128, pin_memory=True)
-        host_in.copy_(A)
-        del A
-        torch.cuda.empty_cache()
-        host_out = [torch.empty(coeffs_total, dtype=torch.complex128, pin_memory=True) for _ in range(2)]
-        hin = host_in.numpy()
-        houts = [h.numpy() for h in host_out]
-        K = max(2, a.e2e_steps)
-        with ptdr.HostPlan(n, "general", depth=2) as plan:
-            plan.decompose_async(hin, houts[0])          # warm-up (allocations, module load)
-            plan.wait()
-            s0 = time.perf_counter()
-            for k in range(K):
-                plan.decompose_async(hin, houts[k % 2])
-            plan.wait()
-            e2e_s = (time.perf_counter() - s0) / K
-            e2e_launches = plan.launch_count() * K
-        # the streamed result must equal the device-timed one (same kernels, same input)
-        idx = torch.from_numpy(np.random.default_rng(7).integers(0, coeffs_total, 1 << 16))
-        same = bool(torch.equal(host_out[(K - 1) % 2][idx], out[idx.to(dev)].cpu()))
-        line["e2e"] = {"value": coeffs_total / e2e_s, "unit": UNIT,
-                       "h2d_bytes_per_step": 16 * coeffs_total, "d2h_bytes_per_step": 16 * coeffs_total,
-                       "steps": K, "s_per_step": e2e_s, "gpu_launches": e2e_launches,
-                       "matches_device_result": same,
-                       "api": "ptdr_plan_decompose_host_async, depth 2 (pinned host buffers)"}
-        del host_in, host_out, hin, houts
+            host_in = torch.empty((N, N), dtype=torch.complex128, pin_memory=True)
+            host_in.copy_(A)
+            del A
+            torch.cuda.empty_cache()
+            host_out = [torch.empty(coeffs_total, dtype=torch.complex128, pin_memory=True) for _ in range(2)]
+            hin = host_in.numpy()
+            houts = [h.numpy() for h in host_out]
+            K = max(2, a.e2e_steps)
+            with ptdr.HostPlan(n, "general", depth=2) as plan:
+                plan.decompose_async(hin, houts[0])          # warm-up (allocations, module load)
+                plan.wait()
+                s0 = time.perf_counter()
+                for k in range(K):
+                    plan.decompose_async(hin, houts[k % 2])
+                plan.wait()
+                e2e_s = (time.perf_counter() - s0) / K
+                e2e_launches = plan.launch_count() * K
+            # the streamed result must equal the device-timed one (same kernels, same input)
+            idx = torch.from_numpy(np.random.default_rng(7).integers(0, coeffs_total, 1 << 16))
+            same = bool(torch.equal(host_out[(K - 1) % 2][idx], out[idx.to(dev)].cpu()))
+            line["e2e"] = {"value": coeffs_total / e2e_s, "unit": UNIT,
+                           "h2d_bytes_per_step": 16 * coeffs_total, "d2h_bytes_per_step": 16 * coeffs_total,
+                           "steps": K, "s_per_step": e2e_s, "gpu_launches": e2e_launches,
+                           "matches_device_result": same,
+                           "api": "ptdr_plan_decompose_host_async, depth 2 (pinned host buffers)"}
+            del host_in, host_out, hin, houts
+
+        try:
+            e2e_single()
+        except Exception as exc:  # never lose the bench line over the e2e leg (e.g. pinned memory)
+            line["e2e"] = {"error": repr(exc)[:200]}
 
     # ---- end to end at N > 1: every rank uploads its row block from pinned host memory,
     # the step runs (exchange + decomposition, or the peer-pull kernel), and every rank

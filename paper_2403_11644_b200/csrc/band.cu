@@ -630,6 +630,35 @@ __device__ __forceinline__ void band_accum(const double2* __restrict__ Wg, unsig
   }
 }
 
+// NL segments with one sample each (block shift >= 8): all loads first, then the signed sums.
+template <int NL>
+__device__ __forceinline__ void band_accum_single(const BandSegRef* __restrict__ rf, const double2* Wb,
+                                                  unsigned lomask, unsigned z0, double (&re)[8], double (&im)[8]) {
+  double2 wk[NL];
+  unsigned lmk[NL];
+#pragma unroll
+  for (int kk = 0; kk < NL; ++kk) {
+    const unsigned long long rl = __ldg(&rf[kk].l), roff = __ldg(&rf[kk].off);
+    lmk[kk] = (unsigned)rl & lomask;
+#if defined(PTDR_DIAG) && (PTDR_DIAG & 8)
+    wk[kk] = make_double2((double)roff, 1.0);
+#else
+    wk[kk] = __ldg(Wb + roff);
+#endif
+  }
+#pragma unroll
+  for (int kk = 0; kk < NL; ++kk) {
+    const unsigned lm = lmk[kk];
+    const unsigned T = __byte_perm(0x66CCAA00u, 0x963C5AF0u, (lm >> 5) & 7u) ^ (0u - (__popc(lm & z0) & 1u));
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const double sg = __hiloint2double((int)(((T << (31 - j)) & 0x80000000u) | 0x3ff00000u), 0);
+      re[j] = fma(sg, wk[kk].x, re[j]);
+      im[j] = fma(sg, wk[kk].y, im[j]);
+    }
+  }
+}
+
 // Expansion: out[b][z] = 2^-n i^{popcount(x_b & z)} sum_k (-1)^{popcount(l_k & z_lo)} W_k[z_hi].
 // Every warp produces 256 consecutive outputs of one block, 8 per lane (z = base + lane + 32 j),
 // so each store instruction writes 512 B.  Warps walk the output in address order (group g =
@@ -679,36 +708,21 @@ __global__ void __launch_bounds__(256, 2) band_expand_kernel(const BandBlockDev*
     int k = 0;
     if (sh >= 8) {
       // one sample per segment: issue all of them (up to 8) before using any, so a group
-      // waits one memory latency instead of one per segment
-      constexpr int KB = 8;
-      double2 wk[KB];
-      unsigned lmk[KB];
-#pragma unroll
-      for (int kk = 0; kk < KB; ++kk) {
-        if (kk < nL) {
-          const unsigned long long rl = __ldg(&refs[first + kk].l), roff = __ldg(&refs[first + kk].off);
-          lmk[kk] = (unsigned)rl & lomask;
-#if defined(PTDR_DIAG) && (PTDR_DIAG & 8)
-          wk[kk] = make_double2((double)roff, 1.0);
-#else
-          wk[kk] = __ldg(segs + roff + ((z0 - lane) >> sh));
-#endif
-        }
+      // waits one memory latency instead of one per segment (exact counts: no predicated-off
+      // work for the common 2-4 segments)
+      const double2* Wb = segs + ((z0 - lane) >> sh);
+      switch (nL < 8 ? nL : 8) {
+        case 0: break;
+        case 1: band_accum_single<1>(refs + first, Wb, lomask, z0, re, im); break;
+        case 2: band_accum_single<2>(refs + first, Wb, lomask, z0, re, im); break;
+        case 3: band_accum_single<3>(refs + first, Wb, lomask, z0, re, im); break;
+        case 4: band_accum_single<4>(refs + first, Wb, lomask, z0, re, im); break;
+        case 5: band_accum_single<5>(refs + first, Wb, lomask, z0, re, im); break;
+        case 6: band_accum_single<6>(refs + first, Wb, lomask, z0, re, im); break;
+        case 7: band_accum_single<7>(refs + first, Wb, lomask, z0, re, im); break;
+        default: band_accum_single<8>(refs + first, Wb, lomask, z0, re, im); break;
       }
-#pragma unroll
-      for (int kk = 0; kk < KB; ++kk) {
-        if (kk < nL) {
-          const unsigned lm = lmk[kk];
-          const unsigned T = __byte_perm(0x66CCAA00u, 0x963C5AF0u, (lm >> 5) & 7u) ^ (0u - (__popc(lm & z0) & 1u));
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const double sg = __hiloint2double((int)(((T << (31 - j)) & 0x80000000u) | 0x3ff00000u), 0);
-            re[j] = fma(sg, wk[kk].x, re[j]);
-            im[j] = fma(sg, wk[kk].y, im[j]);
-          }
-        }
-      }
-      k = KB;
+      k = 8;
     }
     for (; k < nL; ++k) {
       const unsigned long long rl = __ldg(&refs[first + k].l), roff = __ldg(&refs[first + k].off);

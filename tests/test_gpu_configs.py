@@ -128,7 +128,7 @@ def test_n24_band_sampled(gpu, variant):
     assert np.max(np.abs(got - want)) <= TOL * maxabs
 
 
-@pytest.mark.parametrize("n,world", [(10, 2), (10, 4), (12, 8), (8, 2), (6, 4)])
+@pytest.mark.parametrize("n,world", [(10, 2), (10, 4), (12, 8), (8, 2), (6, 4), (11, 2), (13, 8), (14, 4)])
 def test_xshard_emulated_bitwise(gpu, n, world):
     """Every rank's shard path on one GPU == the single-GPU result, bit for bit."""
     torch = _torch()

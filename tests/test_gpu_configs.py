@@ -68,7 +68,9 @@ def test_small_configs_full_oracle(gpu, cfg):
 
 
 @pytest.mark.parametrize("cfg", [("n13a", 13, 2, "hermitian"), ("n13b", 13, 2, "real_symmetric"),
-                                 ("n15", 15, 4, "general"), ("n16", 16, 4, "general")])
+                                 ("n15", 15, 4, "general"), ("n16", 16, 4, "general"),
+                                 ("n15h", 15, 4, "hermitian"), ("n15s", 15, 4, "real_symmetric"),
+                                 ("n16h", 16, 4, "hermitian")])
 def test_large_configs_sampled(gpu, cfg):
     torch = _torch()
     _, n, seed, variant = cfg

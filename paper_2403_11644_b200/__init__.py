@@ -157,29 +157,76 @@ def last_launch_count() -> int:
     return int(lib().ptdr_last_launch_count())
 
 
-def _require_cuda_c128(t, name):
+def _require_cuda_c128(t, name, count=None, device=None):
+    """Type, size and device checks before any ABI call: the C ABI takes raw pointers and
+    cannot check buffer sizes itself."""
     import torch
 
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise TypeError(f"{name} must be a CUDA tensor (no CPU fallback)")
     if t.dtype != torch.complex128 or not t.is_contiguous():
         raise TypeError(f"{name} must be contiguous complex128")
+    if count is not None and t.numel() != count:
+        raise ValueError(f"{name} holds {t.numel()} elements, expected {count}")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name} is on {t.device}, expected {device}")
+
+
+def _require_workspace(ws, nbytes, device):
+    import torch
+
+    if not isinstance(ws, torch.Tensor) or not ws.is_cuda or not ws.is_contiguous():
+        raise TypeError("workspace must be a contiguous CUDA tensor")
+    if ws.device != device:
+        raise ValueError(f"workspace is on {ws.device}, expected {device}")
+    if ws.numel() * ws.element_size() < nbytes:
+        raise ValueError(f"workspace holds {ws.numel() * ws.element_size()} bytes, needs {nbytes}")
+
+
+def _keep_for_stream(stream, *tensors):
+    """Temporaries allocated here come from torch's caching allocator, which orders their
+    reuse on the CURRENT stream only.  When the kernels run on another stream, record that
+    stream on them so the blocks are not handed out again before the kernels finish."""
+    import torch
+
+    if stream is None:
+        return
+    if stream.cuda_stream == torch.cuda.current_stream(stream.device).cuda_stream:
+        return
+    for t in tensors:
+        if t is not None:
+            t.record_stream(stream)
+
+
+def _pow2_exponent(N: int, what: str) -> int:
+    n = int(N).bit_length() - 1
+    if N < 1 or (1 << n) != N:
+        raise ValueError(f"{what} must be a power of two (got {N}); use decompose_padded for other sizes")
+    return n
 
 
 def n_of(A, structure="general") -> int:
+    """n of an input array: dense [2^n, 2^n]; DIAGONAL / ANTI_DIAGONAL [2^n];
+    TRIDIAGONAL [3, 2^n] (or 3 * 2^n elements).  Torch tensors or numpy arrays."""
     s = _structure(structure)
+    ndim = len(A.shape)
+    numel = 1
+    for d in A.shape:
+        numel *= int(d)
     if s <= 2:
         N = A.shape[-1]
-        if A.dim() != 2 or A.shape[0] != N:
+        if ndim != 2 or A.shape[0] != N:
             raise ValueError("dense A must be 2^n x 2^n")
-    elif s in (3, 5):
-        N = A.numel()
-    else:
-        N = A.numel() // 3
-    n = N.bit_length() - 1
-    if (1 << n) != N:
-        raise ValueError("size must be a power of two (the paper's zero padding is out of scope)")
-    return n
+        return _pow2_exponent(N, "the matrix size")
+    if s in (3, 5):
+        if ndim != 1:
+            raise ValueError("DIAGONAL / ANTI_DIAGONAL input is a 1-D array of 2^n elements")
+        return _pow2_exponent(numel, "the band length")
+    if s == 4:
+        if numel % 3 != 0 or (ndim == 2 and A.shape[0] != 3) or ndim > 2:
+            raise ValueError("TRIDIAGONAL input is [3, 2^n] (sub, main, sup)")
+        return _pow2_exponent(numel // 3, "the band length")
+    raise ValueError(f"unknown structure {structure!r}")
 
 
 def alloc_workspace(n: int, structure="general", world: int = 1, device=None):
@@ -188,6 +235,28 @@ def alloc_workspace(n: int, structure="general", world: int = 1, device=None):
     nb = workspace_bytes(n, structure, world)
     # torch's caching allocator returns >= 512-byte aligned blocks
     return torch.empty(max(nb, 1), dtype=torch.uint8, device=device)
+
+
+def _workspace(workspace, n, structure, world, device, stream):
+    """The caller's workspace (checked), or a temporary kept alive for `stream`."""
+    nb = workspace_bytes(n, structure, world)
+    if workspace is None:
+        workspace = alloc_workspace(n, structure, world, device)
+        _keep_for_stream(stream, workspace)
+    else:
+        _require_workspace(workspace, nb, device)
+    return workspace
+
+
+def _out(out, count, device, stream):
+    import torch
+
+    if out is None:
+        out = torch.empty(count, dtype=torch.complex128, device=device)
+        _keep_for_stream(stream, out)
+    else:
+        _require_cuda_c128(out, "out", count, device)
+    return out
 
 
 def decompose(A, structure="general", out=None, workspace=None, stream=None):
@@ -200,11 +269,9 @@ def decompose(A, structure="general", out=None, workspace=None, stream=None):
     _require_cuda_c128(A, "A")
     s = _structure(structure)
     n = n_of(A, s)
-    if out is None:
-        out = torch.empty(output_count(n, s), dtype=torch.complex128, device=A.device)
-    _require_cuda_c128(out, "out")
-    if workspace is None:
-        workspace = alloc_workspace(n, s, 1, A.device)
+    _require_cuda_c128(A, "A", input_count(n, s))
+    out = _out(out, output_count(n, s), A.device, stream)
+    workspace = _workspace(workspace, n, s, 1, A.device, stream)
     st = lib().ptdr_decompose_async(ctypes.c_void_p(A.data_ptr()), n, s,
                                     ctypes.c_void_p(out.data_ptr()),
                                     ctypes.c_void_p(workspace.data_ptr()),
@@ -223,11 +290,14 @@ def decompose_host(A_host, structure="general", out_host=None):
         a = a.numpy()
     if a.dtype != np.complex128 or not a.flags.c_contiguous:
         raise TypeError("A_host must be C-contiguous complex128")
-    N = a.shape[-1] if s <= 2 else (a.size // 3 if s == 4 else a.size)
-    n = N.bit_length() - 1
+    n = n_of(a, s)
+    if a.size != input_count(n, s):
+        raise ValueError(f"A_host holds {a.size} elements, expected {input_count(n, s)}")
     if out_host is None:
         out_host = np.empty(output_count(n, s), dtype=np.complex128)
     o = out_host if isinstance(out_host, np.ndarray) else out_host.numpy()
+    if o.dtype != np.complex128 or not o.flags.c_contiguous or o.size != output_count(n, s):
+        raise ValueError(f"out_host must be C-contiguous complex128 with {output_count(n, s)} elements")
     st = lib().ptdr_decompose_host(ctypes.c_void_p(a.ctypes.data), n, s,
                                    ctypes.c_void_p(o.ctypes.data))
     _check(st, "ptdr_decompose_host")
@@ -292,11 +362,12 @@ def decompose_xshard(A_local, n: int, rank: int, world: int, out=None, workspace
     """Per-rank decomposition of the X-mask shard (after the all-to-all)."""
     import torch
 
-    _require_cuda_c128(A_local, "A_local")
-    if out is None:
-        out = torch.empty((1 << (2 * n)) // world, dtype=torch.complex128, device=A_local.device)
-    if workspace is None:
-        workspace = alloc_workspace(n, "general", world, A_local.device)
+    if world < 1 or world & (world - 1) or not 0 <= rank < world:
+        raise ValueError(f"invalid rank {rank} / world {world}")
+    count = (1 << (2 * n)) // world
+    _require_cuda_c128(A_local, "A_local", count)
+    out = _out(out, count, A_local.device, stream)
+    workspace = _workspace(workspace, n, "general", world, A_local.device, stream)
     st = lib().ptdr_decompose_xshard_async(ctypes.c_void_p(A_local.data_ptr()), n, rank, world,
                                            ctypes.c_void_p(out.data_ptr()),
                                            ctypes.c_void_p(workspace.data_ptr()),
@@ -313,8 +384,8 @@ def coefficients(A, qs, out=None, stream=None):
     _require_cuda_c128(A, "A")
     n = n_of(A, 0)
     q = torch.as_tensor(qs, dtype=torch.int64, device=A.device).contiguous()
-    if out is None:
-        out = torch.empty(q.numel(), dtype=torch.complex128, device=A.device)
+    _keep_for_stream(stream, q)
+    out = _out(out, q.numel(), A.device, stream)
     _check(lib().ptdr_coefficients_async(ctypes.c_void_p(A.data_ptr()), n, ctypes.c_void_p(q.data_ptr()), q.numel(),
                                          ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)),
            "ptdr_coefficients_async")
@@ -336,7 +407,8 @@ def decompose_batched(A, structure="general", out=None, stream=None):
     s = _structure(structure)
     if out is None:
         out = torch.empty((B, 4 ** n), dtype=torch.complex128, device=A.device)
-    _require_cuda_c128(out, "out")
+        _keep_for_stream(stream, out)
+    _require_cuda_c128(out, "out", B * 4 ** n, A.device)
     _check(lib().ptdr_decompose_batched_async(ctypes.c_void_p(A.data_ptr()), n, s, B,
                                               ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)),
            "ptdr_decompose_batched_async")
@@ -359,12 +431,15 @@ def decompose_padded(A, structure="general", out=None, workspace=None, stream=No
         _check(lib().ptdr_decompose_padded_async(None, 0, 0, s, None, None, 0, _stream_ptr(stream)),
                "ptdr_decompose_padded_async")
     n = max(1, (m - 1).bit_length())
-    if out is None:
-        out = torch.empty(4 ** n, dtype=torch.complex128, device=A.device)
-    _require_cuda_c128(out, "out")
+    out = _out(out, 4 ** n, A.device, stream)
+    nb = int(lib().ptdr_padded_workspace_bytes(m, s))
+    if nb == ctypes.c_size_t(-1).value:
+        raise PtdrError(PTDR_EINVAL, f"invalid (m={m}, structure={structure})")
     if workspace is None:
-        nb = int(lib().ptdr_padded_workspace_bytes(m, s))
         workspace = torch.empty(max(nb, 1), dtype=torch.uint8, device=A.device)
+        _keep_for_stream(stream, workspace)
+    elif workspace.device != A.device:
+        raise ValueError("workspace must be on A's device")
     _check(lib().ptdr_decompose_padded_async(ctypes.c_void_p(A.data_ptr()), m, lda, s,
                                              ctypes.c_void_p(out.data_ptr()),
                                              ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
@@ -379,14 +454,15 @@ def decompose_generated(n: int, seed: int, rank: int = 0, world: int = 1, out=No
     import torch
 
     dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
-    if out is None:
-        out = torch.empty((1 << (2 * n)) // world, dtype=torch.complex128, device=dev)
-    _require_cuda_c128(out, "out")
+    out = _out(out, (1 << (2 * n)) // world, dev, stream)
+    nb = int(lib().ptdr_generated_workspace_bytes(n, world))
+    if nb == ctypes.c_size_t(-1).value:
+        raise PtdrError(PTDR_EINVAL, f"invalid (n={n}, world={world})")
     if workspace is None:
-        nb = int(lib().ptdr_generated_workspace_bytes(n, world))
-        if nb == ctypes.c_size_t(-1).value:
-            raise PtdrError(PTDR_EINVAL, f"invalid (n={n}, world={world})")
         workspace = torch.empty(max(nb, 1), dtype=torch.uint8, device=dev)
+        _keep_for_stream(stream, workspace)
+    else:
+        _require_workspace(workspace, nb, dev)
     _check(lib().ptdr_decompose_generated_async(n, seed, rank, world, ctypes.c_void_p(out.data_ptr()),
                                                 ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
                                                 _stream_ptr(stream)), "ptdr_decompose_generated_async")
@@ -403,11 +479,8 @@ def decompose_peer(shard_ptrs, n: int, rank: int, world: int, out=None, workspac
     if len(shard_ptrs) != world:
         raise ValueError("one shard pointer per rank")
     dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
-    if out is None:
-        out = torch.empty((1 << (2 * n)) // world, dtype=torch.complex128, device=dev)
-    _require_cuda_c128(out, "out")
-    if workspace is None:
-        workspace = alloc_workspace(n, "general", world, dev)
+    out = _out(out, (1 << (2 * n)) // world, dev, stream)
+    workspace = _workspace(workspace, n, "general", world, dev, stream)
     arr = (ctypes.c_void_p * world)(*[ctypes.c_void_p(int(p)) for p in shard_ptrs])
     _check(lib().ptdr_decompose_peer_async(arr, n, rank, world, ctypes.c_void_p(out.data_ptr()),
                                            ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
@@ -445,11 +518,10 @@ def decompose_zshard(band, structure, rank: int, world: int, out=None, workspace
     _require_cuda_c128(band, "band")
     s = _structure(structure)
     n = n_of(band, s)
-    if out is None:
-        out = torch.empty(output_count(n, s) // world, dtype=torch.complex128, device=band.device)
-    _require_cuda_c128(out, "out")
-    if workspace is None:
-        workspace = alloc_workspace(n, s, world, band.device)
+    if world < 1 or world & (world - 1) or world > (1 << n) or not 0 <= rank < world:
+        raise ValueError(f"invalid rank {rank} / world {world}")
+    out = _out(out, output_count(n, s) // world, band.device, stream)
+    workspace = _workspace(workspace, n, s, world, band.device, stream)
     st = lib().ptdr_decompose_zshard_async(ctypes.c_void_p(band.data_ptr()), n, s, rank, world,
                                            ctypes.c_void_p(out.data_ptr()),
                                            ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
@@ -484,12 +556,15 @@ def decompose_band(diags, s: int, out=None, workspace=None, stream=None):
     if (1 << n) != N:
         raise ValueError("2^n columns")
     cnt = int(lib().ptdr_band_xmask_count(n, s))
-    if out is None:
-        out = torch.empty(cnt * N, dtype=torch.complex128, device=diags.device)
-    _require_cuda_c128(out, "out")
+    if cnt == 0:
+        raise PtdrError(PTDR_EINVAL, f"invalid (n={n}, s={s})")
+    out = _out(out, cnt * N, diags.device, stream)
+    nb = int(lib().ptdr_band_workspace_bytes(n, s))
     if workspace is None:
-        nb = int(lib().ptdr_band_workspace_bytes(n, s))
         workspace = torch.empty(max(nb, 1), dtype=torch.uint8, device=diags.device)
+        _keep_for_stream(stream, workspace)
+    else:
+        _require_workspace(workspace, nb, diags.device)
     st = lib().ptdr_decompose_band_async(ctypes.c_void_p(diags.data_ptr()), n, s, ctypes.c_void_p(out.data_ptr()),
                                          ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
                                          _stream_ptr(stream))
@@ -512,10 +587,14 @@ def reconstruct(coeffs, out=None, workspace=None, stream=None):
     n = _n_of_coeffs(coeffs)
     if out is None:
         out = torch.empty((1 << n, 1 << n), dtype=torch.complex128, device=coeffs.device)
-    _require_cuda_c128(out, "out")
+        _keep_for_stream(stream, out)
+    _require_cuda_c128(out, "out", 4 ** n, coeffs.device)
+    nb = int(lib().ptdr_reconstruct_workspace_bytes(n))
     if workspace is None:
-        workspace = torch.empty(int(lib().ptdr_reconstruct_workspace_bytes(n)), dtype=torch.uint8,
-                                device=coeffs.device)
+        workspace = torch.empty(nb, dtype=torch.uint8, device=coeffs.device)
+        _keep_for_stream(stream, workspace)
+    else:
+        _require_workspace(workspace, nb, coeffs.device)
     _check(lib().ptdr_reconstruct_async(ctypes.c_void_p(coeffs.data_ptr()), n, ctypes.c_void_p(out.data_ptr()),
                                         ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
                                         _stream_ptr(stream)), "ptdr_reconstruct_async")
@@ -527,11 +606,8 @@ def axpby(mu, x, nu, y, out=None, stream=None):
     import torch
 
     _require_cuda_c128(x, "x")
-    _require_cuda_c128(y, "y")
-    if x.numel() != y.numel():
-        raise ValueError("x and y sizes differ")
-    if out is None:
-        out = torch.empty_like(x)
+    _require_cuda_c128(y, "y", x.numel(), x.device)
+    out = _out(out, x.numel(), x.device, stream)
     mu, nu = complex(mu), complex(nu)
     _check(lib().ptdr_axpby_async(ctypes.c_void_p(out.data_ptr()), mu.real, mu.imag, ctypes.c_void_p(x.data_ptr()),
                                   nu.real, nu.imag, ctypes.c_void_p(y.data_ptr()), x.numel(), _stream_ptr(stream)),
@@ -549,8 +625,7 @@ def block_diag(blocks, out=None, stream=None):
     if (1 << k) != nb or blocks.dim() != 2:
         raise ValueError("blocks must be [2^k, 4^n]")
     n = _n_of_coeffs(blocks[0])
-    if out is None:
-        out = torch.empty(4 ** (n + k), dtype=torch.complex128, device=blocks.device)
+    out = _out(out, 4 ** (n + k), blocks.device, stream)
     _check(lib().ptdr_block_diag_async(ctypes.c_void_p(blocks.data_ptr()), n, k, ctypes.c_void_p(out.data_ptr()),
                                        _stream_ptr(stream)), "ptdr_block_diag_async")
     return out
@@ -569,8 +644,7 @@ def hermitian_augment(coeffs, out=None, stream=None):
 
     _require_cuda_c128(coeffs, "coeffs")
     n = _n_of_coeffs(coeffs)
-    if out is None:
-        out = torch.empty(4 ** (n + 1), dtype=torch.complex128, device=coeffs.device)
+    out = _out(out, 4 ** (n + 1), coeffs.device, stream)
     _check(lib().ptdr_hermitian_augment_async(ctypes.c_void_p(coeffs.data_ptr()), n, ctypes.c_void_p(out.data_ptr()),
                                               _stream_ptr(stream)), "ptdr_hermitian_augment_async")
     return out
@@ -588,7 +662,8 @@ def generate_dense(n: int, seed: int, variant="general", row0: int = 0, nrows=No
     nrows = N - row0 if nrows is None else nrows
     if out is None:
         out = torch.empty((nrows, N), dtype=torch.complex128, device=device or "cuda")
-    _require_cuda_c128(out, "out")
+        _keep_for_stream(stream, out)
+    _require_cuda_c128(out, "out", nrows * N)
     st = lib().ptdr_generate_dense_async(n, seed, int(v), row0, nrows,
                                          ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream))
     _check(st, "ptdr_generate_dense_async")
@@ -602,7 +677,8 @@ def generate_band(n: int, seed: int, variant="tridiagonal", out=None, device=Non
     shape = (1 << n,) if v == 3 else (3, 1 << n)
     if out is None:
         out = torch.empty(shape, dtype=torch.complex128, device=device or "cuda")
-    _require_cuda_c128(out, "out")
+        _keep_for_stream(stream, out)
+    _require_cuda_c128(out, "out", shape[0] if v == 3 else 3 << n)
     st = lib().ptdr_generate_band_async(n, seed, v, ctypes.c_void_p(out.data_ptr()),
                                         _stream_ptr(stream))
     _check(st, "ptdr_generate_band_async")
@@ -617,7 +693,8 @@ def generate_sendblocks(n: int, seed: int, rank: int, world: int, out=None, devi
     R = N // world
     if out is None:
         out = torch.empty((world, R, R), dtype=torch.complex128, device=device or "cuda")
-    _require_cuda_c128(out, "out")
+        _keep_for_stream(stream, out)
+    _require_cuda_c128(out, "out", world * R * R)
     st = lib().ptdr_generate_sendblocks_async(n, seed, rank, world,
                                               ctypes.c_void_p(out.data_ptr()),
                                               _stream_ptr(stream))

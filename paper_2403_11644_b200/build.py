@@ -13,7 +13,14 @@ TRACE_BUILD = os.environ.get("PTDR_TRACE_BUILD") == "1"  # developer timeline bu
 # Developer diagnostic builds: PTDR_DIAG_BUILD=<bits> compiles dense_pipe.cuh with
 # -DPTDR_DIAG=<bits> into libptdr_diag<bits>.so (never loaded by the product path).
 DIAG_BUILD = os.environ.get("PTDR_DIAG_BUILD", "")
-_VARIANT = "_trace" if TRACE_BUILD else (f"_diag{DIAG_BUILD}" if DIAG_BUILD else "")
+# PTDR_DEV_BUILD=1: libptdr_dev.so with every pipeline configuration and the PTDR_*
+# environment switches (DESIGN.md section 7 sweeps).  Trace and diagnostic builds are
+# developer builds too.  The product library reads no environment variable.
+DEV_BUILD = os.environ.get("PTDR_DEV_BUILD") == "1"
+_VARIANT = "_trace" if TRACE_BUILD else (f"_diag{DIAG_BUILD}" if DIAG_BUILD else ("_dev" if DEV_BUILD else ""))
+IS_DEV = bool(_VARIANT)
+# pipeline configurations only developer builds instantiate (dense_plan.h pipe_cfg_built)
+DEV_ONLY_SOURCES = {f"dense_pipe_c{k}.cu" for k in (2, 3, 5, 6, 7, 8)}
 BUILD = os.path.join(HERE, "_build" + _VARIANT)
 LIB = os.path.join(HERE, f"libptdr{_VARIANT}.so")
 ROOT = os.path.dirname(HERE)
@@ -26,7 +33,8 @@ NVCC_FLAGS = [
     "-Xptxas", "-v",
     "--expt-relaxed-constexpr",
     f"-I{os.path.join(ROOT, 'include')}",
-] + (["-DPTDR_ENABLE_TRACE=1"] if TRACE_BUILD else []) + ([f"-DPTDR_DIAG={DIAG_BUILD}"] if DIAG_BUILD else [])
+] + (["-DPTDR_ENABLE_TRACE=1"] if TRACE_BUILD else []) + ([f"-DPTDR_DIAG={DIAG_BUILD}"] if DIAG_BUILD else []) \
+  + (["-DPTDR_DEV=1"] if IS_DEV else [])
 
 
 def _deps():
@@ -60,7 +68,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale(LIB, deps):
         return LIB
     os.makedirs(BUILD, exist_ok=True)
-    srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    srcs = sorted(s for s in glob.glob(os.path.join(CSRC, "*.cu"))
+                  if IS_DEV or os.path.basename(s) not in DEV_ONLY_SOURCES)
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
     tmp = LIB + ".tmp"

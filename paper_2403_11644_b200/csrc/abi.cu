@@ -74,9 +74,12 @@ static bool valid_n(int n, int s) {
 }
 
 
-// Dense-path kernel selection.  PTDR_DENSE_V1=1 forces the dense_impl.cuh kernels;
-// PTDR_PIPE_CFG=<k> picks a dense_pipe configuration (see dense_plan.h).
+// Dense-path kernel selection.  The product library always takes the default pipeline
+// configuration (dense_plan.h kPipeDefault).  Developer builds (PTDR_DEV=1: build.py with
+// PTDR_DEV_BUILD / PTDR_TRACE_BUILD / PTDR_DIAG_BUILD) also read PTDR_DENSE_V1=1 (force the
+// dense_impl.cuh kernels) and PTDR_PIPE_CFG=<k> (another dense_pipe configuration).
 static int pipe_choice() {
+#if PTDR_DEV
   // read once (thread-safe static initialisation)
   static const int v = []() {
     const char* e1 = getenv("PTDR_DENSE_V1");
@@ -86,6 +89,9 @@ static int pipe_choice() {
     return kPipeDefault;
   }();
   return v;
+#else
+  return kPipeDefault;
+#endif
 }
 
 static bool pipe_mode(int mode) {
@@ -95,11 +101,13 @@ static bool pipe_mode(int mode) {
 static DensePlan plan_for(int mode, int nv, uint64_t x_count) {
   return make_dense_plan(nv, x_count, pipe_mode(mode) ? pipe_choice() : kPipeNone, kSingleMax);
 }
-// The workspace is the max over every kernel choice so the env switches never need more.
+// The workspace is the max over every kernel choice the library can make (developer
+// builds: every configuration) so that the size never depends on a switch.
 static size_t plan_ws(int nv, uint64_t x_count) {
   size_t m = 0;
   for (int cfg = kPipeNone; cfg <= kPipeCfgCount; ++cfg)
     for (int smax : {7, kSingleMax}) {
+      if (!pipe_cfg_built(cfg)) continue;
       const size_t b = make_dense_plan(nv, x_count, cfg, smax).ws_bytes();
       if (b > m) m = b;
     }
@@ -627,14 +635,18 @@ static bool padded_in_place(int n, int structure) {
          plan_for(MODE_GENERAL, n, 1ull << n).kind == 2;
 }
 
+// Bytes of the zero-padded copy that precedes the decomposition whenever the stored block
+// cannot be read in place.  The size function does not know the row pitch, so it covers
+// every pitch: an exact m = 2^n with lda != m also takes the copy.
+static size_t pad_copy_bytes(int n) { return ((((size_t)16 << (2 * n)) + 255) / 256) * 256; }
+
 size_t ptdr_padded_workspace_bytes(uint64_t m, int structure) {
   if (m < 1 || !is_dense(structure)) return (size_t)-1;
   const int n = padded_n(m);
   if (n > 16) return (size_t)-1;
   const size_t base = ptdr_workspace_bytes(n, structure, 1);
-  const bool exact = (1ull << n) == m;
-  if (exact || padded_in_place(n, structure)) return base;
-  return ((((size_t)16 << (2 * n)) + 255) / 256) * 256 + base;
+  if (padded_in_place(n, structure)) return base;
+  return pad_copy_bytes(n) + base;
 }
 
 ptdr_status ptdr_decompose_padded_async(const ptdr_c128* A, uint64_t m, uint64_t lda, int structure,
@@ -662,7 +674,9 @@ ptdr_status ptdr_decompose_padded_async(const ptdr_c128* A, uint64_t m, uint64_t
     r = run_dense(reinterpret_cast<const double2*>(A), n, structure, reinterpret_cast<double2*>(out), workspace, st,
                   &nl, lda, m);
   } else {
-    const size_t pad_b = ((((size_t)16 << (2 * n)) + 255) / 256) * 256;
+    const size_t pad_b = pad_copy_bytes(n);
+    if (!workspace || ws_bytes < pad_b + ptdr_workspace_bytes(n, structure, 1))
+      return fail(PTDR_ENOMEM, "workspace too small for the zero-padded copy");
     double2* P = reinterpret_cast<double2*>(workspace);
     const uint64_t N = 1ull << n;
     uint64_t g = (N * N + 255) / 256;

@@ -12,6 +12,8 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "engine.cuh"
@@ -795,21 +797,36 @@ size_t band_s_workspace_bytes(int n, int s) {
   return make_band_plan(n, s).ws_bytes;
 }
 
-cudaError_t launch_band_s(const double2* diags, int n, int s, double2* out, void* ws, cudaStream_t st,
-                          int* nl) {
-  BandPlan p = make_band_plan(n, s);
+// Device tables of a (n, s) plan, staged once per process in pinned host memory: the
+// per-call upload is then a truly asynchronous copy from a buffer that outlives every
+// launch (graph-capturable), instead of a pageable copy that synchronises the stream
+// (ADVICE r01).  Entries are immutable once built; the cache holds one table per (n, s).
+struct BandTables {
+  BandPlan plan;
+  void* pinned = nullptr;
+  size_t xb_off = 0;
+};
+static const BandTables* band_tables(int n, int s, cudaError_t* err) {
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, BandTables*> cache;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find({n, s});
+  if (it != cache.end()) return it->second;
+  BandTables* T = new BandTables();
+  T->plan = make_band_plan(n, s);
+  const BandPlan& p = T->plan;
   const int nseg = (int)p.refs.size(), nb = (int)p.blocks.size();
-  char* base = reinterpret_cast<char*>(ws);
-  BandBlockDev* dblocks = reinterpret_cast<BandBlockDev*>(base);
-  BandSegRef* drefs = reinterpret_cast<BandSegRef*>(base + nb * sizeof(BandBlockDev));
-  int4* dgat = reinterpret_cast<int4*>(base + nb * sizeof(BandBlockDev) + nseg * sizeof(BandSegRef));
-  double2* segs = reinterpret_cast<double2*>(base + p.table_bytes);
-  std::vector<char> host(p.table_bytes, 0);
-  memcpy(host.data(), p.blocks.data(), nb * sizeof(BandBlockDev));
-  memcpy(host.data() + nb * sizeof(BandBlockDev), p.refs.data(), nseg * sizeof(BandSegRef));
+  if ((*err = cudaHostAlloc(&T->pinned, p.table_bytes, cudaHostAllocPortable)) != cudaSuccess) {
+    delete T;
+    return nullptr;
+  }
+  char* host = reinterpret_cast<char*>(T->pinned);
+  memset(host, 0, p.table_bytes);
+  memcpy(host, p.blocks.data(), nb * sizeof(BandBlockDev));
+  memcpy(host + nb * sizeof(BandBlockDev), p.refs.data(), nseg * sizeof(BandSegRef));
   std::vector<int4> gat(nseg);
   for (int k = 0; k < nseg; ++k) gat[k] = make_int4(p.seg_t[k], p.seg_d[k], p.seg_lam[k], 0);
-  memcpy(host.data() + nb * sizeof(BandBlockDev) + nseg * sizeof(BandSegRef), gat.data(), nseg * sizeof(int4));
+  memcpy(host + nb * sizeof(BandBlockDev) + nseg * sizeof(BandSegRef), gat.data(), nseg * sizeof(int4));
   // x -> block table for the diagonal-order gather
   const int sw = s > 0 ? s : 1;
   std::vector<int> xb((size_t)n * sw, -1);
@@ -819,11 +836,26 @@ cudaError_t launch_band_s(const double2* diags, int n, int s, double2* out, void
     const unsigned long long e = ((2ull << B.t) - 1ull) - B.x;
     if (e < (unsigned long long)sw) xb[(size_t)B.t * sw + e] = bi;
   }
-  const size_t xb_off = nb * sizeof(BandBlockDev) + nseg * sizeof(BandSegRef) + nseg * sizeof(int4);
-  memcpy(host.data() + xb_off, xb.data(), xb.size() * sizeof(int));
-  const int* dxb = reinterpret_cast<const int*>(base + xb_off);
-  // pageable source: the call returns once the bytes are staged, so `host` may go
-  cudaError_t e = cudaMemcpyAsync(base, host.data(), p.table_bytes, cudaMemcpyHostToDevice, st);
+  T->xb_off = nb * sizeof(BandBlockDev) + nseg * sizeof(BandSegRef) + nseg * sizeof(int4);
+  memcpy(host + T->xb_off, xb.data(), xb.size() * sizeof(int));
+  cache[{n, s}] = T;
+  return T;
+}
+
+cudaError_t launch_band_s(const double2* diags, int n, int s, double2* out, void* ws, cudaStream_t st,
+                          int* nl) {
+  cudaError_t e = cudaSuccess;
+  const BandTables* T = band_tables(n, s, &e);
+  if (!T) return e;
+  const BandPlan& p = T->plan;
+  const int nseg = (int)p.refs.size(), nb = (int)p.blocks.size();
+  char* base = reinterpret_cast<char*>(ws);
+  BandBlockDev* dblocks = reinterpret_cast<BandBlockDev*>(base);
+  BandSegRef* drefs = reinterpret_cast<BandSegRef*>(base + nb * sizeof(BandBlockDev));
+  int4* dgat = reinterpret_cast<int4*>(base + nb * sizeof(BandBlockDev) + nseg * sizeof(BandSegRef));
+  double2* segs = reinterpret_cast<double2*>(base + p.table_bytes);
+  const int* dxb = reinterpret_cast<const int*>(base + T->xb_off);
+  e = cudaMemcpyAsync(base, T->pinned, p.table_bytes, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return e;
   const int sms = device_sm_count();
   if (s >= 1) {

@@ -6,17 +6,21 @@
 namespace ptdr {
 
 cudaError_t pipe_cfg1(int mode, const TmapSet& map, const DenseArgs& a, int M, cudaStream_t st);
+cudaError_t pipe_cfg4(int mode, const TmapSet& map, const DenseArgs& a, int M, cudaStream_t st);
+#if PTDR_DEV
+// developer-only configurations (dense_plan.h pipe_cfg_built; DESIGN.md section 7 sweeps)
 cudaError_t pipe_cfg2(int mode, const TmapSet& map, const DenseArgs& a, int M, cudaStream_t st);
 cudaError_t pipe_cfg3(int mode, const TmapSet& map, const DenseArgs& a, int M, cudaStream_t st);
-cudaError_t pipe_cfg4(int mode, const TmapSet& map, const DenseArgs& a, int M, cudaStream_t st);
 cudaError_t pipe_cfg5(int mode, const TmapSet& map, const DenseArgs& a, int M, cudaStream_t st);
 cudaError_t pipe_cfg6(int mode, const TmapSet& map, const DenseArgs& a, int M, cudaStream_t st);
 cudaError_t pipe_cfg7(int mode, const TmapSet& map, const DenseArgs& a, int M, cudaStream_t st);
 cudaError_t pipe_cfg8(int mode, const TmapSet& map, const DenseArgs& a, int M, cudaStream_t st);
+#endif
 
+#if PTDR_ENABLE_TRACE
 static unsigned long long* g_trace = nullptr;
 static unsigned long long* debug_trace_buffer() {
-  // developer timeline (PTDR_TRACE=1): allocated once, thread-safe
+  // developer timeline (trace build, PTDR_TRACE=1): allocated once, thread-safe
   static std::once_flag once;
   std::call_once(once, []() {
     const char* e = getenv("PTDR_TRACE");
@@ -30,6 +34,10 @@ int debug_trace_copy(void* host, size_t bytes) {
   if (cudaDeviceSynchronize() != cudaSuccess) return -2;
   return cudaMemcpy(host, g_trace, n, cudaMemcpyDeviceToHost) == cudaSuccess ? (int)n : -3;
 }
+#else
+static unsigned long long* debug_trace_buffer() { return nullptr; }
+int debug_trace_copy(void*, size_t) { return -1; }
+#endif
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static std::once_flag once;
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -48,12 +56,16 @@ cudaError_t launch_dense_pipe(int mode, const DenseArgs& a_in, const DensePlan& 
   if (p.kind != 2 || p.pipe_cfg == 0) return cudaErrorInvalidValue;
   DenseArgs a = a_in;
   a.L = p.L;
+#if PTDR_DEV
   {
-    // developer override of the look-ahead (the workspace formula already covers any L:
-    // nslot is fixed by the byte budget, counters by the chunk count)
+    // developer override of the look-ahead.  Liveness needs L + 1 <= nslot (phase A of
+    // chunk c waits for phase B of chunk c - nslot, whose tickets follow A(c - nslot + L + 1)),
+    // so the override is clamped to nslot - 1.
     const char* el = getenv("PTDR_L");
     if (el && atoi(el) > 0) a.L = atoi(el);
+    if (a.L > p.nslot - 1) a.L = p.nslot - 1 > 1 ? p.nslot - 1 : 1;
   }
+#endif
   a.nslot = p.nslot;
   a.slot_elems = p.slot_elems;
   PFN_cuTensorMapEncodeTiled_v12000 enc = encode_fn();
@@ -84,15 +96,19 @@ cudaError_t launch_dense_pipe(int mode, const DenseArgs& a_in, const DensePlan& 
   }
   if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
   {
-    const char* nd = getenv("PTDR_NO_DISCARD");
-    a.discard = (nd && nd[0] == '1') ? 0 : 1;
-    // L2 policies of A loads / scratch stores / scratch loads (developer override PTDR_POL,
-    // three letters of f n l u = evict_first / normal / last / unchanged)
-    // Default f n n, measured: scratch stores with evict_normal beat
-    // evict_last by ~3 % (8.02-8.09 vs 8.31-8.34 ms at n = 15); A must stay evict_first.
+    // L2 policies of A loads / scratch stores / scratch loads: f n n, measured (DESIGN.md
+    // section 7): scratch stores with evict_normal beat evict_last by ~3 % (8.02-8.09 vs
+    // 8.31-8.34 ms at n = 15); A must stay evict_first.  Consumed scratch lines are
+    // discarded from L2.
+    a.discard = 1;
     a.pol_a = 0;
     a.pol_s = 1;
     a.pol_b = 1;
+#if PTDR_DEV
+    // developer overrides: PTDR_NO_DISCARD=1, PTDR_POL = three letters of f n l u
+    // (evict_first / normal / last / unchanged)
+    const char* nd = getenv("PTDR_NO_DISCARD");
+    if (nd && nd[0] == '1') a.discard = 0;
     const char* pe = getenv("PTDR_POL");
     if (pe && strlen(pe) >= 3) {
       auto code = [](char c) { return c == 'n' ? 1 : c == 'l' ? 2 : c == 'u' ? 3 : 0; };
@@ -100,6 +116,7 @@ cudaError_t launch_dense_pipe(int mode, const DenseArgs& a_in, const DensePlan& 
       a.pol_s = code(pe[1]);
       a.pol_b = code(pe[2]);
     }
+#endif
   }
   cudaError_t e = cudaMemsetAsync(a.ctr, 0, p.ctr_bytes, st);
   if (e != cudaSuccess) return e;
@@ -111,13 +128,15 @@ cudaError_t launch_dense_pipe(int mode, const DenseArgs& a_in, const DensePlan& 
   *nlaunch += 1;
   switch (p.pipe_cfg) {
     case 1: return pipe_cfg1(mode, map, a, p.M, st);
+    case 4: return pipe_cfg4(mode, map, a, p.M, st);
+#if PTDR_DEV
     case 2: return pipe_cfg2(mode, map, a, p.M, st);
     case 3: return pipe_cfg3(mode, map, a, p.M, st);
-    case 4: return pipe_cfg4(mode, map, a, p.M, st);
     case 5: return pipe_cfg5(mode, map, a, p.M, st);
     case 6: return pipe_cfg6(mode, map, a, p.M, st);
     case 7: return pipe_cfg7(mode, map, a, p.M, st);
     case 8: return pipe_cfg8(mode, map, a, p.M, st);
+#endif
     default: return cudaErrorInvalidValue;
   }
 }

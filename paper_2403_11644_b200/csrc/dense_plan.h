@@ -40,6 +40,13 @@ struct PipeGeom {
 };
 constexpr int kPipeNone = 0;
 constexpr int kPipeCfgCount = 8;
+// Developer builds (PTDR_DEV=1, build.py) compile every configuration and read the
+// PTDR_* environment switches; the product library has configurations 1 and 4 only (the
+// default and its n = 11 fallback) and reads no environment variable.
+#ifndef PTDR_DEV
+#define PTDR_DEV 0
+#endif
+inline bool pipe_cfg_built(int cfg) { return PTDR_DEV || cfg == kPipeNone || cfg == 1 || cfg == 4; }
 inline PipeGeom pipe_geom(int cfg) {
   switch (cfg) {
     case 1: return {12, 4, 8, 2, 3, 0};

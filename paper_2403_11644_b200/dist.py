@@ -36,6 +36,10 @@ def decompose_sharded(send: torch.Tensor, n: int, group=None, out=None, recv=Non
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     recv = exchange(send, group, recv)
+    if stream is not None:
+        # all_to_all_single is ordered on the current stream only: make `stream` wait for
+        # the exchange before the kernels read `recv`
+        stream.wait_stream(torch.cuda.current_stream(send.device))
     N = 1 << n
     return decompose_xshard(recv.view(N, N // world), n, rank, world, out=out,
                             workspace=workspace, stream=stream)

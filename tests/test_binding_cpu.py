@@ -44,3 +44,29 @@ def test_q_order_helpers_roundtrip():
     for q in range(4 ** n):
         x, z = ptdr.xz_of(q, n)
         assert ptdr.q_of(x, z, n) == q
+
+
+def test_band_shapes_are_validated():
+    with pytest.raises(ValueError):
+        ptdr.n_of(torch.zeros(3 * 5), "tridiagonal")        # 5 is not a power of two
+    with pytest.raises(ValueError):
+        ptdr.n_of(torch.zeros((4, 8)), "tridiagonal")       # [3, 2^n] only
+    with pytest.raises(ValueError):
+        ptdr.n_of(torch.zeros((2, 8)), "diagonal")          # 1-D band
+    with pytest.raises(ValueError):
+        ptdr.n_of(torch.zeros(0), "diagonal")
+
+
+def test_host_entry_validates_sizes_before_the_abi_call():
+    """decompose_host checks every size against n before passing raw host pointers (the
+    ABI cannot): a non-square, non-power-of-two or wrongly sized out_host is refused."""
+    with pytest.raises(ValueError):
+        ptdr.decompose_host(np.zeros((4, 8), dtype=np.complex128))
+    with pytest.raises(ValueError):
+        ptdr.decompose_host(np.zeros((6, 6), dtype=np.complex128))
+    with pytest.raises(ValueError):
+        ptdr.decompose_host(np.zeros((4, 4), dtype=np.complex128), out_host=np.zeros(15, dtype=np.complex128))
+    with pytest.raises(ValueError):
+        ptdr.decompose_host(np.zeros(3 * 8 + 1, dtype=np.complex128), "tridiagonal")
+    with pytest.raises(TypeError):
+        ptdr.decompose_host(np.zeros((4, 4), dtype=np.complex64))

@@ -93,3 +93,28 @@ def test_padded_empty_is_rejected(gpu):
     with pytest.raises(ptdr.PtdrError) as e:
         ptdr.decompose_padded(A)
     assert e.value.status == ptdr.PTDR_EINVAL
+
+
+@pytest.mark.parametrize("m,variant", [(1024, "hermitian"), (1024, "real_symmetric"), (512, "general"),
+                                       (16, "general"), (16, "hermitian")])
+def test_padded_exact_size_strided_view(gpu, m, variant):
+    """m = 2^n stored with row pitch > m takes the zero-padded copy: the
+    workspace the size function reports must cover that copy, and the result must equal the
+    contiguous decomposition bit for bit."""
+    torch = _torch()
+    rng = np.random.default_rng(m + len(variant))
+    big = _matrix(rng, 2100, variant)
+    Bt = torch.from_numpy(big).cuda()
+    view = Bt[:m, :m]
+    nb = int(ptdr.lib().ptdr_padded_workspace_bytes(m, ptdr.STRUCTURES[variant]))
+    assert nb >= 16 * m * m
+    got = ptdr.decompose_padded(view, variant).cpu().numpy()
+    want = ptdr.decompose(view.contiguous(), variant).cpu().numpy()
+    assert np.array_equal(got, want)
+    # an exact-size workspace passes, a byte short is refused before any launch
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    got2 = ptdr.decompose_padded(view, variant, workspace=ws).cpu().numpy()
+    assert np.array_equal(got2, want)
+    with pytest.raises(ptdr.PtdrError) as e:
+        ptdr.decompose_padded(view, variant, workspace=ws[: nb - 256])
+    assert e.value.status == ptdr.PTDR_ENOMEM

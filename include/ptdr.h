@@ -109,6 +109,20 @@ ptdr_status ptdr_decompose(const ptdr_c128* A, int n, int structure, ptdr_c128* 
 ptdr_status ptdr_decompose_async(const ptdr_c128* A, int n, int structure, ptdr_c128* out,
                                  void* workspace, size_t ws_bytes, void* stream);
 
+/* In-place decomposition (BASELINE.json configs[4]: "n=16 ... at 1 GPU in-place"): A (device,
+ * dense, 4^n elements) is overwritten with its coefficients in the MATRIX LAYOUT
+ *   A[z][z ^ x] = alpha(x, z)   (x, z: X- and Z-mask of the string; a bit permutation of
+ *                                the q order, Python helper matrix_index),
+ * i.e. each coefficient sits where the element A[z][z ^ x] of its XOR-diagonal was.  The
+ * X-masks of a pipeline chunk read and write exactly the same elements, so no second
+ * 4^n buffer is needed: n = 16 takes 64 GiB + ptdr_inplace_workspace_bytes (2 GiB) on one
+ * GPU.  HERMITIAN / REAL_SYMMETRIC read only their triangle as in ptdr_decompose_async and
+ * overwrite the whole matrix.  Values are bitwise those of ptdr_decompose_async.
+ * workspace: device, 256-byte aligned, not overlapping A. */
+size_t ptdr_inplace_workspace_bytes(int n, int structure); /* (size_t)-1 if invalid */
+ptdr_status ptdr_decompose_inplace_async(ptdr_c128* A, int n, int structure, void* workspace,
+                                         size_t ws_bytes, void* stream);
+
 /* End-to-end from HOST memory: copies A_host to the device, decomposes, copies the
  * result to out_host, synchronizes.  Host buffers may be pageable or pinned
  * (pinned is faster).  Allocates and frees its own device buffers. */
@@ -122,6 +136,11 @@ ptdr_status ptdr_decompose_host(const ptdr_c128* A_host, int n, int structure,
  * of q are undefined (not checked on the device). */
 ptdr_status ptdr_coefficients_async(const ptdr_c128* A, int n, const uint64_t* qs, uint64_t count,
                                     ptdr_c128* out, void* stream);
+/* The same on rank `rank`'s X-mask shard A_local (the input of ptdr_decompose_xshard_async,
+ * [2^n][2^n / world]): qs are GLOBAL q indices; a string whose X-mask is not in the shard
+ * (x >> (n - log2 world) != rank) yields NaN.  bench.py's multi-GPU result check. */
+ptdr_status ptdr_coefficients_xshard_async(const ptdr_c128* A_local, int n, int rank, int world,
+                                           const uint64_t* qs, uint64_t count, ptdr_c128* out, void* stream);
 
 /* Batched small matrices (serving many decompositions per launch): A = [batch][2^n][2^n]
  * dense matrices of one structure stored back to back, out = [batch][4^n] coefficient
@@ -253,22 +272,36 @@ ptdr_status ptdr_hermitian_augment_async(const ptdr_c128* coeffs, int n, ptdr_c1
  * distribution, "a generic matrix", l.631).  Writes rows [row0, row0+nrows) of the
  * dense variant (0 GENERAL, 1 HERMITIAN, 2 REAL_SYMMETRIC) into A (row-major,
  * nrows x 2^n), entry = Philox4x32-10(counter = global element index) + Box-Muller.
- * Bitwise independent of the row split (any sharding sees the same matrix). */
+ * Bitwise independent of the row split (any sharding sees the same matrix).
+ * fro2_partials (nullable, device, ptdr_fro2_partial_count() doubles, 8-byte aligned):
+ * per-block partial sums of |a|^2 over the written elements -- their sum is ||A_rows||_F^2,
+ * the right-hand side of Parseval (Theorem 1, l.98-114: sum_P |alpha_P|^2 = ||A||_F^2 / 2^n)
+ * without another pass over A.  Deterministic; unused entries are 0. */
+size_t ptdr_fro2_partial_count(void);
 ptdr_status ptdr_generate_dense_async(int n, uint64_t seed, int variant, uint64_t row0,
-                                      uint64_t nrows, ptdr_c128* A, void* stream);
+                                      uint64_t nrows, ptdr_c128* A, double* fro2_partials, void* stream);
 
 /* Same generator for the band inputs: variant 3 (DIAGONAL) writes d[2^n] into
- * band; variant 4 (TRIDIAGONAL) writes the [3][2^n] sub/main/sup array. */
+ * band; variant 4 (TRIDIAGONAL) writes the [3][2^n] sub/main/sup array (sub[0] and
+ * sup[2^n-1] written as 0).  fro2_partials: as above, over the band's entries. */
 ptdr_status ptdr_generate_band_async(int n, uint64_t seed, int variant, ptdr_c128* band,
-                                     void* stream);
+                                     double* fro2_partials, void* stream);
 
-/* Same generator, but writes the column-block-major send layout used by the
- * multi-GPU all-to-all: for rank `rank` of `world`, R = 2^n/world, block b of
- * the output ([world][R][R]) holds rows rank*R.. of column block (rank ^ b),
- * i.e. send[b][r][c] = A[rank*R + r][(rank ^ b)*R + c].  Then a plain equal-split
- * all-to-all delivers exactly ptdr_decompose_xshard_async's A_local layout. */
-ptdr_status ptdr_generate_sendblocks_async(int n, uint64_t seed, int rank, int world,
-                                           ptdr_c128* send, void* stream);
+/* Same generator, but writes the send layout of the multi-GPU all-to-all for rank `rank`
+ * of `world` (R = 2^n / world), split into `subranges` = K (a power of two) sub-ranges of
+ * every rank's X-masks so the exchange of one sub-range can overlap the decomposition of
+ * the previous one.  Layout [K][world][K][R'][R'], R' = R / K:
+ * element (s, h, t, r', c') = A[(rank K + t) R' + r'][((rank ^ h) K + (t ^ s)) R' + c'].
+ * Slice s is one equal-split all-to-all; afterwards rank h holds, as a [2^n][R'] row-major
+ * array, exactly the A_local of ptdr_decompose_xshard_async(rank' = h K + s,
+ * world' = world K).  K = 1: send[h][r][c] = A[rank R + r][(rank ^ h) R + c].
+ * fro2_partials: as above, over the rank's row block. */
+ptdr_status ptdr_generate_sendblocks_async(int n, uint64_t seed, int rank, int world, int subranges,
+                                           ptdr_c128* send, double* fro2_partials, void* stream);
+
+/* Parseval's left-hand side: partials (device, ptdr_fro2_partial_count() doubles) receive
+ * per-block sums of |x_e|^2 over the `count` elements of x (deterministic). */
+ptdr_status ptdr_sumsq_async(const ptdr_c128* x, uint64_t count, double* partials, void* stream);
 
 /* ---- Host plans: streaming decomposition of matrices held in HOST memory ----------------
  * A plan owns `depth` (1..4) slots of device buffers for one (n, structure) -- input,

@@ -52,6 +52,10 @@ def lib():
         L.ptdr_workspace_bytes.restype = sz
         L.ptdr_decompose.argtypes = [vp, i32, i32, vp]
         L.ptdr_decompose_async.argtypes = [vp, i32, i32, vp, vp, sz, vp]
+        L.ptdr_inplace_workspace_bytes.argtypes = [i32, i32]
+        L.ptdr_inplace_workspace_bytes.restype = sz
+        L.ptdr_decompose_inplace_async.argtypes = [vp, i32, i32, vp, sz, vp]
+        L.ptdr_decompose_inplace_async.restype = i32
         L.ptdr_decompose_host.argtypes = [vp, i32, i32, vp]
         L.ptdr_decompose_xshard_async.argtypes = [vp, i32, i32, i32, vp, vp, sz, vp]
         L.ptdr_decompose_zshard_async.argtypes = [vp, i32, i32, i32, i32, vp, vp, sz, vp]
@@ -92,11 +96,16 @@ def lib():
         L.ptdr_decompose_generated_async.restype = i32
         L.ptdr_coefficients_async.argtypes = [vp, i32, vp, u64, vp, vp]
         L.ptdr_coefficients_async.restype = i32
+        L.ptdr_coefficients_xshard_async.argtypes = [vp, i32, i32, i32, vp, u64, vp, vp]
+        L.ptdr_coefficients_xshard_async.restype = i32
         L.ptdr_decompose_batched_async.argtypes = [vp, i32, i32, u64, vp, vp]
         L.ptdr_decompose_batched_async.restype = i32
-        L.ptdr_generate_dense_async.argtypes = [i32, u64, i32, u64, u64, vp, vp]
-        L.ptdr_generate_band_async.argtypes = [i32, u64, i32, vp, vp]
-        L.ptdr_generate_sendblocks_async.argtypes = [i32, u64, i32, i32, vp, vp]
+        L.ptdr_generate_dense_async.argtypes = [i32, u64, i32, u64, u64, vp, vp, vp]
+        L.ptdr_generate_band_async.argtypes = [i32, u64, i32, vp, vp, vp]
+        L.ptdr_generate_sendblocks_async.argtypes = [i32, u64, i32, i32, i32, vp, vp, vp]
+        L.ptdr_fro2_partial_count.restype = sz
+        L.ptdr_sumsq_async.argtypes = [vp, u64, vp, vp]
+        L.ptdr_sumsq_async.restype = i32
         L.ptdr_status_string.argtypes = [i32]
         L.ptdr_status_string.restype = ctypes.c_char_p
         L.ptdr_last_error.restype = ctypes.c_char_p
@@ -259,16 +268,37 @@ def _out(out, count, device, stream):
     return out
 
 
-def decompose(A, structure="general", out=None, workspace=None, stream=None):
+def decompose(A, structure="general", out=None, workspace=None, stream=None, inplace=False):
     """All Pauli coefficients of A (CUDA complex128) via ptdr_decompose_async.
 
     Dense structures: A is [2^n, 2^n]; DIAGONAL: d[2^n]; TRIDIAGONAL: [3, 2^n]
-    (sub, main, sup).  Returns `out` (q order, see include/ptdr.h)."""
+    (sub, main, sup).  Returns `out` (q order, see include/ptdr.h).
+
+    inplace=True (dense structures): A is overwritten with its coefficients in the matrix
+    layout A[z][z ^ x] = alpha(x, z) (ptdr_decompose_inplace_async; matrix_index maps a
+    string to its element) and A is returned -- no second 4^n buffer (n = 16 on one GPU
+    in 64 GiB + 2 GiB)."""
     import torch
 
     _require_cuda_c128(A, "A")
     s = _structure(structure)
     n = n_of(A, s)
+    if inplace:
+        if out is not None:
+            raise ValueError("inplace=True writes into A; do not pass out")
+        nb = int(lib().ptdr_inplace_workspace_bytes(n, s))
+        if nb == ctypes.c_size_t(-1).value:
+            raise PtdrError(PTDR_EINVAL, f"in-place decomposition needs a dense structure (got {structure!r})")
+        if workspace is None:
+            workspace = torch.empty(max(nb, 1), dtype=torch.uint8, device=A.device)
+            _keep_for_stream(stream, workspace)
+        else:
+            _require_workspace(workspace, nb, A.device)
+        _check(lib().ptdr_decompose_inplace_async(ctypes.c_void_p(A.data_ptr()), n, s,
+                                                  ctypes.c_void_p(workspace.data_ptr()),
+                                                  workspace.numel() * workspace.element_size(),
+                                                  _stream_ptr(stream)), "ptdr_decompose_inplace_async")
+        return A
     _require_cuda_c128(A, "A", input_count(n, s))
     out = _out(out, output_count(n, s), A.device, stream)
     workspace = _workspace(workspace, n, s, 1, A.device, stream)
@@ -389,6 +419,23 @@ def coefficients(A, qs, out=None, stream=None):
     _check(lib().ptdr_coefficients_async(ctypes.c_void_p(A.data_ptr()), n, ctypes.c_void_p(q.data_ptr()), q.numel(),
                                          ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)),
            "ptdr_coefficients_async")
+    return out
+
+
+def coefficients_xshard(A_local, n: int, rank: int, world: int, qs, out=None, stream=None):
+    """Selected coefficients (global q's of rank's X-mask shard) by Algorithm 2 on the shard
+    A_local [2^n, 2^n / world] (ptdr_coefficients_xshard_async); strings outside the shard
+    give NaN."""
+    import torch
+
+    _require_cuda_c128(A_local, "A_local", (1 << (2 * n)) // world)
+    q = torch.as_tensor(qs, dtype=torch.int64, device=A_local.device).contiguous()
+    _keep_for_stream(stream, q)
+    out = _out(out, q.numel(), A_local.device, stream)
+    _check(lib().ptdr_coefficients_xshard_async(ctypes.c_void_p(A_local.data_ptr()), n, rank, world,
+                                                ctypes.c_void_p(q.data_ptr()), q.numel(),
+                                                ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)),
+           "ptdr_coefficients_xshard_async")
     return out
 
 
@@ -653,8 +700,46 @@ def hermitian_augment(coeffs, out=None, stream=None):
 _DENSE_VARIANTS = {"general": 0, "hermitian": 1, "real_symmetric": 2}
 
 
+def fro2_partials(device=None):
+    """A zeroed device array for the ||.||_F^2 partials of the generators / sumsq."""
+    import torch
+
+    return torch.zeros(int(lib().ptdr_fro2_partial_count()), dtype=torch.float64, device=device or "cuda")
+
+
+def fro2_total(partials) -> float:
+    """Sum of the partials (copied to the host, exactly rounded sum: math.fsum)."""
+    import math
+
+    return math.fsum(partials.cpu().tolist())
+
+
+def sumsq(x, partials=None, stream=None) -> float:
+    """sum |x_e|^2 of a CUDA complex128 tensor by ptdr_sumsq_async (Parseval's left side)."""
+    _require_cuda_c128(x, "x")
+    if partials is None:
+        partials = fro2_partials(x.device)
+        _keep_for_stream(stream, partials)
+    _check(lib().ptdr_sumsq_async(ctypes.c_void_p(x.data_ptr()), x.numel(), ctypes.c_void_p(partials.data_ptr()),
+                                  _stream_ptr(stream)), "ptdr_sumsq_async")
+    return fro2_total(partials)
+
+
+def _fro2_ptr(fro2):
+    if fro2 is None:
+        return None
+    import torch
+
+    if not isinstance(fro2, torch.Tensor) or fro2.dtype != torch.float64 or not fro2.is_cuda or \
+            fro2.numel() < int(lib().ptdr_fro2_partial_count()):
+        raise ValueError("fro2 must be a CUDA float64 tensor of ptdr_fro2_partial_count() elements")
+    return ctypes.c_void_p(fro2.data_ptr())
+
+
 def generate_dense(n: int, seed: int, variant="general", row0: int = 0, nrows=None, out=None,
-                   device=None, stream=None):
+                   device=None, stream=None, fro2=None):
+    """Seeded dense input (row block [row0, row0 + nrows)); fro2 (optional, fro2_partials())
+    receives the ||A||_F^2 partials of the written rows."""
     import torch
 
     v = _DENSE_VARIANTS.get(variant, variant)
@@ -665,12 +750,12 @@ def generate_dense(n: int, seed: int, variant="general", row0: int = 0, nrows=No
         _keep_for_stream(stream, out)
     _require_cuda_c128(out, "out", nrows * N)
     st = lib().ptdr_generate_dense_async(n, seed, int(v), row0, nrows,
-                                         ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream))
+                                         ctypes.c_void_p(out.data_ptr()), _fro2_ptr(fro2), _stream_ptr(stream))
     _check(st, "ptdr_generate_dense_async")
     return out
 
 
-def generate_band(n: int, seed: int, variant="tridiagonal", out=None, device=None, stream=None):
+def generate_band(n: int, seed: int, variant="tridiagonal", out=None, device=None, stream=None, fro2=None):
     import torch
 
     v = _structure(variant)
@@ -679,24 +764,29 @@ def generate_band(n: int, seed: int, variant="tridiagonal", out=None, device=Non
         out = torch.empty(shape, dtype=torch.complex128, device=device or "cuda")
         _keep_for_stream(stream, out)
     _require_cuda_c128(out, "out", shape[0] if v == 3 else 3 << n)
-    st = lib().ptdr_generate_band_async(n, seed, v, ctypes.c_void_p(out.data_ptr()),
+    st = lib().ptdr_generate_band_async(n, seed, v, ctypes.c_void_p(out.data_ptr()), _fro2_ptr(fro2),
                                         _stream_ptr(stream))
     _check(st, "ptdr_generate_band_async")
     return out
 
 
 def generate_sendblocks(n: int, seed: int, rank: int, world: int, out=None, device=None,
-                        stream=None):
+                        stream=None, subranges: int = 1, fro2=None):
+    """Rank `rank`'s row block in the all-to-all send layout [K][world][K][R/K][R/K]
+    (K = subranges; include/ptdr.h ptdr_generate_sendblocks_async).  Returned as
+    [K, world, R/K * R] so that slice s is the contiguous equal-split send buffer of
+    sub-range s (K = 1: [1, world, R * R])."""
     import torch
 
     N = 1 << n
     R = N // world
+    K = subranges
     if out is None:
-        out = torch.empty((world, R, R), dtype=torch.complex128, device=device or "cuda")
+        out = torch.empty((K, world, R * R // K), dtype=torch.complex128, device=device or "cuda")
         _keep_for_stream(stream, out)
     _require_cuda_c128(out, "out", world * R * R)
-    st = lib().ptdr_generate_sendblocks_async(n, seed, rank, world,
-                                              ctypes.c_void_p(out.data_ptr()),
+    st = lib().ptdr_generate_sendblocks_async(n, seed, rank, world, K,
+                                              ctypes.c_void_p(out.data_ptr()), _fro2_ptr(fro2),
                                               _stream_ptr(stream))
     _check(st, "ptdr_generate_sendblocks_async")
     return out
@@ -710,6 +800,26 @@ def q_of(x: int, z: int, n: int) -> int:
         xl, zl = (x >> l) & 1, (z >> l) & 1
         q |= (2 * zl + (xl ^ zl)) << (2 * l)
     return q
+
+
+def matrix_index(x: int, z: int, n: int):
+    """(row, column) of coefficient (x, z) in the in-place matrix layout: (z, z ^ x)."""
+    return z, z ^ x
+
+
+def q_to_matrix_flat(q, n: int):
+    """Flat index z * 2^n + (z ^ x) of the in-place layout for q indices (numpy, vectorised)."""
+    import numpy as np
+
+    q = np.asarray(q, dtype=np.int64)
+    x = np.zeros_like(q)
+    z = np.zeros_like(q)
+    for l in range(n):
+        c = (q >> (2 * l)) & 3
+        zl = c >> 1
+        x |= ((c & 1) ^ zl) << l
+        z |= zl << l
+    return (z << n) | (z ^ x)
 
 
 def xz_of(q: int, n: int):

@@ -170,12 +170,13 @@ static DenseArgs base_args(const double2* A, double2* out, int n, void* ws) {
 
 static ptdr_status run_dense(const double2* A, int n, int s, double2* out, void* ws,
                              cudaStream_t st, int* nl, uint64_t lda = 0, uint64_t m = 0,
-                             uint64_t batch = 0) {
+                             uint64_t batch = 0, int layout_mat = 0) {
   const uint64_t N = 1ull << n;
   auto batched = [&](DenseArgs& a) {
     a.batch = batch;
     a.bstride_in = N * N;
     a.bstride_out = N * N;
+    a.layout_mat = layout_mat;
   };
   if (s == PTDR_GENERAL || n <= 8) {
     const int mode = s == PTDR_GENERAL ? MODE_GENERAL
@@ -385,7 +386,7 @@ ptdr_status ptdr_decompose_generated_async(int n, uint64_t seed, int rank, int w
   if (!generated_pipe(n, world)) {  // world == 1, small n
     const size_t ab = ((((size_t)16 << (2 * n)) + 255) / 256) * 256;
     double2* A = reinterpret_cast<double2*>(workspace);
-    cudaError_t e = launch_generate_dense(n, seed, 0, 0, N, A, st);
+    cudaError_t e = launch_generate_dense(n, seed, 0, 0, N, A, nullptr, st);
     if (e != cudaSuccess) return cuda_fail(e, "generator launch");
     ptdr_status r = ptdr_decompose_async(reinterpret_cast<const ptdr_c128*>(A), n, PTDR_GENERAL, out_local,
                                          reinterpret_cast<char*>(workspace) + ab, ws_bytes - ab, stream);
@@ -692,6 +693,63 @@ ptdr_status ptdr_decompose_padded_async(const ptdr_c128* A, uint64_t m, uint64_t
   return r;
 }
 
+// ---- in-place decomposition (BASELINE configs[4] "n=16 ... at 1 GPU in-place") --------
+// Output in the matrix layout A[z][z ^ x] = alpha(x, z).  Every kernel that reads all of an
+// X-mask's XOR-diagonal S_x = {(i, i ^ x)} before writing its coefficients -- and writes
+// them only into S_x -- runs in place: the pipeline and the v1 two-phase kernels per chunk
+// (phase B of a chunk starts after all its phase-A tiles), the whole-vector tiles per tile.
+// Only the direct kernel (one thread per coefficient, n <= 5) would race; there the
+// coefficients go through a workspace copy first (16 4^n bytes, at most 16 KiB).
+static bool inplace_via_copy(int n) { return n <= 5; }
+
+size_t ptdr_inplace_workspace_bytes(int n, int structure) {
+  if (!is_dense(structure) || !valid_n(n, structure)) return (size_t)-1;
+  const size_t base = ptdr_workspace_bytes(n, structure, 1);
+  return inplace_via_copy(n) ? pad_copy_bytes(n) + base : base;
+}
+
+__global__ void q_to_matrix_layout_kernel(const double2* __restrict__ Q, int n, double2* __restrict__ M) {
+  const uint64_t N = 1ull << n;
+  for (uint64_t id = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; id < N * N;
+       id += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t x = id >> n, z = id & (N - 1);
+    M[(z << n) | (z ^ x)] = Q[q_offset(x, z, n)];
+  }
+}
+
+ptdr_status ptdr_decompose_inplace_async(ptdr_c128* A, int n, int structure, void* workspace, size_t ws_bytes,
+                                         void* stream) {
+  g_last_launches = 0;
+  if (!is_dense(structure)) return fail(PTDR_EINVAL, "in-place decomposition is for the dense structures");
+  if (!valid_n(n, structure)) return fail(PTDR_EINVAL, "invalid n (1..16)");
+  if (!A || ((uintptr_t)A & 15)) return fail(PTDR_EINVAL, "null or misaligned A");
+  const size_t need = ptdr_inplace_workspace_bytes(n, structure);
+  if (need > 0 && (!workspace || ((uintptr_t)workspace & 255)))
+    return fail(PTDR_EINVAL, "workspace missing or not 256-byte aligned");
+  if (ws_bytes < need) return fail(PTDR_ENOMEM, "workspace too small");
+  if (need > 0 && overlaps(workspace, need, A, (size_t)16 << (2 * n)))
+    return fail(PTDR_EINVAL, "workspace overlaps A");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  double2* a = reinterpret_cast<double2*>(A);
+  int nl = 0;
+  ptdr_status r;
+  if (inplace_via_copy(n)) {
+    double2* Q = reinterpret_cast<double2*>(workspace);
+    const size_t cb = pad_copy_bytes(n);
+    r = run_dense(a, n, structure, Q, reinterpret_cast<char*>(workspace) + cb, st, &nl);
+    if (r != PTDR_OK) return r;
+    const uint64_t total = 1ull << (2 * n);
+    q_to_matrix_layout_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(Q, n, a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "layout kernel launch");
+    nl += 1;
+  } else {
+    r = run_dense(a, n, structure, a, workspace, st, &nl, 0, 0, 0, 1);
+  }
+  g_last_launches = nl;
+  return r;
+}
+
 // ---- selected coefficients (Algorithm 2 per string) ------------------------------------
 ptdr_status ptdr_coefficients_async(const ptdr_c128* A, int n, const uint64_t* qs, uint64_t count,
                                     ptdr_c128* out, void* stream) {
@@ -700,8 +758,23 @@ ptdr_status ptdr_coefficients_async(const ptdr_c128* A, int n, const uint64_t* q
   if (count == 0) return PTDR_OK;
   if (!A || !qs || !out) return fail(PTDR_EINVAL, "null pointer");
   if (((uintptr_t)A & 15) || ((uintptr_t)out & 15) || ((uintptr_t)qs & 7)) return fail(PTDR_EINVAL, "misaligned");
-  cudaError_t e = launch_coeffs(reinterpret_cast<const double2*>(A), n, qs, count, reinterpret_cast<double2*>(out),
-                                reinterpret_cast<cudaStream_t>(stream));
+  cudaError_t e = launch_coeffs(reinterpret_cast<const double2*>(A), n, 0, 1, qs, count,
+                                reinterpret_cast<double2*>(out), reinterpret_cast<cudaStream_t>(stream));
+  g_last_launches = 1;
+  return e == cudaSuccess ? PTDR_OK : cuda_fail(e, "coefficients launch");
+}
+
+ptdr_status ptdr_coefficients_xshard_async(const ptdr_c128* A_local, int n, int rank, int world, const uint64_t* qs,
+                                           uint64_t count, ptdr_c128* out, void* stream) {
+  g_last_launches = 0;
+  if (n < 1 || n > 16) return fail(PTDR_EINVAL, "invalid n (1..16)");
+  if (world < 1 || (world & (world - 1)) || (uint64_t)world > (1ull << n)) return fail(PTDR_EINVAL, "invalid world");
+  if (rank < 0 || rank >= world) return fail(PTDR_EINVAL, "rank out of range");
+  if (count == 0) return PTDR_OK;
+  if (!A_local || !qs || !out) return fail(PTDR_EINVAL, "null pointer");
+  if (((uintptr_t)A_local & 15) || ((uintptr_t)out & 15) || ((uintptr_t)qs & 7)) return fail(PTDR_EINVAL, "misaligned");
+  cudaError_t e = launch_coeffs(reinterpret_cast<const double2*>(A_local), n, rank, world, qs, count,
+                                reinterpret_cast<double2*>(out), reinterpret_cast<cudaStream_t>(stream));
   g_last_launches = 1;
   return e == cudaSuccess ? PTDR_OK : cuda_fail(e, "coefficients launch");
 }
@@ -802,42 +875,62 @@ ptdr_status ptdr_decompose_host(const ptdr_c128* A_host, int n, int structure,
   return r;
 }
 
+size_t ptdr_fro2_partial_count(void) { return (size_t)fro2_partial_count(); }
+
+static bool fro2_ok(const double* p) { return p == nullptr || ((uintptr_t)p & 7) == 0; }
+
 ptdr_status ptdr_generate_dense_async(int n, uint64_t seed, int variant, uint64_t row0,
-                                      uint64_t nrows, ptdr_c128* A, void* stream) {
+                                      uint64_t nrows, ptdr_c128* A, double* fro2_partials, void* stream) {
   g_last_launches = 0;
   if (n < 1 || n > 16 || variant < 0 || variant > 2) return fail(PTDR_EINVAL, "invalid n or variant");
   if (!A || ((uintptr_t)A & 15)) return fail(PTDR_EINVAL, "null or misaligned A");
+  if (!fro2_ok(fro2_partials)) return fail(PTDR_EINVAL, "misaligned fro2_partials");
   if (row0 + nrows > (1ull << n)) return fail(PTDR_EINVAL, "rows out of range");
   cudaError_t e = launch_generate_dense(n, seed, variant, row0, nrows, reinterpret_cast<double2*>(A),
-                                        reinterpret_cast<cudaStream_t>(stream));
+                                        fro2_partials, reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "generator launch");
   g_last_launches = nrows ? 1 : 0;
   return PTDR_OK;
 }
 
 ptdr_status ptdr_generate_band_async(int n, uint64_t seed, int variant, ptdr_c128* band,
-                                     void* stream) {
+                                     double* fro2_partials, void* stream) {
   g_last_launches = 0;
   if (n < 1 || n > 28 || (variant != 3 && variant != 4)) return fail(PTDR_EINVAL, "invalid n or variant");
   if (!band || ((uintptr_t)band & 15)) return fail(PTDR_EINVAL, "null or misaligned band");
-  cudaError_t e = launch_generate_band(n, seed, variant, reinterpret_cast<double2*>(band),
+  if (!fro2_ok(fro2_partials)) return fail(PTDR_EINVAL, "misaligned fro2_partials");
+  cudaError_t e = launch_generate_band(n, seed, variant, reinterpret_cast<double2*>(band), fro2_partials,
                                        reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "generator launch");
   g_last_launches = 1;
   return PTDR_OK;
 }
 
-ptdr_status ptdr_generate_sendblocks_async(int n, uint64_t seed, int rank, int world,
-                                           ptdr_c128* send, void* stream) {
+ptdr_status ptdr_generate_sendblocks_async(int n, uint64_t seed, int rank, int world, int subranges,
+                                           ptdr_c128* send, double* fro2_partials, void* stream) {
   g_last_launches = 0;
   if (n < 1 || n > 16 || world < 1 || (world & (world - 1)) || rank < 0 || rank >= world ||
       (uint64_t)world > (1ull << n))
     return fail(PTDR_EINVAL, "invalid n / rank / world");
+  if (subranges < 1 || (subranges & (subranges - 1)) || (uint64_t)world * (uint64_t)subranges > (1ull << n))
+    return fail(PTDR_EINVAL, "subranges must be a power of two with world * subranges <= 2^n");
   if (!send || ((uintptr_t)send & 15)) return fail(PTDR_EINVAL, "null or misaligned send buffer");
-  cudaError_t e = launch_generate_sendblocks(n, seed, rank, world, reinterpret_cast<double2*>(send),
-                                             reinterpret_cast<cudaStream_t>(stream));
+  if (!fro2_ok(fro2_partials)) return fail(PTDR_EINVAL, "misaligned fro2_partials");
+  cudaError_t e = launch_generate_sendblocks(n, seed, rank, world, subranges, reinterpret_cast<double2*>(send),
+                                             fro2_partials, reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "generator launch");
   g_last_launches = 1;
+  return PTDR_OK;
+}
+
+ptdr_status ptdr_sumsq_async(const ptdr_c128* x, uint64_t count, double* partials, void* stream) {
+  g_last_launches = 0;
+  if ((!x && count) || !partials) return fail(PTDR_EINVAL, "null pointer");
+  if (((uintptr_t)x & 15) || ((uintptr_t)partials & 7)) return fail(PTDR_EINVAL, "misaligned pointer");
+  cudaError_t e = launch_sumsq(reinterpret_cast<const double2*>(x), count, partials,
+                               reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "sumsq launch");
+  g_last_launches = count ? 1 : 0;
   return PTDR_OK;
 }
 

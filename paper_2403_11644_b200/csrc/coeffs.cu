@@ -10,8 +10,14 @@
 
 namespace ptdr {
 
-__global__ void __launch_bounds__(256) coeffs_kernel(const double2* __restrict__ A, int n, const u64* __restrict__ qs,
-                                                     u64 count, double2* __restrict__ out) {
+// A[i][j] at A + i * ld + (j & colmask): the dense matrix (ld = 2^n, colmask = 2^n - 1), or
+// rank `rank`'s X-mask shard after the all-to-all (ld = colmask + 1 = R: A_local[i][c] =
+// A[i][((i >> (n - g)) ^ rank) R + c], which holds A[i][i ^ x] at column (i ^ x) & (R - 1) for
+// every x of the shard).  Strings whose X-mask is outside the shard (x & ~colmask != xbase)
+// get NaN.
+__global__ void __launch_bounds__(256) coeffs_kernel(const double2* __restrict__ A, int n, u64 ld, u64 colmask,
+                                                     u64 xbase, const u64* __restrict__ qs, u64 count,
+                                                     double2* __restrict__ out) {
   const u64 N = 1ull << n;
   const int lane = threadIdx.x & 31;
   const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
@@ -25,10 +31,14 @@ __global__ void __launch_bounds__(256) coeffs_kernel(const double2* __restrict__
       z |= zl << l;
       x |= ((c & 1ull) ^ zl) << l;
     }
+    if ((x & ~colmask) != xbase) {
+      if (lane == 0) out[w] = make_double2(__longlong_as_double(0x7ff8000000000000ll), __longlong_as_double(0x7ff8000000000000ll));
+      continue;
+    }
     // lanes stride over i; each lane keeps a Kahan-free pairwise-ish partial sum
     double re = 0.0, im = 0.0;
     for (u64 i = (u64)lane; i < N; i += 32) {
-      const double2 v = ld_stream(A + i * N + (i ^ x));
+      const double2 v = ld_stream(A + i * ld + ((i ^ x) & colmask));
       if (__popcll(i & z) & 1) { re -= v.x; im -= v.y; }
       else { re += v.x; im += v.y; }
     }
@@ -45,13 +55,15 @@ __global__ void __launch_bounds__(256) coeffs_kernel(const double2* __restrict__
   }
 }
 
-cudaError_t launch_coeffs(const double2* A, int n, const uint64_t* qs, uint64_t count, double2* out,
-                          cudaStream_t st) {
+cudaError_t launch_coeffs(const double2* A, int n, int rank, int world, const uint64_t* qs, uint64_t count,
+                          double2* out, cudaStream_t st) {
   if (count == 0) return cudaSuccess;
   u64 g = (count * 32 + 255) / 256;
   const u64 cap = (u64)device_sm_count() * 16;
   if (g > cap) g = cap;
-  coeffs_kernel<<<(unsigned)g, 256, 0, st>>>(A, n, reinterpret_cast<const u64*>(qs), count, out);
+  const u64 R = (1ull << n) / (u64)world;
+  coeffs_kernel<<<(unsigned)g, 256, 0, st>>>(A, n, R, R - 1ull, world > 1 ? (u64)rank * R : 0ull,
+                                             reinterpret_cast<const u64*>(qs), count, out);
   return cudaGetLastError();
 }
 

@@ -53,7 +53,16 @@ struct DenseArgs {
   u64 cols_valid;      // 0 = all (the TMA tensor map fills the rest with zeros)
   unsigned long long* trace;  // pipeline debug timeline (nullptr unless PTDR_TRACE=1)
   double scale;        // 2^-n
+  int layout_mat;      // output layout: 0 = q order at q_offset(x, z, gshift); 1 = matrix
+                       //   layout out[z 2^n + (z ^ x)] (the in-place decomposition)
 };
+
+// Output index of coefficient (x, z).  The matrix layout puts alpha(x, z) where A[z][z ^ x]
+// was: the X-masks of a chunk occupy exactly the elements the chunk reads, so the pipeline
+// can overwrite A in place (ptdr_decompose_inplace_async, R12).
+__device__ __forceinline__ u64 out_index(const DenseArgs& a, u64 x, u64 z) {
+  return a.layout_mat ? ((z << a.n) | (z ^ x)) : q_offset(x, z, a.gshift);
+}
 
 // ---- loads: v_x[i] for the MODE -------------------------------------------------
 template <int MODE>
@@ -89,10 +98,10 @@ __device__ __forceinline__ void emit(const DenseArgs& a, u64 x, u64 zv, double2 
     double2 c = rot_ipow(w, __popcll(x & zv));
     c.x *= a.scale;
     c.y *= a.scale;
-    st_stream(a.out + q_offset(x, zv, a.gshift), c);
+    st_stream(a.out + out_index(a, x, zv), c);
   } else if constexpr (MODE == MODE_HERM_MIRROR || MODE == MODE_SYM_MIRROR) {
     double2 c = rot_ipow(w, __popcll(x & zv));
-    st_stream(a.out + q_offset(x, zv, a.gshift), make_double2(c.x * a.scale, 0.0));
+    st_stream(a.out + out_index(a, x, zv), make_double2(c.x * a.scale, 0.0));
   } else {
     const u64 z0 = insert0(zv, t);
     const u64 z1 = z0 | (1ull << t);
@@ -101,8 +110,8 @@ __device__ __forceinline__ void emit(const DenseArgs& a, u64 x, u64 zv, double2 
     const double sel0 = (p0 == 0) ? w.x : (p0 == 1) ? -w.y : (p0 == 2) ? -w.x : w.y;
     const int p1 = (p0 + 1) & 3;
     const double sel1 = (p1 == 0) ? w.x : (p1 == 1) ? -w.y : (p1 == 2) ? -w.x : w.y;
-    st_stream(a.out + q_offset(x, z0, a.gshift), make_double2(sel0 * s, 0.0));
-    st_stream(a.out + q_offset(x, z1, a.gshift), make_double2(sel1 * s, 0.0));
+    st_stream(a.out + out_index(a, x, z0), make_double2(sel0 * s, 0.0));
+    st_stream(a.out + out_index(a, x, z1), make_double2(sel1 * s, 0.0));
   }
 }
 

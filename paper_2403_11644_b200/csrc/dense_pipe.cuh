@@ -114,6 +114,13 @@ __device__ __forceinline__ uint32_t q_offset32(uint32_t x, uint32_t z, int gshif
 __device__ __forceinline__ uint32_t q_delta32(uint32_t x, int l, int gshift) {
   return (l < gshift) ? ((uint32_t)(3 - 2 * (int)((x >> l) & 1u)) << (2 * l)) : (1u << (l + gshift));
 }
+// Matrix layout (in-place decomposition): alpha(x, z) at z 2^n + (z ^ x); setting z bit l
+// adds 2^(l+n) and flips bit l of z ^ x (+2^l if x_l = 0, -2^l if x_l = 1).  n <= 16, so
+// every index fits 32 bits (mod-2^32 arithmetic handles the negative deltas).
+__device__ __forceinline__ uint32_t mat_offset32(uint32_t x, uint32_t z, int n) { return (z << n) | (z ^ x); }
+__device__ __forceinline__ uint32_t mat_delta32(uint32_t x, int l, int n) {
+  return (1u << (l + n)) + (((x >> l) & 1u) ? (0u - (1u << l)) : (1u << l));
+}
 __device__ __forceinline__ uint32_t insert0_32(uint32_t v, int t) {
   const uint32_t lo = v & ((1u << t) - 1u);
   return ((v >> t) << (t + 1)) | lo;
@@ -126,18 +133,19 @@ struct EpiUnit {
   uint32_t q0, p0, Dt;
   uint32_t D[NB];
   uint32_t P[NB];
-  __device__ __forceinline__ void init(uint32_t x, uint32_t zu, int base_pos, int t, int gshift) {
+  // mat_n = 0: q order (gshift: rank-local blocks); mat_n = n: matrix layout
+  __device__ __forceinline__ void init(uint32_t x, uint32_t zu, int base_pos, int t, int gshift, int mat_n) {
     const uint32_t zf = HALF ? insert0_32(zu, t) : zu;
-    q0 = q_offset32(x, zf, gshift);
+    q0 = mat_n ? mat_offset32(x, zf, mat_n) : q_offset32(x, zf, gshift);
     p0 = __popc(x & zf);
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       int l = base_pos + b;
       if (HALF) l += (l >= t) ? 1 : 0;
-      D[b] = q_delta32(x, l, gshift);
+      D[b] = mat_n ? mat_delta32(x, l, mat_n) : q_delta32(x, l, gshift);
       P[b] = (x >> l) & 1u;
     }
-    Dt = HALF ? q_delta32(x, t, gshift) : 0u;
+    Dt = HALF ? (mat_n ? mat_delta32(x, t, mat_n) : q_delta32(x, t, gshift)) : 0u;
   }
 };
 
@@ -717,7 +725,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
           const uint32_t phi = (uint32_t)m.tile * FB + (uint32_t)f;
           EpiUnit<R2, HALF> e;
           e.init((uint32_t)x0 + phi_u_of<XB>(phi), ((uint32_t)jl << R) | phi_zl_of<XB>(phi), R + 4, t,
-                 a.gshift);
+                 a.gshift, a.layout_mat ? a.n : 0);
           emit_all<MODE, R2>(a, e, w);
         };
         if constexpr (UB >= 2) {
@@ -747,7 +755,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
         if (lane == 0) mbar_arrive(&empty[s]);
         const uint32_t phi = (uint32_t)m.tile * FB + (uint32_t)f;
         EpiUnit<4, HALF> e;
-        e.init((uint32_t)x0 + phi_u_of<XB>(phi), phi_zl_of<XB>(phi), R, t, a.gshift);
+        e.init((uint32_t)x0 + phi_u_of<XB>(phi), phi_zl_of<XB>(phi), R, t, a.gshift, a.layout_mat ? a.n : 0);
         emit_all<MODE, 4>(a, e, v);
       } else {
         constexpr int R2 = M - 4;
@@ -779,7 +787,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
           pwht<R2>(&v[p * (1 << R2)]);
           EpiUnit<R2, HALF> e;
           e.init((uint32_t)x0 + phi_u_of<XB>(phi), ((uint32_t)jl << R) | phi_zl_of<XB>(phi), R + 4, t,
-                 a.gshift);
+                 a.gshift, a.layout_mat ? a.n : 0);
           emit_all<MODE, R2>(a, e, &v[p * (1 << R2)]);
         }
       }

@@ -48,15 +48,17 @@ cudaError_t launch_block_diag(const double2* blocks, int n, int k, double2* out,
 cudaError_t launch_herm_augment(const double2* a, int n, double2* out, cudaStream_t st);
 
 // selected coefficients (coeffs.cu)
-cudaError_t launch_coeffs(const double2* A, int n, const uint64_t* qs, uint64_t count, double2* out,
-                          cudaStream_t st);
+cudaError_t launch_coeffs(const double2* A, int n, int rank, int world, const uint64_t* qs, uint64_t count,
+                          double2* out, cudaStream_t st);
 
-// generators (generate.cu)
+// generators (generate.cu); fro2: nullable device array of fro2_partial_count() doubles
+int fro2_partial_count();
 cudaError_t launch_generate_dense(int n, uint64_t seed, int variant, uint64_t row0,
-                                  uint64_t nrows, double2* A, cudaStream_t st);
-cudaError_t launch_generate_band(int n, uint64_t seed, int variant, double2* band,
+                                  uint64_t nrows, double2* A, double* fro2, cudaStream_t st);
+cudaError_t launch_generate_band(int n, uint64_t seed, int variant, double2* band, double* fro2,
                                  cudaStream_t st);
-cudaError_t launch_generate_sendblocks(int n, uint64_t seed, int rank, int world, double2* send,
-                                       cudaStream_t st);
+cudaError_t launch_generate_sendblocks(int n, uint64_t seed, int rank, int world, int K, double2* send,
+                                       double* fro2, cudaStream_t st);
+cudaError_t launch_sumsq(const double2* x, uint64_t count, double* partials, cudaStream_t st);
 
 }  // namespace ptdr

@@ -17,32 +17,78 @@ import torch.distributed as dist
 from . import decompose_xshard, decompose_zshard, q_of
 
 
+def _nvtx(name):
+    """NVTX range (for nsys timelines of the exchange / kernel overlap); no-op without CUDA."""
+    import contextlib
+
+    if torch.cuda.is_available():
+        return torch.cuda.nvtx.range(name)
+    return contextlib.nullcontext()
+
+
 def exchange(send: torch.Tensor, group=None, recv: torch.Tensor | None = None) -> torch.Tensor:
-    """Equal-split all-to-all of the [world][R][R] send blocks.
+    """Equal-split all-to-all of the send blocks (one sub-range: send is [world][R*R] or
+    [1][world][R*R]).
 
     Rank h receives block h of every rank g: recv[g][r][c] = A[g*R + r][(g ^ h)*R + c],
     which read as a [2^n][R] row-major array is A_local[i][c] = A[i][((i >> (n-log2 world)) ^ h)*R + c].
     """
     if recv is None:
         recv = torch.empty_like(send)
-    dist.all_to_all_single(recv.view(-1), send.contiguous().view(-1), group=group)
+    with _nvtx("ptdr.exchange"):
+        dist.all_to_all_single(recv.view(-1), send.contiguous().view(-1), group=group)
     return recv
+
+
+def exchange_async(send: torch.Tensor, group=None, recv: torch.Tensor | None = None):
+    """Issue the K sub-range all-to-alls of a [K][world][R*R/K] send layout at once
+    (async_op=True); returns (recv, works).  works[s].wait() orders sub-range s."""
+    if send.dim() == 2:
+        send = send.unsqueeze(0)
+    if recv is None:
+        recv = torch.empty_like(send)
+    with _nvtx("ptdr.exchange.issue"):
+        works = [dist.all_to_all_single(recv[s].view(-1), send[s].contiguous().view(-1), group=group,
+                                        async_op=True) for s in range(send.shape[0])]
+    return recv, works
 
 
 def decompose_sharded(send: torch.Tensor, n: int, group=None, out=None, recv=None, workspace=None,
                       stream=None) -> torch.Tensor:
-    """All-to-all + per-rank decomposition.  Returns the rank-local coefficients
-    (4^n / world, ordering in include/ptdr.h ptdr_decompose_xshard_async)."""
+    """All-to-all + per-rank decomposition, overlapped by sub-range.
+
+    send: the [K][world][R*R/K] layout of generate_sendblocks(..., subranges=K).  Sub-range
+    s of every rank's X-masks is one equal-split all-to-all; all K are issued up front
+    (asynchronous on NCCL's stream) and the decomposition of sub-range s -- which is
+    ptdr_decompose_xshard_async for virtual rank h K + s of world K -- starts as soon as
+    its exchange has landed, while the exchanges of the later sub-ranges are in flight.
+    Returns [K][4^n / (world K)]: sub-output s in the layout of virtual rank h K + s
+    (global_q_sub).  K = 1 is the plain exchange-then-decompose path.
+    """
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    recv = exchange(send, group, recv)
-    if stream is not None:
-        # all_to_all_single is ordered on the current stream only: make `stream` wait for
-        # the exchange before the kernels read `recv` (ADVICE r01)
-        stream.wait_stream(torch.cuda.current_stream(send.device))
+    if send.dim() == 2:
+        send = send.unsqueeze(0)
+    K = send.shape[0]
+    if recv is None:
+        recv = torch.empty_like(send)
     N = 1 << n
-    return decompose_xshard(recv.view(N, N // world), n, rank, world, out=out,
-                            workspace=workspace, stream=stream)
+    Rk = N // world // K
+    if out is None:
+        out = torch.empty((K, (1 << (2 * n)) // (world * K)), dtype=torch.complex128, device=send.device)
+    cur = torch.cuda.current_stream(send.device) if send.is_cuda else None
+    recv, works = exchange_async(send, group, recv)
+    for s in range(K):
+        with _nvtx(f"ptdr.exchange.wait[{s}]"):
+            works[s].wait()          # NCCL: the current stream waits for exchange s
+        if stream is not None and cur is not None:
+            # all_to_all_single is ordered on the current stream only: make `stream` wait
+            # for the exchange before the kernels read `recv` (ADVICE r01)
+            stream.wait_stream(cur)
+        with _nvtx(f"ptdr.decompose_xshard[{s}]"):
+            decompose_xshard(recv[s].view(N, Rk), n, rank * K + s, world * K, out=out[s],
+                             workspace=workspace, stream=stream)
+    return out
 
 
 def global_q(rank: int, local_index: int, n: int, world: int) -> int:
@@ -51,6 +97,12 @@ def global_q(rank: int, local_index: int, n: int, world: int) -> int:
     w = 2 * (n - g)
     zt = local_index >> w
     return (q_of(rank, zt, g) << w) | (local_index & ((1 << w) - 1))
+
+
+def global_q_sub(rank: int, s: int, local_index: int, n: int, world: int, subranges: int) -> int:
+    """Global q of element `local_index` of sub-output s of decompose_sharded (virtual rank
+    rank * K + s of world * K)."""
+    return global_q(rank * subranges + s, local_index, n, world * subranges)
 
 
 def global_q_array(rank: int, n: int, world: int):
@@ -63,6 +115,25 @@ def global_q_array(rank: int, n: int, world: int):
     zt = local >> w
     top = np.array([q_of(rank, int(v), g) for v in range(1 << g)], dtype=np.int64)
     return (top[zt] << w) | (local & ((1 << w) - 1))
+
+
+def sendblocks_host(rows, n: int, rank: int, world: int, subranges: int = 1):
+    """Host (numpy) copy of the send layout of ptdr_generate_sendblocks_async for a rank's
+    row block `rows` ([R][2^n]), for tests of the exchange plumbing without a GPU:
+    element (s, h, t, r', c') = A[(rank K + t) R' + r'][((rank ^ h) K + (t ^ s)) R' + c']."""
+    import numpy as np
+
+    N = 1 << n
+    K = subranges
+    R = N // world
+    Rp = R // K
+    out = np.empty((K, world, K, Rp, Rp), dtype=rows.dtype)
+    for s in range(K):
+        for h in range(world):
+            for t in range(K):
+                c0 = ((rank ^ h) * K + (t ^ s)) * Rp
+                out[s, h, t] = rows[t * Rp:(t + 1) * Rp, c0:c0 + Rp]
+    return out.reshape(K, world, K * Rp * Rp)
 
 
 # ---- structured (DIAGONAL / TRIDIAGONAL): replicated band, z-sharded output -------------

@@ -70,3 +70,15 @@ def test_host_entry_validates_sizes_before_the_abi_call():
         ptdr.decompose_host(np.zeros(3 * 8 + 1, dtype=np.complex128), "tridiagonal")
     with pytest.raises(TypeError):
         ptdr.decompose_host(np.zeros((4, 4), dtype=np.complex64))
+
+
+def test_matrix_layout_index_is_a_permutation():
+    """The in-place layout puts alpha(x, z) at A[z][z ^ x]: a bijection of the 4^n slots,
+    and the flat map agrees with matrix_index."""
+    for n in (1, 3, 5):
+        flat = ptdr.q_to_matrix_flat(np.arange(4 ** n), n)
+        assert sorted(flat.tolist()) == list(range(4 ** n))
+        for q in range(0, 4 ** n, 7):
+            x, z = ptdr.xz_of(q, n)
+            r, c = ptdr.matrix_index(x, z, n)
+            assert flat[q] == r * (1 << n) + c and (r ^ c) == x

@@ -42,6 +42,7 @@ def _worker(rank, world, port, n, result_q):
         rows = ptdr_inputs.dense(n, 4, "general", row0=rank * R, nrows=R)
         # send layout [world][R][R]: block b = my rows x column block (rank ^ b)
         send = np.stack([rows[:, (rank ^ b) * R:((rank ^ b) + 1) * R] for b in range(world)])
+        assert np.array_equal(send.reshape(-1), pdist.sendblocks_host(rows, n, rank, world).reshape(-1))
         send_t = torch.from_numpy(np.ascontiguousarray(send))
         recv = pdist.exchange(send_t)
         local = recv.numpy().reshape(N, R)
@@ -201,3 +202,66 @@ def test_peer_handle_exchange(world):
         for r, pt in enumerate(ptrs):
             want = 0xDEAD0000 if r == rank else 0x7000_0000_0000 + (r << 32) + 4096 * r + 16
             assert pt == want
+
+
+def _subrange_worker(rank, world, port, n, K, result_q):
+    """Sub-range overlapped exchange (dist.exchange_async): every one of the K equal-split
+    all-to-alls must deliver exactly the A_local of virtual rank rank*K + s of world*K (the
+    input contract of ptdr_decompose_xshard_async), so the K decompositions can start one
+    by one as their sub-range lands."""
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import ptdr_inputs
+        from paper_2403_11644_b200 import dist as pdist
+        from paper_2403_11644_b200 import xz_of
+
+        N = 1 << n
+        R = N // world
+        Rp = R // K
+        gv = (world * K).bit_length() - 1
+        rows = ptdr_inputs.dense(n, 4, "general", row0=rank * R, nrows=R)
+        send = torch.from_numpy(np.ascontiguousarray(pdist.sendblocks_host(rows, n, rank, world, K)))
+        recv, works = pdist.exchange_async(send)
+        A = ptdr_inputs.dense(n, 4, "general")
+        ok = True
+        allq = []
+        for s in range(K):
+            works[s].wait()
+            local = recv[s].numpy().reshape(N, Rp)
+            v = rank * K + s
+            for i in range(N):
+                blk = (i >> (n - gv)) ^ v
+                ok &= np.array_equal(local[i], A[i, blk * Rp:(blk + 1) * Rp])
+            # sub-output s covers exactly the X-masks of virtual rank v
+            for li in range(0, (1 << (2 * n)) // (world * K), 7):
+                q = pdist.global_q_sub(rank, s, li, n, world, K)
+                x, _ = xz_of(q, n)
+                ok &= (x >> (n - gv)) == v
+                allq.append(q)
+        result_q.put((rank, bool(ok), allq))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n,K", [(2, 6, 2), (2, 6, 4), (4, 7, 2)])
+def test_subrange_exchange_contract(world, n, K):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_subrange_worker, args=(r, world, port, n, K, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    allq = []
+    for rank, ok, qs in sorted(results):
+        assert ok, f"rank {rank}: sub-range exchange contract failed"
+        allq += qs
+    assert len(set(allq)) == len(allq)

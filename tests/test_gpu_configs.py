@@ -95,39 +95,94 @@ def test_large_configs_sampled(gpu, cfg):
                 assert v == 0
 
 
-@pytest.mark.parametrize("variant", ["tridiagonal", "diagonal"])
+def _support_x(variant, n, b):
+    """X-mask of output block b (include/ptdr.h): tridiagonal 2^b - 1, diagonal 0,
+    anti-diagonal 2^n - 1."""
+    return {"tridiagonal": (1 << b) - 1, "diagonal": 0, "anti_diagonal": (1 << n) - 1}[variant]
+
+
+def _outside_support(variant, n, rng, count):
+    """(x, z) pairs whose X-mask is NOT an output block: by Table I (l.511/l.513) and the
+    anti-diagonal remark (l.391-392) their coefficient is exactly 0."""
+    inside = {_support_x(variant, n, b) for b in range(n + 1 if variant == "tridiagonal" else 1)}
+    xs = [x for x in (1, 2, 5, (1 << n) - 2, 1 << (n - 1)) if x not in inside]
+    while len(xs) < count:
+        x = int(rng.integers(0, 1 << n))
+        if x not in inside:
+            xs.append(x)
+    zs = rng.integers(0, 1 << n, len(xs))
+    return np.array([ptdr.q_of(int(x), int(z), n) for x, z in zip(xs, zs)], dtype=np.uint64)
+
+
+@pytest.mark.parametrize("variant", ["tridiagonal", "diagonal", "anti_diagonal"])
 def test_n24_band_sampled(gpu, variant):
+    """BASELINE configs[3] (n = 24, seed 3): SURVEY 8(c) item 15 -- 4096 seeded in-block
+    coefficients against the oracle, 64 out-of-block strings whose oracle value is exactly
+    0 (the omitted blocks are the zero blocks), and Parseval over the whole output."""
     torch = _torch()
     n, seed = 24, 3
-    band = ptdr.generate_band(n, seed, variant)
+    gen_variant = "diagonal" if variant == "anti_diagonal" else variant
+    band = ptdr.generate_band(n, seed, gen_variant)
     out = ptdr.decompose(band, variant)
     torch.cuda.synchronize()
-    rel = _parseval_gpu(band, out, n) if variant == "diagonal" else None
-    if variant == "tridiagonal":
-        # ||A||_F^2 = sum |main|^2 + sum |sup|^2 + sum |sub|^2
-        lhs = _sumsq(out)
-        rhs = _sumsq(band) / (1 << n)
-        rel = abs(lhs - rhs) / rhs
+    # ||A||_F^2 = sum over the stored band (tridiagonal: sub, main and sup, whose unused
+    # ends sub[0] and sup[2^n - 1] the generator writes as 0)
+    rel = abs(_sumsq(out) - _sumsq(band) / (1 << n)) / (_sumsq(band) / (1 << n))
     assert rel < 1e-11
-    rng = np.random.default_rng(24)
+    rng = np.random.default_rng(24 + len(variant))
     nb = n + 1 if variant == "tridiagonal" else 1
-    blocks = rng.integers(0, nb, 192)
-    zs = rng.integers(0, 1 << n, 192)
+    blocks = np.concatenate([np.arange(nb), rng.integers(0, nb, 4096 - nb)])
+    zs = np.concatenate([np.full(nb, (1 << n) - 1), rng.integers(0, 1 << n, 4096 - nb)])
     idx = blocks * (1 << n) + zs
     got = out[torch.from_numpy(idx.astype(np.int64)).cuda()].cpu().numpy()
     del out, band
     torch.cuda.empty_cache()
-    qs = np.array([ptdr.q_of((1 << int(b)) - 1, int(z), n) for b, z in zip(blocks, zs)],
+    qs = np.array([ptdr.q_of(_support_x(variant, n, int(b)), int(z), n) for b, z in zip(blocks, zs)],
                   dtype=np.uint64)
+    qout = _outside_support(variant, n, rng, 64)
+    assert qout.size == 64
     if variant == "tridiagonal":
         sub, main, sup = ptdr_inputs.band(n, seed, variant)
         want = oracle.coeffs_tridiagonal(sub, main, sup, qs)
+        zero = oracle.coeffs_tridiagonal(sub, main, sup, qout)
         maxabs = max(np.max(np.abs(main)), np.max(np.abs(sup)))
     else:
-        d = ptdr_inputs.band(n, seed, variant)
-        want = oracle.coeffs_diagonal(d, qs)
+        d = ptdr_inputs.band(n, seed, "diagonal")
+        fn = oracle.coeffs_diagonal if variant == "diagonal" else oracle.coeffs_antidiagonal
+        want = fn(d, qs)
+        zero = fn(d, qout)
         maxabs = np.max(np.abs(d))
     assert np.max(np.abs(got - want)) <= TOL * maxabs
+    assert np.all(zero == 0)
+
+
+@pytest.mark.parametrize("variant", ["hermitian", "real_symmetric"])
+def test_n13_complete_xmask_blocks(gpu, variant):
+    """BASELINE configs[2] (n = 13, seed 2).  The full oracle over all 4^13 strings takes
+    about an hour on 16 host cores (1.8e4-3.3e4 coefficients/s), so
+    besides the 4096 samples of test_large_configs_sampled this checks COMPLETE X-mask
+    blocks -- every one of the 2^13 Z-masks -- for the X-masks of every kernel regime
+    (x = 0 and the mirrored launch's small x, half-length chunks at the top bit boundaries,
+    x = 2^13 - 1, and random ones): DESIGN.md reading R19."""
+    torch = _torch()
+    n, seed = 13, 2
+    N = 1 << n
+    A = ptdr.generate_dense(n, seed, variant)
+    out = ptdr.decompose(A, variant)
+    torch.cuda.synchronize()
+    maxabs = torch.max(torch.abs(A)).item()
+    del A
+    rng = np.random.default_rng(1313)
+    xs = [0, 1, 15, 16, 31, 32, 1 << 12, (1 << 12) + 1, N - 1] + [int(v) for v in rng.integers(0, N, 3)]
+    z = np.arange(N)
+    for x in xs:
+        qs = np.array([ptdr.q_of(x, int(zz), n) for zz in z], dtype=np.uint64)
+        got = out[torch.from_numpy(qs.astype(np.int64)).cuda()].cpu().numpy()
+        want = oracle.coeffs_generated(n, seed, ptdr_inputs.VARIANTS[variant], qs)
+        assert np.max(np.abs(got - want)) <= TOL * maxabs, x
+        assert np.all(got.imag == 0)
+    del out
+    torch.cuda.empty_cache()
 
 
 @pytest.mark.parametrize("n,world", [(10, 2), (10, 4), (12, 8), (8, 2), (6, 4), (11, 2), (13, 8), (14, 4)])
@@ -141,7 +196,7 @@ def test_xshard_emulated_bitwise(gpu, n, world):
     full = np.empty(4 ** n, dtype=np.complex128)
     for h in range(world):
         # emulate the equal-split all-to-all: rank h receives block h of every rank
-        recv = torch.stack([sends[g][h] for g in range(world)]).contiguous()
+        recv = torch.stack([sends[g][0, h] for g in range(world)]).contiguous()
         out = ptdr.decompose_xshard(recv.view(N, R), n, h, world).cpu().numpy()
         full[pdist.global_q_array(h, n, world)] = out
     if n >= 8:   # same two-phase schedule on every rank -> bitwise identical

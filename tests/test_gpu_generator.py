@@ -42,7 +42,48 @@ def test_sendblocks_layout(gpu, world):
     N, R = 1 << n, (1 << n) // world
     A = ptdr.generate_dense(n, 4, "general").cpu().numpy()
     for rank in range(world):
-        s = ptdr.generate_sendblocks(n, 4, rank, world).cpu().numpy()
+        s = ptdr.generate_sendblocks(n, 4, rank, world).cpu().numpy().reshape(world, R, R)
         for b in range(world):
             want = A[rank * R:(rank + 1) * R, (rank ^ b) * R:((rank ^ b) + 1) * R]
             assert np.array_equal(s[b], want)
+
+
+@pytest.mark.parametrize("world,K", [(2, 2), (2, 4), (4, 2), (8, 4), (1, 4)])
+def test_sendblocks_subrange_layout(gpu, world, K):
+    """[K][world][K][R'][R'] layout: element (s, h, t, r', c') =
+    A[(rank K + t) R' + r'][((rank ^ h) K + (t ^ s)) R' + c'] (include/ptdr.h)."""
+    n = 9
+    N, R = 1 << n, (1 << n) // world
+    Rp = R // K
+    A = ptdr.generate_dense(n, 4, "general").cpu().numpy()
+    for rank in range(world):
+        s = ptdr.generate_sendblocks(n, 4, rank, world, subranges=K).cpu().numpy()
+        s = s.reshape(K, world, K, Rp, Rp)
+        for sr in range(K):
+            for h in range(world):
+                for t in range(K):
+                    r0 = (rank * K + t) * Rp
+                    c0 = ((rank ^ h) * K + (t ^ sr)) * Rp
+                    assert np.array_equal(s[sr, h, t], A[r0:r0 + Rp, c0:c0 + Rp])
+
+
+@pytest.mark.parametrize("variant", ["general", "hermitian", "real_symmetric"])
+def test_generator_fro2_partials(gpu, variant):
+    """The fused ||A||_F^2 partials equal a sum over the written matrix (and a row block)."""
+    import torch
+
+    n = 11
+    f = ptdr.fro2_partials()
+    A = ptdr.generate_dense(n, 4, variant, fro2=f)
+    want = float(torch.sum(torch.abs(A) ** 2).item())
+    assert abs(ptdr.fro2_total(f) - want) <= 1e-12 * want
+    assert abs(ptdr.sumsq(A) - want) <= 1e-12 * want
+    part = ptdr.generate_dense(n, 4, variant, row0=64, nrows=100, fro2=f)
+    want = float(torch.sum(torch.abs(part) ** 2).item())
+    assert abs(ptdr.fro2_total(f) - want) <= 1e-12 * want
+    B = ptdr.generate_band(12, 3, "tridiagonal", fro2=f)
+    want = float(torch.sum(torch.abs(B) ** 2).item())
+    assert abs(ptdr.fro2_total(f) - want) <= 1e-12 * want
+    S = ptdr.generate_sendblocks(10, 4, 1, 4, subranges=2, fro2=f)
+    want = float(torch.sum(torch.abs(S) ** 2).item())
+    assert abs(ptdr.fro2_total(f) - want) <= 1e-12 * want

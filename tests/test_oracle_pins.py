@@ -369,3 +369,57 @@ def test_band_xmask_set_and_count(s, n):
     L = int(np.floor(np.log2(s)))
     cs = s * (L + 1) - (1 << (L + 1))
     assert len(want) == s * n - cs
+
+
+# ---- the oracle's compensated trace (R7: mandatory at n >= 16) ---------------------
+def test_neumaier_trace_small_exact():
+    """Tr of diag(1, 1e16, 1, -1e16) is 2: plain left-to-right double summation returns 0
+    (1e16 + 1 rounds to 1e16), a dropped compensation term returns 0, and swapping the two
+    branches of the compensation update loses a unit as well.  The oracle must give the
+    exact 2 / 2^n for II and IZ (z = 1: signs +,-,+,- of the same entries in reverse)."""
+    d = np.array([1.0, 1e16, 1.0, -1e16])
+    assert ((1.0 + 1e16) + 1.0) - 1e16 == 0.0  # the naive sum of the same order fails
+    out = oracle.decompose(np.diag(d).astype(np.complex128))
+    assert out[0] == 0.5                        # II: (1 + 1e16 + 1 - 1e16) / 4
+    d2 = np.array([1.0, -1e16, 1.0, 1e16])      # IZ trace: 1 + 1e16 + 1 - 1e16 with signs folded in
+    out2 = oracle.decompose(np.diag(d2).astype(np.complex128))
+    assert out2[3] == 0.5
+    # the imaginary accumulator is compensated too
+    out3 = oracle.decompose(np.diag(1j * d).astype(np.complex128))
+    assert out3[0] == 0.5j
+
+
+def test_neumaier_trace_adversarial_2pow16():
+    """A 2^16-term trace whose partial sums reach ~1e18 while the exact total (checked with
+    fractions.Fraction) is the sum of the small terms alone: naive summation loses all of
+    them, the oracle's Neumaier sum stays within the compensated bound n u^2 sum|x|."""
+    from fractions import Fraction
+
+    n = 16
+    N = 1 << n
+    rng = np.random.default_rng(1616)
+
+    def adversarial():
+        big = rng.integers(1, 1 << 20, N // 4).astype(np.float64) * 2.0 ** 33   # ~1e16
+        big *= rng.choice([-1.0, 1.0], big.size)
+        small = rng.random(N // 2)
+        # first half: +big interleaved with small terms; second half: -big (shuffled)
+        # interleaved with small terms -> the bigs cancel exactly in the true sum
+        first = np.empty(N // 2)
+        first[0::2], first[1::2] = big, small[: N // 4]
+        second = np.empty(N // 2)
+        second[0::2], second[1::2] = -rng.permutation(big), small[N // 4:]
+        return np.concatenate([first, second])
+
+    re, im = adversarial(), adversarial()
+    exact_re = sum(Fraction(float(v)) for v in re)
+    exact_im = sum(Fraction(float(v)) for v in im)
+    naive_re = 0.0
+    for v in re:
+        naive_re += v
+    bound_re = N * (2.0 ** -53) ** 2 * float(np.sum(np.abs(re))) + 2.0 ** -52 * abs(float(exact_re))
+    bound_im = N * (2.0 ** -53) ** 2 * float(np.sum(np.abs(im))) + 2.0 ** -52 * abs(float(exact_im))
+    assert abs(naive_re - float(exact_re)) > 1e3 * bound_re   # the input defeats plain summation
+    got = oracle.coeffs_diagonal(re + 1j * im, np.array([0], dtype=np.uint64))[0] * N
+    assert abs(Fraction(got.real) - exact_re) <= Fraction(bound_re)
+    assert abs(Fraction(got.imag) - exact_im) <= Fraction(bound_im)

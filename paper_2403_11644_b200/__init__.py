@@ -243,7 +243,7 @@ def alloc_workspace(n: int, structure="general", world: int = 1, device=None):
 
     nb = workspace_bytes(n, structure, world)
     # torch's caching allocator returns >= 512-byte aligned blocks
-    return torch.empty(max(nb, 1), dtype=torch.uint8, device=device)
+    return torch.empty(max(nb, 1), dtype=torch.uint8, device=device if device is not None else "cuda")
 
 
 def _workspace(workspace, n, structure, world, device, stream):

@@ -23,6 +23,10 @@
 
 namespace ptdr {
 
+// Vectors of at least 2^kTopMin elements run their three top butterfly levels first (the
+// z-sharded paths read them once and transform only the rank's part; see top3_pass_kernel).
+constexpr int kTopMin = 15;
+
 // ---- flat WHT pass over bits [b0, b0+K) of a contiguous array ---------------------
 template <int K>
 struct FlatLd {
@@ -44,9 +48,9 @@ __device__ __forceinline__ bool in_slice(u64 e, int zshift, u64 zrank) { return 
 // i^{popcount(px & z)} of a fixed X-mask px (ANTI_DIAGONAL: px = 2^n - 1; 0 otherwise) and the
 // slice filter.
 __device__ __forceinline__ void store_final(double2* out, u64 e, double2 v, double scale, int zshift,
-                                            u64 zrank, u64 px) {
+                                            u64 zrank, u64 px, u64 zoff = 0) {
   if (!in_slice(e, zshift, zrank)) return;
-  if (px) v = rot_ipow(v, __popcll(px & e));
+  if (px) v = rot_ipow(v, __popcll(px & (e + zoff)));
   st_l2(out + (e - (zrank << zshift)), make_double2(v.x * scale, v.y * scale));
 }
 
@@ -59,10 +63,11 @@ struct FlatSt {
   int zshift;
   u64 zrank;
   u64 px;
+  u64 zoff;
   __device__ __forceinline__ void operator()(int f, int j, double2 v) const {
     const u64 rho = rbase + (u64)f;
     const u64 e = ((rho >> b0) << (b0 + K)) | ((u64)j << b0) | (rho & ((1ull << b0) - 1ull));
-    store_final(out, e, v, scale, zshift, zrank, px);
+    store_final(out, e, v, scale, zshift, zrank, px, zoff);
   }
 };
 
@@ -110,33 +115,31 @@ __device__ __forceinline__ void contig8_tile(double2* S, const double2* in, doub
   }
 }
 
-// ---- tridiagonal split: (S_t, U_t) -> (S_t + U_t, S_t - U_t) compacted per t --------
-// One thread per super-diagonal index i (coalesced reads of sup[i] and sub[i+1]): i has t
-// trailing ones, b_h = i with h = i >> (t+1), S_t[h] = sup[i], U_t[h] = sub[i+1].
-__global__ void tridiag_split_kernel(const double2* band, double2* PM, int n) {
-  const u64 N = 1ull << n;
-  const double2* sub = band;
-  const double2* sup = band + 2 * N;
-  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < N - 1;
-       i += (u64)gridDim.x * blockDim.x) {
-    const int t = __ffsll((long long)~i) - 1;  // trailing ones of i (i < N-1 so t <= n-1)
-    const int lam = n - t - 1;
-    const u64 seg = N - (N >> t);
-    const u64 h = i >> (t + 1);
-    const double2 s = ld_stream(sup + i);
-    const double2 u = ld_stream(sub + i + 1);
-    PM[2 * seg + h] = cadd(s, u);
-    PM[2 * seg + (1ull << lam) + h] = csub(s, u);
-  }
-}
-
 // ---- tridiagonal expansion into blocks 1..n (write-bound) ------------------------------
 // Each thread writes 8 outputs of one block at z = base + lane + 32 k (512 B per warp store);
 // the P/M values (reused 2^(t+1) times) come through the read-only cache.
 // z-sharded (world > 1): only z in [zrank 2^zshift, (zrank+1) 2^zshift) of each block, stored
 // block-major with 2^zshift outputs per block (block 0 is written by the WHT passes).
+// Segment t's P/M values for zh (long segments, lam >= kTopMin: the KS kept top-bit branches
+// of the rank, stored compactly, local index zh mod KS 2^(lam-3); short ones: full vectors).
+struct SegView {
+  const double2* P;
+  const double2* M;
+  u64 mask;
+};
+__device__ __forceinline__ SegView seg_view(const double2* PM, int n, int t, int k_keep) {
+  const u64 N = 1ull << n;
+  const int lam = n - t - 1;
+  const double2* Pt = PM + 2 * (N - (N >> t));
+  if (lam >= kTopMin) {
+    const u64 len = 1ull << (lam - 3 + k_keep);
+    return SegView{Pt, Pt + len, len - 1ull};
+  }
+  return SegView{Pt, Pt + (1ull << lam), ~0ull};
+}
+
 __global__ void __launch_bounds__(256) tridiag_expand_kernel(const double2* PM, double2* out, int n,
-                                                             double scale, int zshift, u64 zrank) {
+                                                             double scale, int zshift, u64 zrank, int k_keep) {
   const u64 N = 1ull << n;
   const u64 NL = 1ull << zshift;              // outputs per block on this rank
   const u64 z0 = zrank << zshift;
@@ -146,10 +149,7 @@ __global__ void __launch_bounds__(256) tridiag_expand_kernel(const double2* PM, 
        gidx += ((u64)gridDim.x * blockDim.x) >> 5) {
     const u64 id0 = gidx << 8;
     const int t = (int)(id0 >> zshift);
-    const int lam = n - t - 1;
-    const u64 seg = N - (N >> t);
-    const double2* Pt = PM + 2 * seg;
-    const double2* Mt = Pt + (1ull << lam);
+    const SegView sv = seg_view(PM, n, t, k_keep);
     double2 w[8];
     int ph[8];
 #pragma unroll
@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(256) tridiag_expand_kernel(const double2* PM, 
       const u64 zh = z >> (t + 1);
       const int s1 = __popcll(z & ((1ull << t) - 1ull)) & 1;
       const int s2 = (int)((z >> t) & 1ull);
-      w[k] = __ldg(((s1 == s2) ? Pt : Mt) + zh);
+      w[k] = __ldg(((s1 == s2) ? sv.P : sv.M) + (zh & sv.mask));
       ph[k] = __popcll(zl) + 2 * s1;  // i^{popcount(zl)} * (-1)^{s1}
     }
 #pragma unroll
@@ -175,19 +175,18 @@ __global__ void __launch_bounds__(256) tridiag_expand_kernel(const double2* PM, 
 
 // Small slices (2^zshift < 256): one output per thread.
 __global__ void tridiag_expand_small_kernel(const double2* PM, double2* out, int n, double scale,
-                                            int zshift, u64 zrank) {
+                                            int zshift, u64 zrank, int k_keep) {
   const u64 N = 1ull << n;
   const u64 NL = 1ull << zshift;
   const u64 id = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= (u64)n * NL) return;
   const int t = (int)(id >> zshift);
   const u64 z = (zrank << zshift) + (id & (NL - 1));
-  const int lam = n - t - 1;
-  const u64 seg = N - (N >> t);
+  const SegView sv = seg_view(PM, n, t, k_keep);
   const u64 zl = z & ((2ull << t) - 1ull);
   const int s1 = __popcll(z & ((1ull << t) - 1ull)) & 1;
   const int s2 = (int)((z >> t) & 1ull);
-  const double2 w = PM[2 * seg + (s1 == s2 ? 0ull : (1ull << lam)) + (z >> (t + 1))];
+  const double2 w = ((s1 == s2) ? sv.P : sv.M)[(z >> (t + 1)) & sv.mask];
   const int ph = __popcll(zl) + 2 * s1;
   const double2 c = rot_ipow(w, ph);
   out[NL + id] = make_double2(c.x * scale, c.y * scale);
@@ -210,6 +209,7 @@ struct SegPass {
   int zshift;  // slice filter of the stores (63: none)
   unsigned long long zrank;
   unsigned long long px;  // X-mask phase of the last pass (0: none)
+  unsigned long long zoff;  // z of element 0 (px phase)
 };
 constexpr int kMaxSeg = 40;
 struct SegPassTable {
@@ -241,7 +241,7 @@ template <int K>
 __device__ __forceinline__ void flat_tile(double2* S, const SegPass& sp, u64 local) {
   constexpr int F = kTileElems >> K;
   FlatLd<K> ld{sp.in, local * F, sp.b0};
-  FlatSt<K> st{sp.out, local * F, sp.b0, sp.scale, sp.zshift, sp.zrank, sp.px};
+  FlatSt<K> st{sp.out, local * F, sp.b0, sp.scale, sp.zshift, sp.zrank, sp.px, sp.zoff};
   fiber_tile<K>(S, ld, st);
 }
 
@@ -280,9 +280,13 @@ cudaError_t run_families(const WhtFamily* fam, int nfam, cudaStream_t st, int* n
     cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(seg_pass_kernel), kBandSmem);
     if (e != cudaSuccess) return e;
   }
-  int maxlam = 0;
-  for (int f = 0; f < nfam; ++f) maxlam = fam[f].lam > maxlam ? fam[f].lam : maxlam;
-  const int npass = maxlam <= 12 ? 1 : (maxlam + 7) / 8;
+  // whole-vector tiles for lam <= 12 (pass 0 only), else flat passes over bits [8p, 8p+8)
+  auto whole = [](const WhtFamily& w) { return w.first_bit == 0 && w.lam <= 12; };
+  int npass = 0;
+  for (int f = 0; f < nfam; ++f) {
+    const int need = whole(fam[f]) ? 1 : (fam[f].lam + 7) / 8;
+    npass = need > npass ? need : npass;
+  }
   for (int p = 0; p < npass; ++p) {
     SegPassTable T;
     T.count = 0;
@@ -296,7 +300,8 @@ cudaError_t run_families(const WhtFamily* fam, int nfam, cudaStream_t st, int* n
       sp.zshift = 63;
       sp.zrank = 0;
       sp.px = 0;
-      if (w.lam <= 12) {
+      sp.zoff = 0;
+      if (whole(w)) {
         if (p != 0) continue;
         sp.small = 1;
         sp.in = w.in;
@@ -306,14 +311,15 @@ cudaError_t run_families(const WhtFamily* fam, int nfam, cudaStream_t st, int* n
         sp.zshift = w.zshift;
         sp.zrank = w.zrank;
         sp.px = w.px;
+        sp.zoff = w.zoff;
         sp.first_tile = tiles;
         tiles += w.count;
       } else {
         const int b0 = 8 * p;
-        if (b0 >= w.lam) continue;
+        if (b0 < w.first_bit || b0 >= w.lam) continue;
         const int K = (w.lam - b0) < 8 ? (w.lam - b0) : 8;
         const bool last = b0 + K >= w.lam;
-        sp.in = p == 0 ? w.in : w.out;
+        sp.in = b0 == w.first_bit ? w.in : w.out;
         sp.out = last ? fin : w.out;
         sp.b0 = b0;
         sp.K = K;
@@ -322,6 +328,7 @@ cudaError_t run_families(const WhtFamily* fam, int nfam, cudaStream_t st, int* n
           sp.zshift = w.zshift;
           sp.zrank = w.zrank;
           sp.px = w.px;
+          sp.zoff = w.zoff;
         }
         sp.first_tile = tiles;
         tiles += (w.count << w.lam) / kTileElems;
@@ -341,8 +348,152 @@ cudaError_t run_families(const WhtFamily* fam, int nfam, cudaStream_t st, int* n
   return cudaSuccess;
 }
 
+// ---- top bits first: the z-sharded structured paths -------------
+// Rank r of G = 2^g GPUs needs W[r 2^(lam-g) + zl] of every long WHT.  Splitting the index
+// into its top 3 bits h and the rest il, W[zt 2^(lam-3) + zl] = WHT_{lam-3}(u_zt)[zl] with
+// u_zt[il] = sum_h (-1)^{popcount(h & zt)} v[h 2^(lam-3) + il]: the three butterfly levels
+// over the top bits come FIRST, and a rank keeps only the branches its z bits select (the
+// signed projection u_r of the SURVEY's 8(e) formula), so it reads the vector once and
+// transforms 1/G of it.  The one-GPU path runs the very same levels in the same order (top
+// bit first) and keeps all eight branches, so every rank's outputs are bitwise the one-GPU
+// values.  Used for vectors of at least 2^kTopMin elements; shorter ones stay replicated.
+
+// W over the 3 top index bits for output zt, levels in descending bit order: pairs
+// (h, h + 4) first, then (h, h + 2), then (h, h + 1); a z bit of 0 takes the sum.
+__device__ __forceinline__ double2 top3_value(const double2 (&d)[8], unsigned zt) {
+  double2 a[4], b[2];
+#pragma unroll
+  for (int h = 0; h < 4; ++h) a[h] = (zt & 4u) ? csub(d[h], d[h + 4]) : cadd(d[h], d[h + 4]);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) b[h] = (zt & 2u) ? csub(a[h], a[h + 2]) : cadd(a[h], a[h + 2]);
+  return (zt & 1u) ? csub(b[0], b[1]) : cadd(b[0], b[1]);
+}
+
+// Pass 0 of a long single vector (lam >= kTopMin): the three top levels, then bits 4-7 and
+// 0-3 of il exactly as contig8_tile orders them.  A tile holds KS = 2^k_keep kept top-bit
+// branches x IL = 4096 / KS consecutive il (16 fibres of 256); it reads 8 x IL elements
+// (8 runs of IL contiguous, coalesced) and writes KS runs of IL: out[kt 2^(lam-3) + il].
+// zt = (rsel << k_keep) | kt.
+__global__ void __launch_bounds__(kThreads, 2) top3_pass_kernel(const double2* __restrict__ in, double2* out,
+                                                                int lam, int k_keep, unsigned rsel) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* S = reinterpret_cast<double2*>(smem_raw);
+  const int L = lam - 3;
+  const int KS = 1 << k_keep;
+  const int IL = kTileElems >> k_keep;
+  const u64 Q = 1ull << L;
+  const u64 ntiles = Q / (u64)IL;
+  const int tid = threadIdx.x;
+  for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const u64 il0 = tile * (u64)IL;
+    // stage 0: top levels, two il per thread per round (16 loads in flight)
+    for (int m = 0; m < IL / 256; m += 2) {
+      double2 d0[8], d1[8];
+      const u64 ia = il0 + (u64)(tid + 256 * m), ib = ia + 256;
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        d0[h] = ld_l2(in + (u64)h * Q + ia);
+        d1[h] = ld_l2(in + (u64)h * Q + ib);
+      }
+      for (int kt = 0; kt < KS; ++kt) {
+        const unsigned zt = (rsel << k_keep) | (unsigned)kt;
+        const int ea = kt * IL + tid + 256 * m, eb = ea + 256;
+        S[contig_slot(ea >> 8, ea & 255)] = top3_value(d0, zt);
+        S[contig_slot(eb >> 8, eb & 255)] = top3_value(d1, zt);
+      }
+    }
+    __syncthreads();
+    double2 v[16];
+    {  // bits 4-7 of il
+      const int f = tid >> 4, jl = tid & 15;
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) v[kk] = S[contig_slot(f, jl + 16 * kk)];
+      wht_regs<4>(v);
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) S[contig_slot(f, jl + 16 * kk)] = v[kk];  // own slots only
+    }
+    __syncthreads();
+    {  // bits 0-3 of il
+      const int f = tid >> 4, kh = tid & 15;
+#pragma unroll
+      for (int jl = 0; jl < 16; ++jl) v[jl] = S[contig_slot(f, jl + 16 * kh)];
+      wht_regs<4>(v);
+#pragma unroll
+      for (int jl = 0; jl < 16; ++jl) S[contig_slot(f, jl + 16 * kh)] = v[jl];
+    }
+    __syncthreads();
+    {
+      const int f = tid >> 4, jl = tid & 15;
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) {
+        const int e = f * 256 + jl + 16 * kk;
+        const int kt = e / IL, il = e - kt * IL;
+        st_l2(out + ((u64)kt << L) + il0 + (u64)il, S[contig_slot(f, jl + 16 * kk)]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Tridiagonal split of the long segments (lam = n - t - 1 >= kTopMin) fused with their top
+// levels: for i = h 2^(n-3) + i_low with t trailing ones (t < n - 3, the same for all eight
+// top blocks h), S_t[.] = sup[i] and U_t[.] = sub[i + 1] sit at segment index
+// h 2^(lam-3) + hl, hl = i_low >> (t + 1), so one coalesced read of the eight blocks feeds
+// the top levels of P_t = WHT(S_t + U_t) and M_t = WHT(S_t - U_t).  Layout of a long
+// segment: P_t at PM + 2 seg, KS branches of 2^(lam-3) (kt major), M_t right after.
+__global__ void __launch_bounds__(256) tri_split_top3_kernel(const double2* __restrict__ band, double2* PM, int n,
+                                                             int k_keep, unsigned rsel) {
+  const u64 N = 1ull << n;
+  const u64 Q = N >> 3;
+  const double2* sub = band;
+  const double2* sup = band + 2 * N;
+  const int KS = 1 << k_keep;
+  for (u64 il = (u64)blockIdx.x * blockDim.x + threadIdx.x; il < Q - 1; il += (u64)gridDim.x * blockDim.x) {
+    const int t = __ffsll((long long)~il) - 1;
+    const int lam = n - t - 1;
+    if (lam < kTopMin) continue;
+    double2 P[8], M[8];
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+      const double2 sv = ld_stream(sup + (u64)h * Q + il);
+      const double2 uv = ld_stream(sub + (u64)h * Q + il + 1);
+      P[h] = cadd(sv, uv);
+      M[h] = csub(sv, uv);
+    }
+    const u64 seg = N - (N >> t);
+    const int Lb = lam - 3;
+    double2* Pt = PM + 2 * seg;
+    double2* Mt = Pt + ((u64)KS << Lb);
+    const u64 hl = il >> (t + 1);
+    for (int kt = 0; kt < KS; ++kt) {
+      const unsigned zt = (rsel << k_keep) | (unsigned)kt;
+      st_l2(Pt + ((u64)kt << Lb) + hl, top3_value(P, zt));
+      st_l2(Mt + ((u64)kt << Lb) + hl, top3_value(M, zt));
+    }
+  }
+}
+
+// Split of the short segments (lam < kTopMin, replicated on every rank): one thread per
+// (lam, h), id = 2^lam - 1 + h; full P_t (2^lam) then M_t (2^lam).
+__global__ void tri_split_small_kernel(const double2* __restrict__ band, double2* PM, int n, int lam_max) {
+  const u64 N = 1ull << n;
+  const double2* sub = band;
+  const double2* sup = band + 2 * N;
+  const u64 total = (2ull << lam_max) - 1ull;  // lam = 0 .. lam_max
+  for (u64 id = (u64)blockIdx.x * blockDim.x + threadIdx.x; id < total; id += (u64)gridDim.x * blockDim.x) {
+    const int lam = 63 - __clzll((long long)(id + 1));
+    const u64 h = id + 1 - (1ull << lam);
+    const int t = n - 1 - lam;
+    const u64 i = (h << (t + 1)) + (1ull << t) - 1ull;
+    const double2 sv = ld_stream(sup + i), uv = ld_stream(sub + i + 1);
+    const u64 seg = N - (N >> t);
+    PM[2 * seg + h] = cadd(sv, uv);
+    PM[2 * seg + (1ull << lam) + h] = csub(sv, uv);
+  }
+}
+
 // Workspace: [P/M segments: 2 * 2^n] (TRIDIAGONAL) + [x = 0 vector: 2^n] (world > 1: the
-// passes before the last run on a full-length copy; only the last one writes the slice).
+// x = 0 intermediate when it does not fit the rank's output block).
 size_t band_workspace_bytes(int n, int structure, int world) {
   const size_t N = (size_t)1 << n;
   size_t b = structure == 4 ? 2 * N * 16 : 0;
@@ -358,41 +509,85 @@ cudaError_t launch_band(const double2* A, double2* out, int n, int structure, vo
   const int zshift = world > 1 ? n - g : 63;
   const u64 zrank = world > 1 ? (u64)rank : 0ull;
   double2* PM = reinterpret_cast<double2*>(ws);
-  double2* X0 = world > 1 ? PM + (structure == 4 ? 2 * N : 0) : nullptr;  // full-length x=0 scratch
-  // the x = 0 family (main diagonal): in place on `out` on one GPU; on a full-length
-  // workspace copy with a slice-writing last pass when z-sharded
-  auto x0_family = [&](const double2* src) {
-    WhtFamily f{src, world > 1 && n > 12 ? X0 : out, n, 1, scale};
+  double2* X0 = world > 1 ? PM + (structure == 4 ? 2 * N : 0) : nullptr;  // x = 0 scratch
+  const int sms = device_sm_count();
+  // top-bits-first geometry: gp of the rank's bits select branches (at most the 3 top ones),
+  // the remaining g - gp bits are a slice filter of the last pass
+  const int gp = g < 3 ? g : 3;
+  const int k_keep = 3 - gp;
+  const unsigned rsel = (unsigned)(world > 1 ? (rank >> (g - gp)) : 0);
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(top3_pass_kernel), kBandSmem);
+  if (e != cudaSuccess) return e;
+  // The x = 0 family (diagonal, anti-diagonal, tridiagonal main diagonal): vector `src`,
+  // output block 0 of `out` (2^n / world elements), px = X-mask phase.
+  auto x0_family = [&](const double2* src, u64 px, WhtFamily& f) -> cudaError_t {
+    if (n >= kTopMin) {
+      // top levels + bits 0-7 in one pass into the rank's KS branches, then bits 8.. of the
+      // 2^(n-3) branches; ranks beyond the top 3 bits filter their slice in the last pass
+      double2* mid = (g <= 3) ? out : X0;
+      u64 tiles = ((N >> 3) / (u64)(kTileElems >> k_keep));
+      u64 grid = (u64)sms * 2;
+      if (grid > tiles) grid = tiles;
+      top3_pass_kernel<<<(unsigned)grid, kThreads, kBandSmem, st>>>(src, mid, n, k_keep, rsel);
+      *nl += 1;
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+      f = WhtFamily{mid, mid, n - 3, 1ull << k_keep, scale};
+      f.first_bit = 8;
+      f.final_out = out;
+      f.zshift = g > 3 ? n - g : 63;
+      f.zrank = g > 3 ? (u64)(rank & ((1 << (g - 3)) - 1)) : 0ull;
+      f.zoff = (u64)rsel << (n - gp);
+      f.px = px;
+      return cudaSuccess;
+    }
+    // short vectors: every rank runs the whole transform; only the last pass stores, and
+    // only the rank's slice
+    f = WhtFamily{src, world > 1 && n > 12 ? X0 : out, n, 1, scale};
     f.final_out = out;
     f.zshift = zshift;
     f.zrank = zrank;
-    return f;
+    f.px = px;
+    return cudaSuccess;
   };
   if (structure == 3 || structure == 5) {
     // DIAGONAL: x = 0.  ANTI_DIAGONAL: v_x[i] = A[i][i ^ (2^n - 1)] = a[i] is
     // nonzero only for x = 2^n - 1, so alpha(2^n - 1, z) = 2^-n i^{popcount(z)} WHT(a)[z].
-    WhtFamily f = x0_family(A);
-    if (structure == 5) f.px = N - 1;
+    WhtFamily f;
+    if ((e = x0_family(A, structure == 5 ? N - 1 : 0ull, f)) != cudaSuccess) return e;
     return run_families(&f, 1, st, nl);
   }
-  // TRIDIAGONAL: A = [sub | main | sup]
-  const int sms = device_sm_count();
-  cudaError_t e;
+  // TRIDIAGONAL: A = [sub | main | sup].  Segments t with lam = n - t - 1 >= kTopMin: fused
+  // split + top levels (the rank's branches only); shorter ones: plain split, replicated.
+  const int lam_small = n - 1 < kTopMin - 1 ? n - 1 : kTopMin - 1;
   {
-    u64 blocks = (N + 255) / 256;
+    u64 total = (2ull << lam_small) - 1ull;
+    u64 blocks = (total + 255) / 256;
     if (blocks > (u64)sms * 32) blocks = (u64)sms * 32;
-    tridiag_split_kernel<<<(unsigned)blocks, 256, 0, st>>>(A, PM, n);
+    tri_split_small_kernel<<<(unsigned)blocks, 256, 0, st>>>(A, PM, n, lam_small);
     *nl += 1;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  // block 0 (x = 0): WHT(main) scaled; blocks t+1: P_t / M_t (two vectors of 2^(n-t-1))
+  if (n - 1 >= kTopMin) {
+    u64 blocks = ((N >> 3) + 255) / 256;
+    if (blocks > (u64)sms * 16) blocks = (u64)sms * 16;
+    tri_split_top3_kernel<<<(unsigned)blocks, 256, 0, st>>>(A, PM, n, k_keep, rsel);
+    *nl += 1;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  // block 0 (x = 0): WHT(main) scaled; blocks t+1: P_t / M_t
   WhtFamily fam[kMaxSeg];
   int nf = 0;
-  fam[nf++] = x0_family(A + N);
+  if ((e = x0_family(A + N, 0ull, fam[nf++])) != cudaSuccess) return e;
   for (int t = 0; t < n; ++t) {
     const int lam = n - t - 1;
     const u64 seg = N - (N >> t);
-    fam[nf++] = WhtFamily{PM + 2 * seg, PM + 2 * seg, lam, 2, 1.0};
+    if (lam >= kTopMin) {
+      WhtFamily f{PM + 2 * seg, PM + 2 * seg, lam - 3, 2ull << k_keep, 1.0};  // P then M branches
+      f.first_bit = 0;
+      fam[nf++] = f;
+    } else {
+      fam[nf++] = WhtFamily{PM + 2 * seg, PM + 2 * seg, lam, 2, 1.0};
+    }
   }
   if ((e = run_families(fam, nf, st, nl)) != cudaSuccess) return e;
   {
@@ -402,10 +597,10 @@ cudaError_t launch_band(const double2* A, double2* out, int n, int structure, vo
     if (NL >= 256) {
       u64 blocks = (total / 8 + 255) / 256;
       if (blocks > (u64)sms * 16) blocks = (u64)sms * 16;
-      tridiag_expand_kernel<<<(unsigned)blocks, 256, 0, st>>>(PM, out, n, scale, zs, zrank);
+      tridiag_expand_kernel<<<(unsigned)blocks, 256, 0, st>>>(PM, out, n, scale, zs, zrank, k_keep);
     } else {
       tridiag_expand_small_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(PM, out, n, scale, zs,
-                                                                                 zrank);
+                                                                                 zrank, k_keep);
     }
     *nl += 1;
     e = cudaGetLastError();

@@ -18,6 +18,10 @@ struct WhtFamily {
   int zshift = 63;               // slice filter of the last pass (single-vector families)
   unsigned long long zrank = 0;
   unsigned long long px = 0;                    // X-mask phase i^{popcount(px & z)} of the last pass
+  int first_bit = 0;             // bits below first_bit are already transformed (a multiple of 8:
+                                 //   the family starts at pass first_bit / 8 and never uses the
+                                 //   whole-vector tiles)
+  unsigned long long zoff = 0;   // z of element 0 of the last pass's output (the px phase uses z)
 };
 
 constexpr int kMaxFamilies = 40;  // per run_families call

@@ -205,13 +205,16 @@ def test_xshard_emulated_bitwise(gpu, n, world):
         assert np.max(np.abs(full - ref)) <= TOL * torch.max(torch.abs(A)).item()
 
 
-@pytest.mark.parametrize("structure", ["diagonal", "tridiagonal"])
-@pytest.mark.parametrize("n,world", [(5, 2), (9, 8), (13, 4), (14, 2), (17, 8)])
+@pytest.mark.parametrize("structure", ["diagonal", "tridiagonal", "anti_diagonal"])
+@pytest.mark.parametrize("n,world", [(5, 2), (9, 8), (13, 4), (14, 2), (15, 8), (16, 2), (16, 16), (17, 8),
+                                     (18, 4), (19, 32)])
 def test_zshard_emulated_bitwise(gpu, structure, n, world):
     """Every rank's z-slice (replicated band, no communication) == the same slice of the
-    one-GPU output, bit for bit (same WHT schedule on every rank)."""
+    one-GPU output, bit for bit: the long vectors (2^15 elements and up) run their top
+    butterfly levels first on every path, a rank keeping only its branches (world <= 8) and
+    filtering the rest of its bits in the last pass (world > 8)."""
     torch = _torch()
-    B = ptdr.generate_band(n, 3, structure)
+    B = ptdr.generate_band(n, 3, "diagonal" if structure == "anti_diagonal" else structure)
     ref = ptdr.decompose(B, structure).cpu().numpy()
     blocks = n + 1 if structure == "tridiagonal" else 1
     parts = [ptdr.decompose_zshard(B, structure, r, world).cpu().numpy() for r in range(world)]
@@ -219,16 +222,16 @@ def test_zshard_emulated_bitwise(gpu, structure, n, world):
     assert np.array_equal(full.view(np.uint64), ref.view(np.uint64))
 
 
-@pytest.mark.parametrize("structure", ["diagonal", "tridiagonal"])
+@pytest.mark.parametrize("structure", ["diagonal", "tridiagonal", "anti_diagonal"])
 def test_zshard_n24_world8(gpu, structure):
-    """BASELINE configs[3] at 8 GPUs: ranks 0, 3 and 7 (each independent) vs the one-GPU run."""
+    """BASELINE configs[3] at 8 GPUs: every rank (each independent) vs the one-GPU run."""
     torch = _torch()
     n, world = 24, 8
-    B = ptdr.generate_band(n, 3, structure)
+    B = ptdr.generate_band(n, 3, "diagonal" if structure == "anti_diagonal" else structure)
     ref = ptdr.decompose(B, structure)
     blocks = n + 1 if structure == "tridiagonal" else 1
     NL = (1 << n) // world
-    for r in (0, 3, 7):
+    for r in range(world):
         loc = ptdr.decompose_zshard(B, structure, r, world)
         want = ref.view(blocks, 1 << n)[:, r * NL:(r + 1) * NL].reshape(-1)
         assert torch.equal(torch.view_as_real(loc), torch.view_as_real(want)), r

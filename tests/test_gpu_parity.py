@@ -220,9 +220,13 @@ def test_error_paths(gpu):
         ptdr.decompose(A, out=A.view(-1))                # out aliases A
     assert e.value.status == ptdr.PTDR_EUNSUPPORTED
     ws = torch.empty(16, dtype=torch.uint8, device="cuda")
-    with pytest.raises(ptdr.PtdrError) as e:
-        ptdr.decompose(A, workspace=ws)                  # workspace too small
-    assert e.value.status == ptdr.PTDR_ENOMEM
+    with pytest.raises(ValueError):
+        ptdr.decompose(A, workspace=ws)                  # the binding checks the size first
+    out = torch.empty(4 ** 8, dtype=torch.complex128, device="cuda")
+    import ctypes
+    st = ptdr.lib().ptdr_decompose_async(ctypes.c_void_p(A.data_ptr()), 8, 0, ctypes.c_void_p(out.data_ptr()),
+                                         ctypes.c_void_p(ws.data_ptr()), 16, None)
+    assert st == ptdr.PTDR_ENOMEM                        # ... and so does the ABI
     with pytest.raises(TypeError):
         ptdr.decompose(A.cpu())                          # no CPU fallback
 

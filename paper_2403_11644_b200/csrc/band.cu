@@ -368,19 +368,71 @@ __device__ __forceinline__ double2 top3_value(const double2 (&d)[8], unsigned zt
   for (int h = 0; h < 2; ++h) b[h] = (zt & 2u) ? csub(a[h], a[h + 2]) : cadd(a[h], a[h + 2]);
   return (zt & 1u) ? csub(b[0], b[1]) : cadd(b[0], b[1]);
 }
+// The KS = 2^KK kept outputs zt = (rsel << KK) | kt, kt = 0..KS-1, as one butterfly network
+// sharing its partial sums (12 complex butterflies for all eight on one GPU); the top bits
+// fixed by rsel pick one branch per level (a select, no divergence).  Every output is the
+// same sequence of operations as top3_value(d, zt), so its value is bitwise the same.
+__device__ __forceinline__ double2 bfly(double2 a, double2 b, bool diff) { return diff ? csub(a, b) : cadd(a, b); }
+template <int KK>
+__device__ __forceinline__ void top3_kept(const double2 (&d)[8], unsigned rsel, double2* o) {
+  if constexpr (KK == 3) {
+    double2 a[2][4], b[2][2][2];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      a[0][h] = cadd(d[h], d[h + 4]);
+      a[1][h] = csub(d[h], d[h + 4]);
+    }
+#pragma unroll
+    for (int b2 = 0; b2 < 2; ++b2)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        b[b2][0][h] = cadd(a[b2][h], a[b2][h + 2]);
+        b[b2][1][h] = csub(a[b2][h], a[b2][h + 2]);
+      }
+#pragma unroll
+    for (int kt = 0; kt < 8; ++kt) o[kt] = bfly(b[kt >> 2][(kt >> 1) & 1][0], b[kt >> 2][(kt >> 1) & 1][1], kt & 1);
+  } else {
+    const unsigned zt0 = rsel << KK;  // the fixed bits of every kept zt
+    double2 a[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) a[h] = bfly(d[h], d[h + 4], (zt0 >> 2) & 1u);
+    if constexpr (KK == 2) {
+      double2 b[2][2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        b[0][h] = cadd(a[h], a[h + 2]);
+        b[1][h] = csub(a[h], a[h + 2]);
+      }
+#pragma unroll
+      for (int kt = 0; kt < 4; ++kt) o[kt] = bfly(b[kt >> 1][0], b[kt >> 1][1], kt & 1);
+    } else {
+      double2 b[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) b[h] = bfly(a[h], a[h + 2], (zt0 >> 1) & 1u);
+      if constexpr (KK == 1) {
+        o[0] = cadd(b[0], b[1]);
+        o[1] = csub(b[0], b[1]);
+      } else {
+        o[0] = bfly(b[0], b[1], zt0 & 1u);
+      }
+    }
+  }
+}
 
 // Pass 0 of a long single vector (lam >= kTopMin): the three top levels, then bits 4-7 and
 // 0-3 of il exactly as contig8_tile orders them.  A tile holds KS = 2^k_keep kept top-bit
 // branches x IL = 4096 / KS consecutive il (16 fibres of 256); it reads 8 x IL elements
 // (8 runs of IL contiguous, coalesced) and writes KS runs of IL: out[kt 2^(lam-3) + il].
 // zt = (rsel << k_keep) | kt.
+template <int KK>
 __global__ void __launch_bounds__(kThreads, 2) top3_pass_kernel(const double2* __restrict__ in, double2* out,
-                                                                int lam, int k_keep, unsigned rsel) {
+                                                                int lam, unsigned rsel) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* S = reinterpret_cast<double2*>(smem_raw);
+  constexpr int k_keep = KK;
   const int L = lam - 3;
-  const int KS = 1 << k_keep;
-  const int IL = kTileElems >> k_keep;
+  constexpr int KS = 1 << KK;
+  constexpr int IL = kTileElems >> KK;
   const u64 Q = 1ull << L;
   const u64 ntiles = Q / (u64)IL;
   const int tid = threadIdx.x;
@@ -395,11 +447,14 @@ __global__ void __launch_bounds__(kThreads, 2) top3_pass_kernel(const double2* _
         d0[h] = ld_l2(in + (u64)h * Q + ia);
         d1[h] = ld_l2(in + (u64)h * Q + ib);
       }
+      double2 o0[KS], o1[KS];
+      top3_kept<KK>(d0, rsel, o0);
+      top3_kept<KK>(d1, rsel, o1);
+#pragma unroll
       for (int kt = 0; kt < KS; ++kt) {
-        const unsigned zt = (rsel << k_keep) | (unsigned)kt;
         const int ea = kt * IL + tid + 256 * m, eb = ea + 256;
-        S[contig_slot(ea >> 8, ea & 255)] = top3_value(d0, zt);
-        S[contig_slot(eb >> 8, eb & 255)] = top3_value(d1, zt);
+        S[contig_slot(ea >> 8, ea & 255)] = o0[kt];
+        S[contig_slot(eb >> 8, eb & 255)] = o1[kt];
       }
     }
     __syncthreads();
@@ -435,19 +490,29 @@ __global__ void __launch_bounds__(kThreads, 2) top3_pass_kernel(const double2* _
   }
 }
 
+template <int KK>
+static cudaError_t launch_top3(const double2* in, double2* out, int lam, unsigned rsel, unsigned grid,
+                               cudaStream_t st) {
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(top3_pass_kernel<KK>), kBandSmem);
+  if (e != cudaSuccess) return e;
+  top3_pass_kernel<KK><<<grid, kThreads, kBandSmem, st>>>(in, out, lam, rsel);
+  return cudaGetLastError();
+}
+
 // Tridiagonal split of the long segments (lam = n - t - 1 >= kTopMin) fused with their top
 // levels: for i = h 2^(n-3) + i_low with t trailing ones (t < n - 3, the same for all eight
 // top blocks h), S_t[.] = sup[i] and U_t[.] = sub[i + 1] sit at segment index
 // h 2^(lam-3) + hl, hl = i_low >> (t + 1), so one coalesced read of the eight blocks feeds
 // the top levels of P_t = WHT(S_t + U_t) and M_t = WHT(S_t - U_t).  Layout of a long
 // segment: P_t at PM + 2 seg, KS branches of 2^(lam-3) (kt major), M_t right after.
+template <int KK>
 __global__ void __launch_bounds__(256) tri_split_top3_kernel(const double2* __restrict__ band, double2* PM, int n,
-                                                             int k_keep, unsigned rsel) {
+                                                             unsigned rsel) {
   const u64 N = 1ull << n;
   const u64 Q = N >> 3;
   const double2* sub = band;
   const double2* sup = band + 2 * N;
-  const int KS = 1 << k_keep;
+  constexpr int KS = 1 << KK;
   for (u64 il = (u64)blockIdx.x * blockDim.x + threadIdx.x; il < Q - 1; il += (u64)gridDim.x * blockDim.x) {
     const int t = __ffsll((long long)~il) - 1;
     const int lam = n - t - 1;
@@ -465,10 +530,13 @@ __global__ void __launch_bounds__(256) tri_split_top3_kernel(const double2* __re
     double2* Pt = PM + 2 * seg;
     double2* Mt = Pt + ((u64)KS << Lb);
     const u64 hl = il >> (t + 1);
+    double2 oP[KS], oM[KS];
+    top3_kept<KK>(P, rsel, oP);
+    top3_kept<KK>(M, rsel, oM);
+#pragma unroll
     for (int kt = 0; kt < KS; ++kt) {
-      const unsigned zt = (rsel << k_keep) | (unsigned)kt;
-      st_l2(Pt + ((u64)kt << Lb) + hl, top3_value(P, zt));
-      st_l2(Mt + ((u64)kt << Lb) + hl, top3_value(M, zt));
+      st_l2(Pt + ((u64)kt << Lb) + hl, oP[kt]);
+      st_l2(Mt + ((u64)kt << Lb) + hl, oM[kt]);
     }
   }
 }
@@ -516,8 +584,7 @@ cudaError_t launch_band(const double2* A, double2* out, int n, int structure, vo
   const int gp = g < 3 ? g : 3;
   const int k_keep = 3 - gp;
   const unsigned rsel = (unsigned)(world > 1 ? (rank >> (g - gp)) : 0);
-  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(top3_pass_kernel), kBandSmem);
-  if (e != cudaSuccess) return e;
+  cudaError_t e = cudaSuccess;
   // The x = 0 family (diagonal, anti-diagonal, tridiagonal main diagonal): vector `src`,
   // output block 0 of `out` (2^n / world elements), px = X-mask phase.
   auto x0_family = [&](const double2* src, u64 px, WhtFamily& f) -> cudaError_t {
@@ -528,7 +595,13 @@ cudaError_t launch_band(const double2* A, double2* out, int n, int structure, vo
       u64 tiles = ((N >> 3) / (u64)(kTileElems >> k_keep));
       u64 grid = (u64)sms * 2;
       if (grid > tiles) grid = tiles;
-      top3_pass_kernel<<<(unsigned)grid, kThreads, kBandSmem, st>>>(src, mid, n, k_keep, rsel);
+      switch (k_keep) {
+        case 3: e = launch_top3<3>(src, mid, n, rsel, (unsigned)grid, st); break;
+        case 2: e = launch_top3<2>(src, mid, n, rsel, (unsigned)grid, st); break;
+        case 1: e = launch_top3<1>(src, mid, n, rsel, (unsigned)grid, st); break;
+        default: e = launch_top3<0>(src, mid, n, rsel, (unsigned)grid, st); break;
+      }
+      if (e != cudaSuccess) return e;
       *nl += 1;
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
       f = WhtFamily{mid, mid, n - 3, 1ull << k_keep, scale};
@@ -570,7 +643,12 @@ cudaError_t launch_band(const double2* A, double2* out, int n, int structure, vo
   if (n - 1 >= kTopMin) {
     u64 blocks = ((N >> 3) + 255) / 256;
     if (blocks > (u64)sms * 16) blocks = (u64)sms * 16;
-    tri_split_top3_kernel<<<(unsigned)blocks, 256, 0, st>>>(A, PM, n, k_keep, rsel);
+    switch (k_keep) {
+      case 3: tri_split_top3_kernel<3><<<(unsigned)blocks, 256, 0, st>>>(A, PM, n, rsel); break;
+      case 2: tri_split_top3_kernel<2><<<(unsigned)blocks, 256, 0, st>>>(A, PM, n, rsel); break;
+      case 1: tri_split_top3_kernel<1><<<(unsigned)blocks, 256, 0, st>>>(A, PM, n, rsel); break;
+      default: tri_split_top3_kernel<0><<<(unsigned)blocks, 256, 0, st>>>(A, PM, n, rsel); break;
+    }
     *nl += 1;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }

@@ -210,6 +210,8 @@ struct SegPass {
   unsigned long long zrank;
   unsigned long long px;  // X-mask phase of the last pass (0: none)
   unsigned long long zoff;  // z of element 0 (px phase)
+  int fn;                 // 1: the combined near+far pass 0 of a 17..20-bit family (fn_tile)
+  int fn_lam;
 };
 constexpr int kMaxSeg = 40;
 struct SegPassTable {
@@ -237,6 +239,70 @@ __device__ __forceinline__ void small_wht_tile(double2* S, const double2* in, do
   for (int i = threadIdx.x; i < len; i += blockDim.x) store_final(out, e0 + (u64)i, S[i], scale, zshift, zrank, px);
 }
 
+template <int F>
+__device__ __forceinline__ void fn_far(double2* S, int tid) {
+  constexpr int B = 4 - F;
+#pragma unroll
+  for (int r = 0; r < (1 << (4 - F)); ++r) {
+    const int p = tid + 256 * r;
+    const int b = p >> 8, j = p & 255;
+    double2 w[1 << F];
+#pragma unroll
+    for (int f = 0; f < (1 << F); ++f) w[f] = S[contig_slot((f << B) | b, j)];
+    wht_regs<F>(w);
+#pragma unroll
+    for (int f = 0; f < (1 << F); ++f) S[contig_slot((f << B) | b, j)] = w[f];
+  }
+}
+
+// Pass 0 of a family of 2^lam-element vectors, 17 <= lam <= 20: the 8 near bits [0, 8)
+// (runs of 256, the stages of contig8_tile) and the lam - 16 far bits [16, lam) in ONE tile,
+// with the 20 - lam bits above 8 as batch, so the family needs two passes instead of three
+// (bits [8, 16) are the second).  Tile = 2^(lam-16) far x 2^(20-lam) batch x 256 near;
+// "fibre" fb = (far << (20 - lam)) | batch holds 256 near elements at contig_slot(fb, j).
+__device__ __forceinline__ void fn_tile(double2* S, const double2* in, double2* out, u64 tile, int lam) {
+  const int F = lam - 16, B = 20 - lam;
+  const u64 v = tile >> (lam - 12), mb = tile & ((1ull << (lam - 12)) - 1ull);
+  const u64 vbase = v << lam;
+  auto addr = [&](int fb, int j) -> u64 {
+    const u64 f = (u64)(fb >> B), b = (u64)(fb & ((1 << B) - 1));
+    return vbase + (f << 16) + (((mb << B) + b) << 8) + (u64)j;
+  };
+  const int tid = threadIdx.x;
+  double2 v16[16];
+  {  // near bits 4-7 (as contig8_tile)
+    const int fb = tid >> 4, jl = tid & 15;
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) v16[kk] = ld_l2(in + addr(fb, jl + 16 * kk));
+    wht_regs<4>(v16);
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) S[contig_slot(fb, jl + 16 * kk)] = v16[kk];
+  }
+  __syncthreads();
+  {  // near bits 0-3
+    const int fb = tid >> 4, kh = tid & 15;
+#pragma unroll
+    for (int jl = 0; jl < 16; ++jl) v16[jl] = S[contig_slot(fb, jl + 16 * kh)];
+    wht_regs<4>(v16);
+#pragma unroll
+    for (int jl = 0; jl < 16; ++jl) S[contig_slot(fb, jl + 16 * kh)] = v16[jl];
+  }
+  __syncthreads();
+  // far bits: 2^F values per (batch, near) position, 2^(4-F) positions per thread
+  switch (F) {
+    case 1: fn_far<1>(S, tid); break;
+    case 2: fn_far<2>(S, tid); break;
+    case 3: fn_far<3>(S, tid); break;
+    default: fn_far<4>(S, tid); break;
+  }
+  __syncthreads();
+  {
+    const int fb = tid >> 4, jl = tid & 15;
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) st_l2(out + addr(fb, jl + 16 * kk), S[contig_slot(fb, jl + 16 * kk)]);
+  }
+}
+
 template <int K>
 __device__ __forceinline__ void flat_tile(double2* S, const SegPass& sp, u64 local) {
   constexpr int F = kTileElems >> K;
@@ -253,7 +319,9 @@ __global__ void __launch_bounds__(kThreads, 2) seg_pass_kernel(const __grid_cons
     while (i + 1 < T.count && T.s[i + 1].first_tile <= tile) ++i;
     const SegPass& sp = T.s[i];
     const u64 local = tile - sp.first_tile;
-    if (sp.small) {
+    if (sp.fn) {
+      fn_tile(S, sp.in, sp.out, local, sp.fn_lam);
+    } else if (sp.small) {
       const u64 off = local << sp.small_lam;
       small_wht_tile(S, sp.in + off, sp.out, sp.small_lam, sp.scale, off, sp.zshift, sp.zrank, sp.px);
     } else if (sp.b0 == 0 && sp.K == 8) {
@@ -282,9 +350,11 @@ cudaError_t run_families(const WhtFamily* fam, int nfam, cudaStream_t st, int* n
   }
   // whole-vector tiles for lam <= 12 (pass 0 only), else flat passes over bits [8p, 8p+8)
   auto whole = [](const WhtFamily& w) { return w.first_bit == 0 && w.lam <= 12; };
+  // 17..20 bits: near bits 0-7 + far bits 16.. in pass 0 (fn_tile), bits 8-15 last
+  auto fnfam = [](const WhtFamily& w) { return w.first_bit == 0 && w.lam >= 17 && w.lam <= 20; };
   int npass = 0;
   for (int f = 0; f < nfam; ++f) {
-    const int need = whole(fam[f]) ? 1 : (fam[f].lam + 7) / 8;
+    const int need = whole(fam[f]) ? 1 : fnfam(fam[f]) ? 2 : (fam[f].lam + 7) / 8;
     npass = need > npass ? need : npass;
   }
   for (int p = 0; p < npass; ++p) {
@@ -301,7 +371,28 @@ cudaError_t run_families(const WhtFamily* fam, int nfam, cudaStream_t st, int* n
       sp.zrank = 0;
       sp.px = 0;
       sp.zoff = 0;
-      if (whole(w)) {
+      if (fnfam(w)) {
+        if (p >= 2) continue;
+        const bool last = p == 1;
+        sp.in = p == 0 ? w.in : w.out;
+        sp.out = last ? fin : w.out;
+        if (p == 0) {
+          sp.fn = 1;
+          sp.fn_lam = w.lam;
+        } else {
+          sp.b0 = 8;
+          sp.K = 8;
+        }
+        sp.scale = last ? w.scale : 1.0;
+        if (last) {
+          sp.zshift = w.zshift;
+          sp.zrank = w.zrank;
+          sp.px = w.px;
+          sp.zoff = w.zoff;
+        }
+        sp.first_tile = tiles;
+        tiles += (w.count << w.lam) / kTileElems;
+      } else if (whole(w)) {
         if (p != 0) continue;
         sp.small = 1;
         sp.in = w.in;
@@ -438,23 +529,24 @@ __global__ void __launch_bounds__(kThreads, 2) top3_pass_kernel(const double2* _
   const int tid = threadIdx.x;
   for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const u64 il0 = tile * (u64)IL;
-    // stage 0: top levels, two il per thread per round (16 loads in flight)
-    for (int m = 0; m < IL / 256; m += 2) {
-      double2 d0[8], d1[8];
-      const u64 ia = il0 + (u64)(tid + 256 * m), ib = ia + 256;
+    // stage 0: top levels; IPR il per thread per round (8 IPR loads in flight: 16 when all
+    // eight branches are kept, 32 when fewer outputs leave registers free)
+    constexpr int IPR = KK >= 2 ? 2 : 4;
+    for (int m = 0; m < IL / 256; m += IPR) {
+      double2 d[IPR][8];
 #pragma unroll
-      for (int h = 0; h < 8; ++h) {
-        d0[h] = ld_l2(in + (u64)h * Q + ia);
-        d1[h] = ld_l2(in + (u64)h * Q + ib);
-      }
-      double2 o0[KS], o1[KS];
-      top3_kept<KK>(d0, rsel, o0);
-      top3_kept<KK>(d1, rsel, o1);
+      for (int r = 0; r < IPR; ++r)
 #pragma unroll
-      for (int kt = 0; kt < KS; ++kt) {
-        const int ea = kt * IL + tid + 256 * m, eb = ea + 256;
-        S[contig_slot(ea >> 8, ea & 255)] = o0[kt];
-        S[contig_slot(eb >> 8, eb & 255)] = o1[kt];
+        for (int h = 0; h < 8; ++h) d[r][h] = ld_l2(in + (u64)h * Q + il0 + (u64)(tid + 256 * (m + r)));
+#pragma unroll
+      for (int r = 0; r < IPR; ++r) {
+        double2 o[KS];
+        top3_kept<KK>(d[r], rsel, o);
+#pragma unroll
+        for (int kt = 0; kt < KS; ++kt) {
+          const int e = kt * IL + tid + 256 * (m + r);
+          S[contig_slot(e >> 8, e & 255)] = o[kt];
+        }
       }
     }
     __syncthreads();

@@ -67,6 +67,16 @@ cudaError_t launch_dense_pipe(int mode, const DenseArgs& a_in, const DensePlan& 
   }
 #endif
   a.nslot = p.nslot;
+#if PTDR_DEV
+  {
+    // developer override of the scratch ring (a power of two <= the planned slots; the
+    // workspace holds p.nslot slots): a short ring reuses L2-resident lines
+    const char* es = getenv("PTDR_NSLOT");
+    const int v = es ? atoi(es) : 0;
+    if (v >= 2 && v <= p.nslot && (v & (v - 1)) == 0) a.nslot = v;
+    if (a.L > a.nslot - 1) a.L = a.nslot - 1;
+  }
+#endif
   a.slot_elems = p.slot_elems;
   PFN_cuTensorMapEncodeTiled_v12000 enc = encode_fn();
   if (!enc) return cudaErrorNotSupported;
@@ -118,6 +128,18 @@ cudaError_t launch_dense_pipe(int mode, const DenseArgs& a_in, const DensePlan& 
     }
 #endif
   }
+  // Acquire side of the dependency waits: the producer's relaxed counter read is followed
+  // by fence.proxy.async and a TMA bulk copy that reads the scratch through L2 (the point
+  // of coherence).  Stricter forms measured: fence.acq_rel.gpu after
+  // each wait costs 10 % at n = 15/16 (7.9 -> 8.8 ms); developer builds can switch
+  // between the forms (PTDR_ACQ = 0 relaxed, 1 fence, 2 ld.acquire).
+  a.acq_fence = 0;
+#if PTDR_DEV
+  {
+    const char* ea = getenv("PTDR_ACQ");
+    if (ea && ea[0] >= '0' && ea[0] <= '2') a.acq_fence = ea[0] - '0';
+  }
+#endif
   cudaError_t e = cudaMemsetAsync(a.ctr, 0, p.ctr_bytes, st);
   if (e != cudaSuccess) return e;
   a.trace = debug_trace_buffer();

@@ -65,7 +65,7 @@ struct TmapSet {
 
 struct TileMeta {
   int valid, phase, tile, seq;
-  unsigned chunk, pad0, pad1, pad2;
+  unsigned chunk, slot, pad1, pad2;
 };
 
 // Relaxed GPU-scope load of a completion counter.  No L1 invalidation (an acquire load
@@ -249,7 +249,7 @@ struct PipeCfg {
   // ptxas allocates under __launch_bounds__(THREADS, 1)); setmaxnreg.inc blocks until the
   // pool can satisfy it, so PROD_REGS x 128 + CONS_REGS x CONS_THREADS must fit in it.
   static constexpr int LAUNCH_REGS = ((65536 / THREADS) / 8) * 8 > 248 ? 248 : ((65536 / THREADS) / 8) * 8;
-  static constexpr int PROD_REGS = 32;
+  static constexpr int PROD_REGS = 40;
   static constexpr int CONS_REGS_RAW = ((THREADS * LAUNCH_REGS - PROD_REGS * 128) / CONS_THREADS / 8) * 8;
   static constexpr int CONS_REGS = CONS_REGS_RAW > 248 ? 248 : CONS_REGS_RAW;
   static_assert(CONS_REGS >= LAUNCH_REGS && PROD_REGS * 128 + CONS_REGS * CONS_THREADS <= THREADS * LAUNCH_REGS,
@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
           decode_ticket32(tk, M, C, (uint32_t)a.L, phX, chX, tlX);
           if (phX == 1) depX = &doneA[chX];
           else if (chX >= nslot) depX = &doneB[chX - nslot];
-          if (depX) dvX = ld_relaxed(depX);
+          if (depX) dvX = a.acq_fence == 2 ? ld_acquire(depX) : ld_relaxed(depX);
         }
       };
       int k = 0, ends = 0;
@@ -430,20 +430,25 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
           unsigned v = dvX;
           while (v < done_target) {
             __nanosleep(64);
-            v = ld_relaxed(depX);
+            v = a.acq_fence == 2 ? ld_acquire(depX) : ld_relaxed(depX);
           }
+          // developer variant: a fence after the wait (the acquire pattern of the PTX memory
+          // model); measured 10 % slower, see launch_dense_pipe
+          if (a.acq_fence == 1) asm volatile("fence.acq_rel.gpu;" ::: "memory");
         }
         trace_stamp(a.trace, k, 2);
         if (PTDR_ENABLE_TRACE && a.trace && blockIdx.x == 0 && k < kTraceTiles) a.trace[k * 16 + 8] = phX;
         double2* dst = stage0 + (size_t)s * TE;
         // one 16-byte and one 4-byte shared store instead of five
         *reinterpret_cast<int4*>(&meta[s]) = make_int4(1, phX, (int)tlX, k);
-        meta[s].chunk = chX;
+        const uint32_t gch = chX, slot = chX & slot_mask;
+        meta[s].chunk = gch;
+        meta[s].slot = slot;
         if (phX == 0 && MODE == MODE_GEN) {
           mbar_arrive(&full[s]);  // matrix-free: the consumers generate the tile's entries
         } else if (phX == 0) {
           mbar_arrive_expect_tx(&full[s], (uint32_t)Cfg::TB);
-          const uint32_t x0 = (uint32_t)a.x_base + (chX << XB);
+          const uint32_t x0 = (uint32_t)a.x_base + (gch << XB);
           const int t = HALF ? 31 - __clz(x0) : 0;
           const uint32_t cm = (uint32_t)a.colmask & ~(uint32_t)(W - 1);
           // peer-pull: all rows of a tile lie in one rank's shard (R >= rows per tile), so
@@ -467,7 +472,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
           // scratch written by other CTAs' generic stores, read by the async proxy
           fence_proxy_async_global();
           mbar_arrive_expect_tx(&full[s], (uint32_t)Cfg::TB);
-          const double2* src = a.scratch + ((size_t)(chX & slot_mask) << slot_shift) + ((size_t)tlX << LT);
+          const double2* src = a.scratch + ((size_t)slot << slot_shift) + ((size_t)tlX << LT);
           bulk_load(dst, src, (uint32_t)Cfg::TB, &full[s], pol_sl);
         }
         trace_stamp(a.trace, k, 3);
@@ -590,7 +595,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
     }
     double2* S = stage0 + (size_t)s * TE;
     const uint32_t chunk = m.chunk;
-    double2* Y = a.scratch + ((size_t)(chunk & slot_mask) << slot_shift);
+    double2* Y = a.scratch + ((size_t)m.slot << slot_shift);
     double2 v[16];
     if (m.phase == 0 && NR > 0) {
       // ---- phase A, early release: read the stage once, release it, exchange through X

@@ -45,7 +45,7 @@ constexpr uint64_t TE = 4096;  // elements per tile (64 KiB)
 // mode 0: self (read back own tile); 1: global queue; 2: per-die queue
 __global__ void __launch_bounds__(256) handoff_k(const double2* __restrict__ a, double2* scratch, double2* __restrict__ out,
                                                  uint64_t tiles, uint64_t ring_tiles, unsigned* flags, unsigned* tickets,
-                                                 const int* die_of_sm, uint64_t die0_tiles, int mode, int lag) {
+                                                 const int* die_of_sm, uint64_t die0_tiles, int mode, int lag, int discard) {
   __shared__ unsigned long long s_t;
   const int die = die_of_sm[smid()];
   unsigned* tk = tickets + (mode == 2 ? die : 0);
@@ -90,6 +90,13 @@ __global__ void __launch_bounds__(256) handoff_k(const double2* __restrict__ a, 
       const double2* r = scratch + ((mode == 2 ? (uint64_t)die * ring_tiles : 0) + ((k - lag) % ring_tiles)) * TE;
 #pragma unroll
       for (int j = 0; j < 16; ++j) v[j] = __ldcg(r + j * 256 + threadIdx.x);
+      if (discard) {
+        // drop the consumed scratch lines from L2 without write-back (as the pipeline does)
+        __syncthreads();
+        const char* rb = reinterpret_cast<const char*>(r);
+        for (int d = threadIdx.x; d < (int)(TE * 16 / 128); d += 256)
+          asm volatile("discard.global.L2 [%0], 128;" ::"l"(rb + (size_t)d * 128) : "memory");
+      }
 #pragma unroll
       for (int j = 0; j < 16; ++j) __stcs(out + t * TE + j * 256 + threadIdx.x, v[j]);
     }
@@ -172,28 +179,30 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  auto run = [&](const char* name, int mode, int mib, int lag, int cpb) {
+  auto run = [&](const char* name, int mode, int mib, int lag, int cpb, int discard) {
     const uint64_t ring = ((uint64_t)mib << 20) / (TE * 16);
     float best = 1e30f;
     for (int r = 0; r < 4; ++r) {
       cudaMemset(flags, 0, tiles * 4);
       cudaMemset(tickets, 0, 64);
       cudaEventRecord(e0);
-      handoff_k<<<sms * cpb, 256>>>(a, scratch, out, tiles, ring, flags, tickets, ddie, die0_tiles, mode, lag);
+      handoff_k<<<sms * cpb, 256>>>(a, scratch, out, tiles, ring, flags, tickets, ddie, die0_tiles, mode, lag, discard);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms;
       cudaEventElapsedTime(&ms, e0, e1);
       if (r > 0 && ms < best) best = ms;
     }
-    printf("%-6s ring %3d MiB lag %4d %d CTA/SM  %8.3f ms  %8.1f GB/s (32 B per element)\n", name, mib, lag, cpb,
-           best, 32.0 * n / best / 1e6);
+    printf("%-6s ring %3d MiB lag %4d %d CTA/SM discard %d  %8.3f ms  %8.1f GB/s (32 B per element)\n", name, mib,
+           lag, cpb, discard, best, 32.0 * n / best / 1e6);
   };
   for (int cpb : {2, 4}) {
-    run("self", 0, 32, 0, cpb);
-    for (int lag : {sms * cpb, 2 * sms * cpb}) {
-      run("any", 1, 128, lag, cpb);
-      run("die", 2, 64, lag / 2, cpb);
+    run("self", 0, 32, 0, cpb, 0);
+    for (int lag : {sms * cpb / 2, sms * cpb, 2 * sms * cpb}) {
+      const int mib = lag * 64 / 1024 * 2 + 16;   // ring covers twice the lag
+      run("any", 1, mib, lag, cpb, 0);
+      run("any", 1, mib, lag, cpb, 1);
+      run("die", 2, mib, lag / 2, cpb, 1);
     }
   }
   CK(cudaGetLastError());

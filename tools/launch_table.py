@@ -14,4 +14,4 @@ for r in rows[start:]:
 for (i, k), m in sorted(cur.items()):
     t = m.get("gpu__time_duration.sum", 0) / 1e3
     rd, wr = m.get("dram__bytes_read.sum", 0) / 1e6, m.get("dram__bytes_write.sum", 0) / 1e6
-    print(f"{i:3d} {k:48s} {t:9.1f} us  rd {rd:8.1f} MB  wr {wr:8.1f} MB  {(rd + wr) / max(t, 1e-9) / 1e3:6.2f} TB/s")
+    print(f"{i:3d} {k:48s} {t:9.1f} us  rd {rd:8.1f} MB  wr {wr:8.1f} MB  {(rd + wr) / max(t, 1e-9):6.2f} TB/s")

@@ -128,12 +128,13 @@ cudaError_t launch_dense_pipe(int mode, const DenseArgs& a_in, const DensePlan& 
     }
 #endif
   }
-  // Acquire side of the dependency waits: the producer's relaxed counter read is followed
-  // by fence.proxy.async and a TMA bulk copy that reads the scratch through L2 (the point
-  // of coherence).  Stricter forms measured: fence.acq_rel.gpu after
-  // each wait costs 10 % at n = 15/16 (7.9 -> 8.8 ms); developer builds can switch
-  // between the forms (PTDR_ACQ = 0 relaxed, 1 fence, 2 ld.acquire).
-  a.acq_fence = 0;
+  // Acquire side of the dependency waits: the producer reads the completion
+  // counters with ld.acquire.gpu, which synchronises with the signalers' red.release, then
+  // fence.proxy.async orders the async-proxy bulk copy of the scratch after it.  Measured
+  // (DESIGN.md section 7): free at n = 15/16 (7.84-7.93 vs 7.99-8.08 ms relaxed), while a
+  // fence.acq_rel.gpu after each wait costs 10 %; developer builds can switch between the
+  // forms (PTDR_ACQ = 0 relaxed, 1 fence, 2 ld.acquire).
+  a.acq_fence = 2;
 #if PTDR_DEV
   {
     const char* ea = getenv("PTDR_ACQ");

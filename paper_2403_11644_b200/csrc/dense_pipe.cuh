@@ -68,10 +68,10 @@ struct TileMeta {
   unsigned chunk, slot, pad1, pad2;
 };
 
-// Relaxed GPU-scope load of a completion counter.  No L1 invalidation (an acquire load
-// would emit CCTL.IVALL and stall the producer for a full L2 round trip per tile).  The
-// data the producer then reads is fetched by the TMA from L2 (the point of coherence)
-// in an instruction control-dependent on this value, after fence.proxy.async.global.
+// Completion counters are read with ld.acquire.gpu by default (the acquire half of the
+// signalers' red.release; measured free); the relaxed form below is a
+// developer variant.  Either way the scratch is then fetched by the TMA from L2 after
+// fence.proxy.async.global.
 __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
   unsigned v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

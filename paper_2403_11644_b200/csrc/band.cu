@@ -16,6 +16,7 @@
 #include <mutex>
 #include <vector>
 
+#include "dense_plan.h"
 #include "engine.cuh"
 #include "sm100_ptx.cuh"
 #include "internal.h"
@@ -652,13 +653,139 @@ __global__ void tri_split_small_kernel(const double2* __restrict__ band, double2
   }
 }
 
+// ---- L2-resident tail of a long vector family (top-bits-first x = 0 vectors) ------------
+// After top3_pass_kernel the family is `nvec` branches of 2^L elements (L = lam - 3 >= 17:
+// 32 MiB at n = 24), each still needing bits [8, 16) and [16, L).  Instead of two passes
+// over the whole family (each a DRAM round trip of all of it), one persistent kernel runs
+// both passes branch by branch: pass 1 of branch v reads it from DRAM and leaves it in L2,
+// pass 2 of v (which needs all of v's pass-1 tiles: a completion counter per branch) reads
+// it back from L2 and writes the result -- one DRAM round trip instead of two.  Ticket
+// order P1(0..look), P2(0), P1(look+1), P2(1), ... (decode_tail); a CTA only ever waits for
+// tiles with smaller tickets, which running CTAs hold, so progress is guaranteed.  Same
+// tiles, same order of operations per element as the two flat passes: bitwise identical.
+struct TailArgs {
+  const double2* in;  // branches after pass 0 (pass 1 runs in place on them)
+  double2* out;       // final output (pass 2)
+  int L, nvec, look;
+  double scale;
+  int zshift;
+  u64 zrank, px, zoff;
+  unsigned* ctr;      // [0] ticket, [1 .. nvec] pass-1 tiles done per branch
+};
+
+__device__ __forceinline__ void decode_tail(u64 t, u64 TP, u64 C, u64 look, int& phase, u64& v, u64& tile) {
+  const u64 lp1 = look + 1 < C ? look + 1 : C;
+  if (t < lp1 * TP) { phase = 0; v = t / TP; tile = t % TP; return; }
+  t -= lp1 * TP;
+  const u64 steady = C > look + 1 ? C - look - 1 : 0;
+  if (t < steady * 2 * TP) {
+    const u64 c = t / (2 * TP), o = t % (2 * TP);
+    if (o < TP) { phase = 1; v = c; tile = o; }
+    else { phase = 0; v = c + look + 1; tile = o - TP; }
+    return;
+  }
+  t -= steady * 2 * TP;
+  phase = 1;
+  v = steady + t / TP;
+  tile = t % TP;
+}
+
+__global__ void __launch_bounds__(kThreads, 2) tail_pipe_kernel(const __grid_constant__ TailArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* S = reinterpret_cast<double2*>(smem_raw);
+  __shared__ unsigned long long s_tk;
+  const u64 TP = (1ull << A.L) / (u64)kTileElems;  // tiles per pass per branch
+  const u64 total = 2ull * (u64)A.nvec * TP;
+  unsigned* doneP1 = A.ctr + 1;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_tk = atomicAdd(A.ctr, 1u);
+    __syncthreads();
+    const u64 tk = s_tk;
+    if (tk >= total) break;
+    int phase;
+    u64 v, tile;
+    decode_tail(tk, TP, (u64)A.nvec, (u64)A.look, phase, v, tile);
+    SegPass sp{};
+    sp.in = A.in;
+    sp.zshift = 63;
+    if (phase == 0) {
+      sp.out = const_cast<double2*>(A.in);
+      sp.b0 = 8;
+      sp.scale = 1.0;
+      flat_tile<8>(S, sp, v * TP + tile);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(&doneP1[v], 1u);
+      }
+    } else {
+      if (threadIdx.x == 0) {
+        while (ld_acquire(&doneP1[v]) < (unsigned)TP) __nanosleep(64);
+      }
+      __syncthreads();
+      sp.out = A.out;
+      sp.b0 = 16;
+      sp.scale = A.scale;
+      sp.zshift = A.zshift;
+      sp.zrank = A.zrank;
+      sp.px = A.px;
+      sp.zoff = A.zoff;
+      switch (A.L - 16) {
+        case 1: flat_tile<1>(S, sp, v * TP + tile); break;
+        case 2: flat_tile<2>(S, sp, v * TP + tile); break;
+        case 3: flat_tile<3>(S, sp, v * TP + tile); break;
+        case 4: flat_tile<4>(S, sp, v * TP + tile); break;
+        case 5: flat_tile<5>(S, sp, v * TP + tile); break;
+        case 6: flat_tile<6>(S, sp, v * TP + tile); break;
+        case 7: flat_tile<7>(S, sp, v * TP + tile); break;
+        default: flat_tile<8>(S, sp, v * TP + tile); break;
+      }
+    }
+  }
+}
+
+constexpr int kTailMinL = 17;  // branches of >= 2^17 elements (two tail passes: bits 8-15, 16..)
+constexpr int kTailMaxL = 24;  // pass 2 at most 8 bits
+
+static cudaError_t launch_tail(const WhtFamily& f, unsigned* ctr, cudaStream_t st, int* nl) {
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(tail_pipe_kernel), kBandSmem);
+  if (e != cudaSuccess) return e;
+  TailArgs A;
+  A.in = f.in;
+  A.out = f.final_out ? f.final_out : f.out;
+  A.L = f.lam;
+  A.nvec = (int)f.count;
+  A.look = 1;
+#if PTDR_DEV
+  {
+    const char* el = getenv("PTDR_TAIL_LOOK");
+    if (el && el[0] >= '0' && el[0] <= '3') A.look = el[0] - '0';
+  }
+#endif
+  A.scale = f.scale;
+  A.zshift = f.zshift;
+  A.zrank = f.zrank;
+  A.px = f.px;
+  A.zoff = f.zoff;
+  A.ctr = ctr;
+  if ((e = cudaMemsetAsync(ctr, 0, (size_t)(A.nvec + 1) * 4, st)) != cudaSuccess) return e;
+  const u64 tiles = 2ull * f.count * ((1ull << f.lam) / (u64)kTileElems);
+  u64 grid = (u64)device_sm_count() * 2;
+  if (grid > tiles) grid = tiles;
+  tail_pipe_kernel<<<(unsigned)grid, kThreads, kBandSmem, st>>>(A);
+  *nl += 1;
+  return cudaGetLastError();
+}
+
 // Workspace: [P/M segments: 2 * 2^n] (TRIDIAGONAL) + [x = 0 vector: 2^n] (world > 1: the
-// x = 0 intermediate when it does not fit the rank's output block).
+// x = 0 intermediate when it does not fit the rank's output block) + [tail counters].
+constexpr size_t kTailCtrBytes = 256;
 size_t band_workspace_bytes(int n, int structure, int world) {
   const size_t N = (size_t)1 << n;
   size_t b = structure == 4 ? 2 * N * 16 : 0;
   if (world > 1 && n > 12) b += N * 16;
-  return b;
+  return b + kTailCtrBytes;
 }
 
 cudaError_t launch_band(const double2* A, double2* out, int n, int structure, void* ws, int rank,
@@ -670,6 +797,10 @@ cudaError_t launch_band(const double2* A, double2* out, int n, int structure, vo
   const u64 zrank = world > 1 ? (u64)rank : 0ull;
   double2* PM = reinterpret_cast<double2*>(ws);
   double2* X0 = world > 1 ? PM + (structure == 4 ? 2 * N : 0) : nullptr;  // x = 0 scratch
+  unsigned* tail_ctr = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(ws) + band_workspace_bytes(n, structure, world) -
+                                                   kTailCtrBytes);
+  // the x = 0 family after top3_pass_kernel: its two remaining passes as the L2-resident tail
+  auto tail_ok = [](const WhtFamily& f) { return f.first_bit == 8 && f.lam >= kTailMinL && f.lam <= kTailMaxL; };
   const int sms = device_sm_count();
   // top-bits-first geometry: gp of the rank's bits select branches (at most the 3 top ones),
   // the remaining g - gp bits are a slice filter of the last pass
@@ -719,6 +850,7 @@ cudaError_t launch_band(const double2* A, double2* out, int n, int structure, vo
     // nonzero only for x = 2^n - 1, so alpha(2^n - 1, z) = 2^-n i^{popcount(z)} WHT(a)[z].
     WhtFamily f;
     if ((e = x0_family(A, structure == 5 ? N - 1 : 0ull, f)) != cudaSuccess) return e;
+    if (tail_ok(f)) return launch_tail(f, tail_ctr, st, nl);
     return run_families(&f, 1, st, nl);
   }
   // TRIDIAGONAL: A = [sub | main | sup].  Segments t with lam = n - t - 1 >= kTopMin: fused
@@ -747,7 +879,12 @@ cudaError_t launch_band(const double2* A, double2* out, int n, int structure, vo
   // block 0 (x = 0): WHT(main) scaled; blocks t+1: P_t / M_t
   WhtFamily fam[kMaxSeg];
   int nf = 0;
-  if ((e = x0_family(A + N, 0ull, fam[nf++])) != cudaSuccess) return e;
+  if ((e = x0_family(A + N, 0ull, fam[nf])) != cudaSuccess) return e;
+  if (tail_ok(fam[nf])) {
+    if ((e = launch_tail(fam[nf], tail_ctr, st, nl)) != cudaSuccess) return e;
+  } else {
+    ++nf;
+  }
   for (int t = 0; t < n; ++t) {
     const int lam = n - t - 1;
     const u64 seg = N - (N >> t);

@@ -59,8 +59,9 @@ def test_workspace_is_deterministic_and_small(L):
             # than the input itself
             assert a <= (2 << 30) + (1 << 20), (n, s, a)
             assert a <= 16 * 4 ** n + (1 << 20), (n, s, a)
-    assert ptdr.workspace_bytes(24, "diagonal") == 0
-    assert ptdr.workspace_bytes(24, "tridiagonal") == 2 * (1 << 24) * 16
+    # band paths: 256 B of tail-pipeline counters (+ the P/M segments for the tridiagonal)
+    assert ptdr.workspace_bytes(24, "diagonal") == 256
+    assert ptdr.workspace_bytes(24, "tridiagonal") == 2 * (1 << 24) * 16 + 256
     with pytest.raises(ptdr.PtdrError):
         ptdr.workspace_bytes(15, "hermitian", 2)     # sharding is GENERAL only
     with pytest.raises(ptdr.PtdrError):
@@ -142,7 +143,7 @@ def test_band_xmask_list_matches_definition(L, s):
 def test_anti_diagonal_counts(L):
     assert ptdr.input_count(10, "anti_diagonal") == 1 << 10
     assert ptdr.output_count(10, "anti_diagonal") == 1 << 10
-    assert ptdr.workspace_bytes(24, "anti_diagonal") == 0
+    assert ptdr.workspace_bytes(24, "anti_diagonal") == 256
     assert L.ptdr_max_n(5) == 28
 
 

@@ -25,7 +25,7 @@
 namespace ptdr {
 
 // Vectors of at least 2^kTopMin elements run their three top butterfly levels first (the
-// z-sharded paths read them once and transform only the rank's part; see top3_pass_kernel).
+// z-sharded paths read them once and transform only the rank's part; see topk_pass_kernel).
 constexpr int kTopMin = 15;
 
 // ---- flat WHT pass over bits [b0, b0+K) of a contiguous array ---------------------
@@ -450,79 +450,64 @@ cudaError_t run_families(const WhtFamily* fam, int nfam, cudaStream_t st, int* n
 // bit first) and keeps all eight branches, so every rank's outputs are bitwise the one-GPU
 // values.  Used for vectors of at least 2^kTopMin elements; shorter ones stay replicated.
 
-// W over the 3 top index bits for output zt, levels in descending bit order: pairs
-// (h, h + 4) first, then (h, h + 2), then (h, h + 1); a z bit of 0 takes the sum.
-__device__ __forceinline__ double2 top3_value(const double2 (&d)[8], unsigned zt) {
-  double2 a[4], b[2];
-#pragma unroll
-  for (int h = 0; h < 4; ++h) a[h] = (zt & 4u) ? csub(d[h], d[h + 4]) : cadd(d[h], d[h + 4]);
-#pragma unroll
-  for (int h = 0; h < 2; ++h) b[h] = (zt & 2u) ? csub(a[h], a[h + 2]) : cadd(a[h], a[h + 2]);
-  return (zt & 1u) ? csub(b[0], b[1]) : cadd(b[0], b[1]);
-}
-// The KS = 2^KK kept outputs zt = (rsel << KK) | kt, kt = 0..KS-1, as one butterfly network
-// sharing its partial sums (12 complex butterflies for all eight on one GPU); the top bits
-// fixed by rsel pick one branch per level (a select, no divergence).  Every output is the
-// same sequence of operations as top3_value(d, zt), so its value is bitwise the same.
+// W over the TB top index bits for the kept outputs zt = (rsel << KK) | kt, kt < 2^KK,
+// levels in descending bit order (bit TB-1 first: pairs (h, h + 2^(TB-1)), ...); a z bit of
+// 0 takes the sum.  The TB - KK top bits are fixed by rsel: each of those levels keeps one
+// branch (a select, no divergence); the last KK levels are full butterflies.  Every kept
+// output is the same sequence of operations whatever KK is -- on one GPU (KK = TB) all
+// 2^TB outputs share their partial sums (TB 2^(TB-1) butterflies) -- so a rank's values are
+// bitwise the one-GPU values.
 __device__ __forceinline__ double2 bfly(double2 a, double2 b, bool diff) { return diff ? csub(a, b) : cadd(a, b); }
-template <int KK>
-__device__ __forceinline__ void top3_kept(const double2 (&d)[8], unsigned rsel, double2* o) {
-  if constexpr (KK == 3) {
-    double2 a[2][4], b[2][2][2];
+// fixed level S (S >= KK) and below, compile-time unrolled (a runtime level index would
+// put the array in local memory)
+template <int S, int KK, int N>
+__device__ __forceinline__ void topk_fixed(double2 (&c)[N], unsigned zt0) {
+  if constexpr (S >= KK) {
+    const bool diff = ((zt0 >> S) & 1u) != 0;  // keep branch (zt0 >> S) & 1
 #pragma unroll
-    for (int h = 0; h < 4; ++h) {
-      a[0][h] = cadd(d[h], d[h + 4]);
-      a[1][h] = csub(d[h], d[h + 4]);
-    }
-#pragma unroll
-    for (int b2 = 0; b2 < 2; ++b2)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        b[b2][0][h] = cadd(a[b2][h], a[b2][h + 2]);
-        b[b2][1][h] = csub(a[b2][h], a[b2][h + 2]);
-      }
-#pragma unroll
-    for (int kt = 0; kt < 8; ++kt) o[kt] = bfly(b[kt >> 2][(kt >> 1) & 1][0], b[kt >> 2][(kt >> 1) & 1][1], kt & 1);
-  } else {
-    const unsigned zt0 = rsel << KK;  // the fixed bits of every kept zt
-    double2 a[4];
-#pragma unroll
-    for (int h = 0; h < 4; ++h) a[h] = bfly(d[h], d[h + 4], (zt0 >> 2) & 1u);
-    if constexpr (KK == 2) {
-      double2 b[2][2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        b[0][h] = cadd(a[h], a[h + 2]);
-        b[1][h] = csub(a[h], a[h + 2]);
-      }
-#pragma unroll
-      for (int kt = 0; kt < 4; ++kt) o[kt] = bfly(b[kt >> 1][0], b[kt >> 1][1], kt & 1);
-    } else {
-      double2 b[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) b[h] = bfly(a[h], a[h + 2], (zt0 >> 1) & 1u);
-      if constexpr (KK == 1) {
-        o[0] = cadd(b[0], b[1]);
-        o[1] = csub(b[0], b[1]);
-      } else {
-        o[0] = bfly(b[0], b[1], zt0 & 1u);
-      }
-    }
+    for (int j = 0; j < (1 << S); ++j) c[j] = bfly(c[j], c[j + (1 << S)], diff);
+    topk_fixed<S - 1, KK, N>(c, zt0);
   }
 }
+template <int S, int N>
+__device__ __forceinline__ void topk_full(double2 (&c)[N]) {
+  if constexpr (S >= 0) {  // kept bits: full butterflies in place, bit S
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      if constexpr (true) {
+        if ((j >> S) & 1) continue;
+        const double2 x = c[j], y = c[j | (1 << S)];
+        c[j] = cadd(x, y);
+        c[j | (1 << S)] = csub(x, y);
+      }
+    }
+    topk_full<S - 1, N>(c);
+  }
+}
+template <int TB, int KK>
+__device__ __forceinline__ void topk_kept(const double2 (&d)[1 << TB], unsigned rsel, double2* o) {
+  double2 c[1 << TB];
+#pragma unroll
+  for (int h = 0; h < (1 << TB); ++h) c[h] = d[h];
+  topk_fixed<TB - 1, KK, (1 << TB)>(c, rsel << KK);
+  double2 k[1 << KK];
+#pragma unroll
+  for (int j = 0; j < (1 << KK); ++j) k[j] = c[j];
+  topk_full<KK - 1, (1 << KK)>(k);
+#pragma unroll
+  for (int kt = 0; kt < (1 << KK); ++kt) o[kt] = k[kt];
+}
 
-// Pass 0 of a long single vector (lam >= kTopMin): the three top levels, then bits 4-7 and
-// 0-3 of il exactly as contig8_tile orders them.  A tile holds KS = 2^k_keep kept top-bit
-// branches x IL = 4096 / KS consecutive il (16 fibres of 256); it reads 8 x IL elements
-// (8 runs of IL contiguous, coalesced) and writes KS runs of IL: out[kt 2^(lam-3) + il].
-// zt = (rsel << k_keep) | kt.
-template <int KK>
-__global__ void __launch_bounds__(kThreads, 2) top3_pass_kernel(const double2* __restrict__ in, double2* out,
+// Pass 0 of a long single vector: the TB top levels, then bits 4-7 and 0-3 of il exactly as
+// contig8_tile orders them.  A tile holds KS = 2^KK kept top-bit branches x IL = 4096 / KS
+// consecutive il (16 fibres of 256); it reads 2^TB x IL elements (2^TB runs of IL
+// contiguous, coalesced) and writes KS runs of IL: out[kt 2^(lam-TB) + il].
+template <int TB, int KK>
+__global__ void __launch_bounds__(kThreads, 2) topk_pass_kernel(const double2* __restrict__ in, double2* out,
                                                                 int lam, unsigned rsel) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* S = reinterpret_cast<double2*>(smem_raw);
-  constexpr int k_keep = KK;
-  const int L = lam - 3;
+  const int L = lam - TB;
   constexpr int KS = 1 << KK;
   constexpr int IL = kTileElems >> KK;
   const u64 Q = 1ull << L;
@@ -530,19 +515,18 @@ __global__ void __launch_bounds__(kThreads, 2) top3_pass_kernel(const double2* _
   const int tid = threadIdx.x;
   for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const u64 il0 = tile * (u64)IL;
-    // stage 0: top levels; IPR il per thread per round (8 IPR loads in flight: 16 when all
-    // eight branches are kept, 32 when fewer outputs leave registers free)
-    constexpr int IPR = KK >= 2 ? 2 : 4;
+    // stage 0: top levels; IPR il per thread per round (16-32 loads in flight)
+    constexpr int IPR = TB == 4 ? (KK <= 1 ? 2 : 1) : 2;
     for (int m = 0; m < IL / 256; m += IPR) {
-      double2 d[IPR][8];
+      double2 d[IPR][1 << TB];
 #pragma unroll
       for (int r = 0; r < IPR; ++r)
 #pragma unroll
-        for (int h = 0; h < 8; ++h) d[r][h] = ld_l2(in + (u64)h * Q + il0 + (u64)(tid + 256 * (m + r)));
+        for (int h = 0; h < (1 << TB); ++h) d[r][h] = ld_l2(in + (u64)h * Q + il0 + (u64)(tid + 256 * (m + r)));
 #pragma unroll
       for (int r = 0; r < IPR; ++r) {
         double2 o[KS];
-        top3_kept<KK>(d[r], rsel, o);
+        topk_kept<TB, KK>(d[r], rsel, o);
 #pragma unroll
         for (int kt = 0; kt < KS; ++kt) {
           const int e = kt * IL + tid + 256 * (m + r);
@@ -583,12 +567,12 @@ __global__ void __launch_bounds__(kThreads, 2) top3_pass_kernel(const double2* _
   }
 }
 
-template <int KK>
-static cudaError_t launch_top3(const double2* in, double2* out, int lam, unsigned rsel, unsigned grid,
+template <int TB, int KK>
+static cudaError_t launch_topk(const double2* in, double2* out, int lam, unsigned rsel, unsigned grid,
                                cudaStream_t st) {
-  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(top3_pass_kernel<KK>), kBandSmem);
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(topk_pass_kernel<TB, KK>), kBandSmem);
   if (e != cudaSuccess) return e;
-  top3_pass_kernel<KK><<<grid, kThreads, kBandSmem, st>>>(in, out, lam, rsel);
+  topk_pass_kernel<TB, KK><<<grid, kThreads, kBandSmem, st>>>(in, out, lam, rsel);
   return cudaGetLastError();
 }
 
@@ -624,8 +608,8 @@ __global__ void __launch_bounds__(256) tri_split_top3_kernel(const double2* __re
     double2* Mt = Pt + ((u64)KS << Lb);
     const u64 hl = il >> (t + 1);
     double2 oP[KS], oM[KS];
-    top3_kept<KK>(P, rsel, oP);
-    top3_kept<KK>(M, rsel, oM);
+    topk_kept<3, KK>(P, rsel, oP);
+    topk_kept<3, KK>(M, rsel, oM);
 #pragma unroll
     for (int kt = 0; kt < KS; ++kt) {
       st_l2(Pt + ((u64)kt << Lb) + hl, oP[kt]);
@@ -654,8 +638,8 @@ __global__ void tri_split_small_kernel(const double2* __restrict__ band, double2
 }
 
 // ---- L2-resident tail of a long vector family (top-bits-first x = 0 vectors) ------------
-// After top3_pass_kernel the family is `nvec` branches of 2^L elements (L = lam - 3 >= 17:
-// 32 MiB at n = 24), each still needing bits [8, 16) and [16, L).  Instead of two passes
+// After topk_pass_kernel the family is `nvec` branches of 2^L elements (L = lam - 4 >= 17:
+// 16 MiB each at n = 24), each still needing bits [8, 16) and [16, L).  Instead of two passes
 // over the whole family (each a DRAM round trip of all of it), one persistent kernel runs
 // both passes branch by branch: pass 1 of branch v reads it from DRAM and leaves it in L2,
 // pass 2 of v (which needs all of v's pass-1 tiles: a completion counter per branch) reads
@@ -799,7 +783,7 @@ cudaError_t launch_band(const double2* A, double2* out, int n, int structure, vo
   double2* X0 = world > 1 ? PM + (structure == 4 ? 2 * N : 0) : nullptr;  // x = 0 scratch
   unsigned* tail_ctr = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(ws) + band_workspace_bytes(n, structure, world) -
                                                    kTailCtrBytes);
-  // the x = 0 family after top3_pass_kernel: its two remaining passes as the L2-resident tail
+  // the x = 0 family after topk_pass_kernel: its two remaining passes as the L2-resident tail
   auto tail_ok = [](const WhtFamily& f) { return f.first_bit == 8 && f.lam >= kTailMinL && f.lam <= kTailMaxL; };
   const int sms = device_sm_count();
   // top-bits-first geometry: gp of the rank's bits select branches (at most the 3 top ones),
@@ -812,27 +796,43 @@ cudaError_t launch_band(const double2* A, double2* out, int n, int structure, vo
   // output block 0 of `out` (2^n / world elements), px = X-mask phase.
   auto x0_family = [&](const double2* src, u64 px, WhtFamily& f) -> cudaError_t {
     if (n >= kTopMin) {
-      // top levels + bits 0-7 in one pass into the rank's KS branches, then bits 8.. of the
-      // 2^(n-3) branches; ranks beyond the top 3 bits filter their slice in the last pass
-      double2* mid = (g <= 3) ? out : X0;
-      u64 tiles = ((N >> 3) / (u64)(kTileElems >> k_keep));
+      // top levels + bits 0-7 in one pass into the rank's kept branches (the top 4 bits from
+      // n = 16 on: 16 branches of 2^(n-4), short enough for the L2-resident tail; 3 at
+      // n = 15), then bits 8.. of the branches; ranks beyond the top TB bits filter their
+      // slice in the last pass
+      const int TB = n >= 16 ? 4 : 3;
+      const int gx = g < TB ? g : TB;
+      const int kx = TB - gx;
+      const unsigned rx = (unsigned)(world > 1 ? (rank >> (g - gx)) : 0);
+      double2* mid = (g <= TB) ? out : X0;
+      u64 tiles = ((N >> TB) / (u64)(kTileElems >> kx));
       u64 grid = (u64)sms * 2;
       if (grid > tiles) grid = tiles;
-      switch (k_keep) {
-        case 3: e = launch_top3<3>(src, mid, n, rsel, (unsigned)grid, st); break;
-        case 2: e = launch_top3<2>(src, mid, n, rsel, (unsigned)grid, st); break;
-        case 1: e = launch_top3<1>(src, mid, n, rsel, (unsigned)grid, st); break;
-        default: e = launch_top3<0>(src, mid, n, rsel, (unsigned)grid, st); break;
+      const unsigned gr = (unsigned)grid;
+      if (TB == 4) {
+        switch (kx) {
+          case 4: e = launch_topk<4, 4>(src, mid, n, rx, gr, st); break;
+          case 3: e = launch_topk<4, 3>(src, mid, n, rx, gr, st); break;
+          case 2: e = launch_topk<4, 2>(src, mid, n, rx, gr, st); break;
+          case 1: e = launch_topk<4, 1>(src, mid, n, rx, gr, st); break;
+          default: e = launch_topk<4, 0>(src, mid, n, rx, gr, st); break;
+        }
+      } else {
+        switch (kx) {
+          case 3: e = launch_topk<3, 3>(src, mid, n, rx, gr, st); break;
+          case 2: e = launch_topk<3, 2>(src, mid, n, rx, gr, st); break;
+          case 1: e = launch_topk<3, 1>(src, mid, n, rx, gr, st); break;
+          default: e = launch_topk<3, 0>(src, mid, n, rx, gr, st); break;
+        }
       }
       if (e != cudaSuccess) return e;
       *nl += 1;
-      if ((e = cudaGetLastError()) != cudaSuccess) return e;
-      f = WhtFamily{mid, mid, n - 3, 1ull << k_keep, scale};
+      f = WhtFamily{mid, mid, n - TB, 1ull << kx, scale};
       f.first_bit = 8;
       f.final_out = out;
-      f.zshift = g > 3 ? n - g : 63;
-      f.zrank = g > 3 ? (u64)(rank & ((1 << (g - 3)) - 1)) : 0ull;
-      f.zoff = (u64)rsel << (n - gp);
+      f.zshift = g > TB ? n - g : 63;
+      f.zrank = g > TB ? (u64)(rank & ((1 << (g - TB)) - 1)) : 0ull;
+      f.zoff = (u64)rx << (n - gx);
       f.px = px;
       return cudaSuccess;
     }

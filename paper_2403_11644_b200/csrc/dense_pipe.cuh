@@ -19,6 +19,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
+#include <numeric>
 #include <mutex>
 
 #include "dense_impl.cuh"
@@ -347,15 +348,23 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
   constexpr int R = Cfg::R, TE = Cfg::TE, GT = Cfg::GT, W = Cfg::W;
   constexpr bool HALF = (MODE == MODE_HERM_HALF || MODE == MODE_SYM_HALF);
   constexpr int FB = TE >> M;  // phase-B fibers per tile
+  constexpr int kLcm = NS * NG / std::gcd(NS, NG);
   constexpr int LFB = LT - M;
   static_assert(M >= 4 && M <= 8 && LFB <= XB + 4, "phase-B fibre length 2^4..2^8");
   static_assert(R >= XB && R - 4 >= 1 && R - 4 <= 4, "phase-A tile geometry");
   extern __shared__ __align__(1024) unsigned char smem[];
   double2* stage0 = reinterpret_cast<double2*>(smem);
   double2* xbuf = reinterpret_cast<double2*>(smem + NS * Cfg::TB);  // [NG][XE] (NR > 0)
+  // full barriers per (stage, group): tile k lands in stage k % NS for group k % NG, so the
+  // barrier full[s NG + g] completes once per LCM = lcm(NS, NG) tiles and a group waiting for
+  // tile k can never see an older phase of it (the previous one, tile k - LCM, is its own
+  // and already consumed): a plain parity wait, the warps sleep in hardware until the data
+  // lands (no polling of a sequence number)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * Cfg::TB + NG * Cfg::XE * 16);
-  uint64_t* empty = full + NS;
-  TileMeta* meta = reinterpret_cast<TileMeta*>(empty + NS);
+  uint64_t* empty = full + NS * NG;
+  // 32-byte aligned (the producer publishes a tile's metadata with a 16-byte store)
+  TileMeta* meta = reinterpret_cast<TileMeta*>(
+      (reinterpret_cast<uintptr_t>(empty + NS) + 31) & ~static_cast<uintptr_t>(31));
   constexpr int SIGD = Cfg::SIGD;
   uint64_t* sigbar = reinterpret_cast<uint64_t*>(meta + NS);  // [NG][SIGD], count GW
   uint64_t* sigfree = sigbar + NG * SIGD;                       // [NG][SIGD], count 1
@@ -371,8 +380,8 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
   const unsigned done_target = 1u << M;  // one completion signal per tile
 
   if (threadIdx.x == 0) {
+    for (int i = 0; i < NS * NG; ++i) mbar_init(&full[i], 1);
     for (int s = 0; s < NS; ++s) {
-      mbar_init(&full[s], 1);
       mbar_init(&empty[s], GW);
       meta[s].seq = -1;
     }
@@ -415,6 +424,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
                          const uint32_t& tlX, const unsigned* const& depX,
                          const unsigned& dvX) -> bool {
         const int s = k % NS;
+        uint64_t* fullk = &full[s * NG + k % NG];
         trace_stamp(a.trace, k, 0);
         if (k >= NS) mbar_wait(&empty[s], (uint32_t)((k / NS) - 1) & 1u);
         trace_stamp(a.trace, k, 1);
@@ -422,7 +432,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
           // one invalid tile per group ends the consumers
           meta[s].valid = 0;
           meta[s].seq = k;
-          mbar_arrive(&full[s]);
+          mbar_arrive(fullk);
           ++k;
           return ++ends == NG;
         }
@@ -445,9 +455,9 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
         meta[s].chunk = gch;
         meta[s].slot = slot;
         if (phX == 0 && MODE == MODE_GEN) {
-          mbar_arrive(&full[s]);  // matrix-free: the consumers generate the tile's entries
+          mbar_arrive(fullk);  // matrix-free: the consumers generate the tile's entries
         } else if (phX == 0) {
-          mbar_arrive_expect_tx(&full[s], (uint32_t)Cfg::TB);
+          mbar_arrive_expect_tx(fullk, (uint32_t)Cfg::TB);
           const uint32_t x0 = (uint32_t)a.x_base + (gch << XB);
           const int t = HALF ? 31 - __clz(x0) : 0;
           const uint32_t cm = (uint32_t)a.colmask & ~(uint32_t)(W - 1);
@@ -466,14 +476,14 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
             uint32_t row0 = HALF ? insert0_32(iv0, t) : iv0;
             if constexpr ((kDiag & 2) != 0) row0 &= 255u;
             const uint32_t col0 = (row0 ^ x0) & cm;
-            tma_load_2d(dst + rb * W * W, tm, (int)(col0 * 2u), (int)(row0 & rmask), &full[s], pol);
+            tma_load_2d(dst + rb * W * W, tm, (int)(col0 * 2u), (int)(row0 & rmask), fullk, pol);
           }
         } else {
           // scratch written by other CTAs' generic stores, read by the async proxy
           fence_proxy_async_global();
-          mbar_arrive_expect_tx(&full[s], (uint32_t)Cfg::TB);
+          mbar_arrive_expect_tx(fullk, (uint32_t)Cfg::TB);
           const double2* src = a.scratch + ((size_t)slot << slot_shift) + ((size_t)tlX << LT);
-          bulk_load(dst, src, (uint32_t)Cfg::TB, &full[s], pol_sl);
+          bulk_load(dst, src, (uint32_t)Cfg::TB, fullk, pol_sl);
         }
         trace_stamp(a.trace, k, 3);
         ++k;
@@ -582,11 +592,9 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
     const int s = k % NS;
     const int gtid = fresh_gtid();
     const int lane = fresh_lane();
-    // stages are shared round-robin by the groups, so a parity wait alone could match an
-    // older phase: first wait until the producer has published tile k in this stage
+    // tile k: stage k % NS, this group's full barrier of that stage (phase k / kLcm)
     if (gtid == 0) trace_stamp(a.trace, k, 4);
-    while (*reinterpret_cast<volatile int*>(&meta[s].seq) != k) __nanosleep(20);
-    mbar_wait(&full[s], (uint32_t)(k / NS) & 1u);
+    mbar_wait(&full[s * NG + g], (uint32_t)(k / kLcm) & 1u);
     if (gtid == 0) trace_stamp(a.trace, k, 5);
     const TileMeta m = meta[s];
     if (!m.valid) {

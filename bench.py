@@ -47,6 +47,9 @@ def _args():
                    help="N > 1, NCCL exchange: X-mask sub-ranges per rank whose all-to-alls overlap "
                         "the decomposition of the previous sub-range (1 = exchange, then decompose)")
     p.add_argument("--nccl-timeout", type=float, default=300.0)
+    p.add_argument("--force-multi", action="store_true",
+                   help="run the N > 1 code path (NCCL group, sub-range exchange, combined roofline, "
+                        "checks) even at --gpus 1: a one-GPU test of that path")
     p.add_argument("--dry-run", action="store_true",
                    help="N > 1: every rank reports (rank, world) and exits before touching CUDA "
                         "(CPU test of the self-spawn path)")
@@ -230,7 +233,7 @@ def main():
     if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # one rank per GPU: relaunch under torch.distributed.run (rank 0 prints the line)
         return subprocess.call(spawn_cmd(a.gpus, sys.argv[1:], _free_port()))
-    if a.gpus > 1:
+    if a.gpus > 1 or a.force_multi:
         return main_multi(a)
     return main_single(a)
 
@@ -406,9 +409,12 @@ def main_multi(a):
         print(json.dumps({"dry_run": True, "rank": rank, "world": world, "local_rank": local,
                           "master_addr": os.environ.get("MASTER_ADDR")}), flush=True)
         return 0
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")       # --force-multi without torchrun
+    os.environ.setdefault("MASTER_PORT", str(_free_port()))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev, timeout=timedelta(seconds=a.nccl_timeout))
+    dist.init_process_group("nccl", device_id=dev, timeout=timedelta(seconds=a.nccl_timeout),
+                            rank=rank, world_size=world)
     n = a.n
     N = 1 << n
     coeffs_total = 1 << (2 * n)

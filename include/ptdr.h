@@ -177,6 +177,13 @@ ptdr_status ptdr_decompose_padded_async(const ptdr_c128* A, uint64_t m, uint64_t
 ptdr_status ptdr_decompose_xshard_async(const ptdr_c128* A_local, int n, int rank, int world,
                                         ptdr_c128* out_local, void* workspace, size_t ws_bytes,
                                         void* stream);
+/* The same, with the pipeline kernel limited to max_ctas persistent CTAs (0 = one per SM):
+ * the SMs left free let a concurrent collective on another stream (the next sub-range's
+ * all-to-all) run beside the decomposition instead of after it.
+ * Results do not depend on max_ctas. */
+ptdr_status ptdr_decompose_xshard_ex_async(const ptdr_c128* A_local, int n, int rank, int world,
+                                           ptdr_c128* out_local, void* workspace, size_t ws_bytes,
+                                           int max_ctas, void* stream);
 
 /* Matrix-free input ("no need to store the input matrix ... from a
  * function"): the GENERAL matrix of the seeded generator (ptdr_generate_dense_async,

@@ -58,6 +58,8 @@ def lib():
         L.ptdr_decompose_inplace_async.restype = i32
         L.ptdr_decompose_host.argtypes = [vp, i32, i32, vp]
         L.ptdr_decompose_xshard_async.argtypes = [vp, i32, i32, i32, vp, vp, sz, vp]
+        L.ptdr_decompose_xshard_ex_async.argtypes = [vp, i32, i32, i32, vp, vp, sz, i32, vp]
+        L.ptdr_decompose_xshard_ex_async.restype = i32
         L.ptdr_decompose_zshard_async.argtypes = [vp, i32, i32, i32, i32, vp, vp, sz, vp]
         L.ptdr_decompose_zshard_async.restype = i32
         L.ptdr_band_xmask_count.argtypes = [i32, i32]
@@ -388,8 +390,9 @@ class HostPlan:
 
 
 def decompose_xshard(A_local, n: int, rank: int, world: int, out=None, workspace=None,
-                     stream=None):
-    """Per-rank decomposition of the X-mask shard (after the all-to-all)."""
+                     stream=None, max_ctas: int = 0):
+    """Per-rank decomposition of the X-mask shard (after the all-to-all).  max_ctas > 0
+    caps the pipeline's persistent grid (SMs left to a concurrent collective)."""
     import torch
 
     if world < 1 or world & (world - 1) or not 0 <= rank < world:
@@ -398,11 +401,11 @@ def decompose_xshard(A_local, n: int, rank: int, world: int, out=None, workspace
     _require_cuda_c128(A_local, "A_local", count)
     out = _out(out, count, A_local.device, stream)
     workspace = _workspace(workspace, n, "general", world, A_local.device, stream)
-    st = lib().ptdr_decompose_xshard_async(ctypes.c_void_p(A_local.data_ptr()), n, rank, world,
-                                           ctypes.c_void_p(out.data_ptr()),
-                                           ctypes.c_void_p(workspace.data_ptr()),
-                                           workspace.numel(), _stream_ptr(stream))
-    _check(st, "ptdr_decompose_xshard_async")
+    st = lib().ptdr_decompose_xshard_ex_async(ctypes.c_void_p(A_local.data_ptr()), n, rank, world,
+                                              ctypes.c_void_p(out.data_ptr()),
+                                              ctypes.c_void_p(workspace.data_ptr()),
+                                              workspace.numel(), int(max_ctas), _stream_ptr(stream))
+    _check(st, "ptdr_decompose_xshard_ex_async")
     return out
 
 

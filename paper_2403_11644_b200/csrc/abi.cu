@@ -317,9 +317,9 @@ ptdr_status ptdr_decompose_async(const ptdr_c128* A, int n, int structure, ptdr_
   return r;
 }
 
-ptdr_status ptdr_decompose_xshard_async(const ptdr_c128* A_local, int n, int rank, int world,
-                                        ptdr_c128* out_local, void* workspace, size_t ws_bytes,
-                                        void* stream) {
+ptdr_status ptdr_decompose_xshard_ex_async(const ptdr_c128* A_local, int n, int rank, int world,
+                                           ptdr_c128* out_local, void* workspace, size_t ws_bytes,
+                                           int max_ctas, void* stream) {
   g_last_launches = 0;
   if (world < 1 || (world & (world - 1))) return fail(PTDR_EINVAL, "world must be a power of two");
   if (rank < 0 || rank >= world) return fail(PTDR_EINVAL, "rank out of range");
@@ -344,10 +344,17 @@ ptdr_status ptdr_decompose_xshard_async(const ptdr_c128* A_local, int n, int ran
   a.x_base = (uint64_t)rank * R;
   a.nchunks = p.nchunks;
   a.scratch = reinterpret_cast<double2*>(reinterpret_cast<char*>(workspace) + p.ctr_bytes);
+  a.max_ctas = max_ctas > 0 ? max_ctas : 0;
   int nl = 0;
   ptdr_status r = launch_mode(MODE_GENERAL, a, p, reinterpret_cast<cudaStream_t>(stream), &nl);
   g_last_launches = nl;
   return r;
+}
+
+ptdr_status ptdr_decompose_xshard_async(const ptdr_c128* A_local, int n, int rank, int world,
+                                        ptdr_c128* out_local, void* workspace, size_t ws_bytes,
+                                        void* stream) {
+  return ptdr_decompose_xshard_ex_async(A_local, n, rank, world, out_local, workspace, ws_bytes, 0, stream);
 }
 
 // ---- matrix-free input ------------------------------------

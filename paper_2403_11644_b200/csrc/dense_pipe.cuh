@@ -817,7 +817,11 @@ static cudaError_t launch_pipe_impl(const TmapSet& map, const DenseArgs& a, cuda
   constexpr auto kern = dense_pipe_kernel<LT, XB, GW, NG, NS, NR, M, MODE>;
   const cudaError_t err = ensure_smem_attr(reinterpret_cast<const void*>(kern), Cfg::SMEM);
   if (err != cudaSuccess) return err;
-  kern<<<device_sm_count(), Cfg::THREADS, Cfg::SMEM, st>>>(map, a);
+  // one persistent CTA per SM, or fewer when the caller leaves SMs to a concurrent
+  // collective (DenseArgs::max_ctas; tickets are dynamic, any grid size is correct)
+  int grid = device_sm_count();
+  if (a.max_ctas > 0 && a.max_ctas < grid) grid = a.max_ctas;
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(map, a);
   return cudaGetLastError();
 }
 

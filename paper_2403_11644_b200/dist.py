@@ -53,8 +53,14 @@ def exchange_async(send: torch.Tensor, group=None, recv: torch.Tensor | None = N
     return recv, works
 
 
+# SMs the decomposition of a sub-range leaves to the next sub-range's all-to-all (NCCL's
+# kernels need SMs too; the persistent pipeline otherwise takes every SM and the exchange
+# would only start after it).  The last sub-range, with nothing left in flight, takes all.
+COMM_SMS = 16
+
+
 def decompose_sharded(send: torch.Tensor, n: int, group=None, out=None, recv=None, workspace=None,
-                      stream=None) -> torch.Tensor:
+                      stream=None, comm_sms: int = COMM_SMS) -> torch.Tensor:
     """All-to-all + per-rank decomposition, overlapped by sub-range.
 
     send: the [K][world][R*R/K] layout of generate_sendblocks(..., subranges=K).  Sub-range
@@ -85,9 +91,12 @@ def decompose_sharded(send: torch.Tensor, n: int, group=None, out=None, recv=Non
             # all_to_all_single is ordered on the current stream only: make `stream` wait
             # for the exchange before the kernels read `recv`
             stream.wait_stream(cur)
+        cap = 0
+        if world > 1 and s + 1 < K and comm_sms > 0 and send.is_cuda:
+            cap = max(1, torch.cuda.get_device_properties(send.device).multi_processor_count - comm_sms)
         with _nvtx(f"ptdr.decompose_xshard[{s}]"):
             decompose_xshard(recv[s].view(N, Rk), n, rank * K + s, world * K, out=out[s],
-                             workspace=workspace, stream=stream)
+                             workspace=workspace, stream=stream, max_ctas=cap)
     return out
 
 

@@ -159,3 +159,17 @@ def test_coefficients_xshard_algorithm2(gpu):
     other, _ = _shard_qs(n, world, (h + 1) % world, count=8)
     bad = ptdr.coefficients_xshard(recv, n, h, world, other.astype(np.int64)).cpu().numpy()
     assert np.all(np.isnan(bad.real)) and np.all(np.isnan(bad.imag))
+
+
+@pytest.mark.parametrize("max_ctas", [1, 37, 132])
+def test_xshard_grid_cap_is_bitwise_neutral(gpu, max_ctas):
+    """ptdr_decompose_xshard_ex_async with a capped persistent grid (SMs left to a concurrent
+    all-to-all) gives bit-identical results: tickets are dynamic, the schedule per element is
+    not."""
+    torch = _torch()
+    n, world, h = 14, 2, 1
+    A = ptdr.generate_dense(n, SEED, "general")
+    recv = _recv_block(A, n, world, h)
+    full = ptdr.decompose_xshard(recv, n, h, world)
+    capped = ptdr.decompose_xshard(recv, n, h, world, max_ctas=max_ctas)
+    assert torch.equal(torch.view_as_real(full), torch.view_as_real(capped))

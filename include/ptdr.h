@@ -126,6 +126,10 @@ ptdr_status ptdr_decompose_async(const ptdr_c128* A, int n, int structure, ptdr_
 size_t ptdr_inplace_workspace_bytes(int n, int structure); /* (size_t)-1 if invalid */
 ptdr_status ptdr_decompose_inplace_async(ptdr_c128* A, int n, int structure, void* workspace,
                                          size_t ws_bytes, void* stream);
+/* The same matrix layout out of place: out[z][z ^ x] = alpha(x, z), out must not overlap A;
+ * workspace as for ptdr_decompose_inplace_async. */
+ptdr_status ptdr_decompose_matrix_layout_async(const ptdr_c128* A, int n, int structure, ptdr_c128* out,
+                                               void* workspace, size_t ws_bytes, void* stream);
 
 /* End-to-end from HOST memory: copies A_host to the device, decomposes, copies the
  * result to out_host, synchronizes.  Host buffers may be pageable or pinned

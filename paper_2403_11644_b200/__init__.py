@@ -56,6 +56,8 @@ def lib():
         L.ptdr_inplace_workspace_bytes.restype = sz
         L.ptdr_decompose_inplace_async.argtypes = [vp, i32, i32, vp, sz, vp]
         L.ptdr_decompose_inplace_async.restype = i32
+        L.ptdr_decompose_matrix_layout_async.argtypes = [vp, i32, i32, vp, vp, sz, vp]
+        L.ptdr_decompose_matrix_layout_async.restype = i32
         L.ptdr_decompose_host.argtypes = [vp, i32, i32, vp]
         L.ptdr_decompose_xshard_async.argtypes = [vp, i32, i32, i32, vp, vp, sz, vp]
         L.ptdr_decompose_xshard_ex_async.argtypes = [vp, i32, i32, i32, vp, vp, sz, i32, vp]
@@ -267,6 +269,34 @@ def _out(out, count, device, stream):
         _keep_for_stream(stream, out)
     else:
         _require_cuda_c128(out, "out", count, device)
+    return out
+
+
+def decompose_matrix_layout(A, structure="general", out=None, workspace=None, stream=None):
+    """All coefficients in the matrix layout out[z][z ^ x] = alpha(x, z) (out of place;
+    ptdr_decompose_matrix_layout_async).  Returns out [2^n, 2^n]."""
+    import torch
+
+    _require_cuda_c128(A, "A")
+    s = _structure(structure)
+    n = n_of(A, s)
+    if s > 2:
+        raise ValueError("the matrix layout is for the dense structures")
+    if out is None:
+        out = torch.empty((1 << n, 1 << n), dtype=torch.complex128, device=A.device)
+        _keep_for_stream(stream, out)
+    _require_cuda_c128(out, "out", 4 ** n, A.device)
+    nb = int(lib().ptdr_inplace_workspace_bytes(n, s))
+    if workspace is None:
+        workspace = torch.empty(max(nb, 1), dtype=torch.uint8, device=A.device)
+        _keep_for_stream(stream, workspace)
+    else:
+        _require_workspace(workspace, nb, A.device)
+    _check(lib().ptdr_decompose_matrix_layout_async(ctypes.c_void_p(A.data_ptr()), n, s,
+                                                    ctypes.c_void_p(out.data_ptr()),
+                                                    ctypes.c_void_p(workspace.data_ptr()),
+                                                    workspace.numel() * workspace.element_size(),
+                                                    _stream_ptr(stream)), "ptdr_decompose_matrix_layout_async")
     return out
 
 

@@ -757,6 +757,39 @@ ptdr_status ptdr_decompose_inplace_async(ptdr_c128* A, int n, int structure, voi
   return r;
 }
 
+ptdr_status ptdr_decompose_matrix_layout_async(const ptdr_c128* A, int n, int structure, ptdr_c128* out,
+                                               void* workspace, size_t ws_bytes, void* stream) {
+  g_last_launches = 0;
+  if (!is_dense(structure)) return fail(PTDR_EINVAL, "the matrix layout is for the dense structures");
+  if (!valid_n(n, structure)) return fail(PTDR_EINVAL, "invalid n (1..16)");
+  if (!A || !out || ((uintptr_t)A & 15) || ((uintptr_t)out & 15)) return fail(PTDR_EINVAL, "null or misaligned pointer");
+  if (overlaps(A, (size_t)16 << (2 * n), out, (size_t)16 << (2 * n)))
+    return fail(PTDR_EUNSUPPORTED, "out overlaps A (use ptdr_decompose_inplace_async)");
+  const size_t need = ptdr_inplace_workspace_bytes(n, structure);
+  if (need > 0 && (!workspace || ((uintptr_t)workspace & 255)))
+    return fail(PTDR_EINVAL, "workspace missing or not 256-byte aligned");
+  if (ws_bytes < need) return fail(PTDR_ENOMEM, "workspace too small");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const double2* a = reinterpret_cast<const double2*>(A);
+  double2* o = reinterpret_cast<double2*>(out);
+  int nl = 0;
+  ptdr_status r;
+  if (inplace_via_copy(n)) {
+    double2* Q = reinterpret_cast<double2*>(workspace);
+    r = run_dense(a, n, structure, Q, reinterpret_cast<char*>(workspace) + pad_copy_bytes(n), st, &nl);
+    if (r != PTDR_OK) return r;
+    const uint64_t total = 1ull << (2 * n);
+    q_to_matrix_layout_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(Q, n, o);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "layout kernel launch");
+    nl += 1;
+  } else {
+    r = run_dense(a, n, structure, o, workspace, st, &nl, 0, 0, 0, 1);
+  }
+  g_last_launches = nl;
+  return r;
+}
+
 // ---- selected coefficients (Algorithm 2 per string) ------------------------------------
 ptdr_status ptdr_coefficients_async(const ptdr_c128* A, int n, const uint64_t* qs, uint64_t count,
                                     ptdr_c128* out, void* stream) {

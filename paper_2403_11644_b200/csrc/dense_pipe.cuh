@@ -266,16 +266,22 @@ struct PipeCfg {
 // [4, XB+2)=u2.. [XB+2, ..)=zl2.., so 2^k consecutive fibers form a (u, zl) square of
 // 4^(k/2) consecutive q (coalesced epilogue stores).
 
+// In the matrix layout of the in-place decomposition (A[z][z ^ x]) consecutive addresses
+// are consecutive X-masks of one z instead, so there the fibre index is simply
+// phi = u | zl << XB: 2^XB lanes store one 2^XB x 16 B run.
 template <int XB>
-__device__ __forceinline__ uint32_t phi_of(uint32_t u, uint32_t zl) {
+__device__ __forceinline__ uint32_t phi_of(uint32_t u, uint32_t zl, bool mat) {
+  if (mat) return u | (zl << XB);
   return (u & 3u) | ((zl & 3u) << 2) | ((u >> 2) << 4) | ((zl >> 2) << (XB + 2));
 }
 template <int XB>
-__device__ __forceinline__ uint32_t phi_u_of(uint32_t phi) {
+__device__ __forceinline__ uint32_t phi_u_of(uint32_t phi, bool mat) {
+  if (mat) return phi & ((1u << XB) - 1u);
   return (phi & 3u) | (((phi >> 4) & ((1u << (XB - 2)) - 1u)) << 2);
 }
 template <int XB>
-__device__ __forceinline__ uint32_t phi_zl_of(uint32_t phi) {
+__device__ __forceinline__ uint32_t phi_zl_of(uint32_t phi, bool mat) {
+  if (mat) return phi >> XB;
   return ((phi >> 2) & 3u) | ((phi >> (XB + 2)) << 2);
 }
 
@@ -624,7 +630,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
       const uint64_t pol_last = policy_of(a.pol_s);
       // unit (u, jl) -> Y[tileB][ih][f]
       auto store_unit = [&](const double2* w, int jl) {
-        const uint32_t phi_lo = phi_of<XB>((uint32_t)u, (uint32_t)jl);
+        const uint32_t phi_lo = phi_of<XB>((uint32_t)u, (uint32_t)jl, a.layout_mat != 0);
         double2* base = Y + (((phi_lo >> LFB) << LT) | ((uint32_t)m.tile << LFB) | (phi_lo & (FB - 1)));
 #pragma unroll
         for (int jj = 0; jj < (1 << R2); ++jj)
@@ -696,7 +702,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
         const int u = uu & (W - 1), jl = uu >> XB;
         pwht<R2>(&v[p * (1 << R2)]);
         // element (u, ih = tile, zl = j*16 + jl) -> Y[tileB][ih][f]
-        const uint32_t phi_lo = phi_of<XB>((uint32_t)u, (uint32_t)jl);
+        const uint32_t phi_lo = phi_of<XB>((uint32_t)u, (uint32_t)jl, a.layout_mat != 0);
         double2* base = Y + (((phi_lo >> LFB) << LT) | ((uint32_t)m.tile << LFB) | (phi_lo & (FB - 1)));
 #pragma unroll
         for (int j = 0; j < (1 << R2); ++j)
@@ -737,7 +743,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
         auto emit_unit = [&](const double2* w, int jl) {
           const uint32_t phi = (uint32_t)m.tile * FB + (uint32_t)f;
           EpiUnit<R2, HALF> e;
-          e.init((uint32_t)x0 + phi_u_of<XB>(phi), ((uint32_t)jl << R) | phi_zl_of<XB>(phi), R + 4, t,
+          e.init((uint32_t)x0 + phi_u_of<XB>(phi, a.layout_mat != 0), ((uint32_t)jl << R) | phi_zl_of<XB>(phi, a.layout_mat != 0), R + 4, t,
                  a.gshift, a.layout_mat ? a.n : 0);
           emit_all<MODE, R2>(a, e, w);
         };
@@ -768,7 +774,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
         if (lane == 0) mbar_arrive(&empty[s]);
         const uint32_t phi = (uint32_t)m.tile * FB + (uint32_t)f;
         EpiUnit<4, HALF> e;
-        e.init((uint32_t)x0 + phi_u_of<XB>(phi), phi_zl_of<XB>(phi), R, t, a.gshift, a.layout_mat ? a.n : 0);
+        e.init((uint32_t)x0 + phi_u_of<XB>(phi, a.layout_mat != 0), phi_zl_of<XB>(phi, a.layout_mat != 0), R, t, a.gshift, a.layout_mat ? a.n : 0);
         emit_all<MODE, 4>(a, e, v);
       } else {
         constexpr int R2 = M - 4;
@@ -799,7 +805,7 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
           const uint32_t phi = (uint32_t)m.tile * FB + (uint32_t)f2;
           pwht<R2>(&v[p * (1 << R2)]);
           EpiUnit<R2, HALF> e;
-          e.init((uint32_t)x0 + phi_u_of<XB>(phi), ((uint32_t)jl << R) | phi_zl_of<XB>(phi), R + 4, t,
+          e.init((uint32_t)x0 + phi_u_of<XB>(phi, a.layout_mat != 0), ((uint32_t)jl << R) | phi_zl_of<XB>(phi, a.layout_mat != 0), R + 4, t,
                  a.gshift, a.layout_mat ? a.n : 0);
           emit_all<MODE, R2>(a, e, &v[p * (1 << R2)]);
         }

@@ -208,6 +208,50 @@ def inverse(name, n):
     torch.cuda.empty_cache()
 
 
+def inplace(name, n, seed):
+    """BASELINE configs[4] "n=16 at 1 GPU in-place": ptdr_decompose_inplace_async overwrites A
+    with its coefficients (matrix layout); A is regenerated before every timed call (the
+    generator outside the timed region)."""
+    A = ptdr.generate_dense(n, seed, "general", device="cuda")
+    nb = int(ptdr.lib().ptdr_inplace_workspace_bytes(n, 0))
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    times = []
+    for it in range(8):
+        ptdr.generate_dense(n, seed, "general", out=A)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        ptdr.decompose(A, "general", workspace=ws, inplace=True)
+        e1.record()
+        torch.cuda.synchronize()
+        if it >= 2:
+            times.append(e0.elapsed_time(e1))
+    ms = sorted(times)[len(times) // 2]
+    coeffs = 1 << (2 * n)
+    gbs = 32 * coeffs / (ms * 1e-3) / 1e9
+    peak_gib = (16 * coeffs + nb) / 2 ** 30
+    print(json.dumps({"config": name, "n": n, "structure": "general", "ms": ms, "coeffs_per_s": coeffs / (ms * 1e-3),
+                      "alg_bytes_per_coeff": 32, "hbm_gbs": gbs, "frac_of_measured": gbs / PEAK,
+                      "device_memory_gib": peak_gib}), flush=True)
+    del A, ws
+    torch.cuda.empty_cache()
+
+
+def matrix_layout(name, n, seed):
+    """The same transform out of place with the matrix-layout output (for comparison with
+    the in-place call and the q-order one)."""
+    A = ptdr.generate_dense(n, seed, "general", device="cuda")
+    out = torch.empty((1 << n, 1 << n), dtype=torch.complex128, device="cuda")
+    ws = torch.empty(int(ptdr.lib().ptdr_inplace_workspace_bytes(n, 0)), dtype=torch.uint8, device="cuda")
+    ms = time_it(lambda: ptdr.decompose_matrix_layout(A, "general", out=out, workspace=ws))
+    coeffs = 1 << (2 * n)
+    gbs = 32 * coeffs / (ms * 1e-3) / 1e9
+    print(json.dumps({"config": name, "n": n, "structure": "general", "ms": ms, "coeffs_per_s": coeffs / (ms * 1e-3),
+                      "alg_bytes_per_coeff": 32, "hbm_gbs": gbs, "frac_of_measured": gbs / PEAK}), flush=True)
+    del A, out, ws
+    torch.cuda.empty_cache()
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["all"]
     if "all" in which or "small" in which:
@@ -233,3 +277,8 @@ if __name__ == "__main__":
         dense("n15", 15, 4, "general")
         dense("n15_hermitian", 15, 4, "hermitian")
         dense("n16", 16, 4, "general")
+    if "all" in which or "big" in which or "inplace" in which:
+        inplace("n15_inplace", 15, 4)
+        inplace("n16_inplace", 16, 4)
+        matrix_layout("n15_matrix_layout", 15, 4)
+        matrix_layout("n16_matrix_layout", 16, 4)

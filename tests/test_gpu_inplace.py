@@ -75,3 +75,17 @@ def test_inplace_rejects_band_structures(gpu):
     d = torch.zeros(1 << 6, dtype=torch.complex128, device="cuda")
     with pytest.raises(ptdr.PtdrError):
         ptdr.decompose(d, "diagonal", inplace=True)
+
+
+@pytest.mark.parametrize("variant", ["general", "hermitian"])
+@pytest.mark.parametrize("n", [4, 9, 12, 14])
+def test_matrix_layout_out_of_place(gpu, n, variant):
+    """ptdr_decompose_matrix_layout_async: the in-place layout written to a separate buffer,
+    bitwise the permuted q-order result; A untouched."""
+    torch = _torch()
+    A = ptdr.generate_dense(n, 6, variant)
+    keep = A.clone()
+    ref = ptdr.decompose(A, variant)
+    M = ptdr.decompose_matrix_layout(A, variant)
+    assert torch.equal(torch.view_as_real(A), torch.view_as_real(keep))
+    assert torch.equal(torch.view_as_real(M.reshape(-1)[_flat_map(n)]), torch.view_as_real(ref))

@@ -102,7 +102,7 @@ def test_xshard_bench_configs(gpu, n, world):
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("n,world,K", [(15, 8, 4), (15, 2, 4), (12, 4, 2), (16, 8, 4)])
+@pytest.mark.parametrize("n,world,K", [(15, 8, 4), (15, 4, 4), (15, 2, 4), (12, 4, 2), (16, 8, 4)])
 def test_subrange_sharded_bench_path(gpu, n, world, K):
     """The overlapped path bench.py runs at N > 1 (dist.decompose_sharded with K
     sub-ranges): rank h's sub-range s is received as the K-sub-range send layout of every

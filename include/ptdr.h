@@ -265,6 +265,19 @@ ptdr_status ptdr_decompose_band_async(const ptdr_c128* diags, int n, int s, ptdr
 size_t ptdr_reconstruct_workspace_bytes(int n);
 ptdr_status ptdr_reconstruct_async(const ptdr_c128* coeffs, int n, ptdr_c128* A, void* workspace,
                                    size_t ws_bytes, void* stream);
+/* Inverse transform from the matrix layout (l.116-121): A[i][i ^ x] = sum_z (-1)^{z.i}
+ * (-i)^{popcount(x & z)} M[z][z ^ x], where M[z][z ^ x] = alpha(x, z) is the layout
+ * ptdr_decompose_inplace_async / ptdr_decompose_matrix_layout_async write (so
+ * reconstruct_matrix_layout(decompose_inplace(A)) = A up to rounding).  M, A: device
+ * [2^n][2^n] row-major; A == M runs in place (every XOR-diagonal is read before it is
+ * written); any other overlap is PTDR_EUNSUPPORTED.  Sizes with the TMA pipeline (n >= 11)
+ * run the forward pipeline with the phase applied on input (one launch, no copy); smaller
+ * sizes permute M to q order in the workspace and call the q-order inverse.  workspace:
+ * device, >= ptdr_reconstruct_matrix_layout_workspace_bytes(n), 256-byte aligned, disjoint
+ * from M and A.  n in 1..16; (size_t)-1 for invalid n. */
+size_t ptdr_reconstruct_matrix_layout_workspace_bytes(int n);
+ptdr_status ptdr_reconstruct_matrix_layout_async(const ptdr_c128* M, int n, ptdr_c128* A, void* workspace,
+                                                 size_t ws_bytes, void* stream);
 /* Linear combination (l.570-577): out = mu x + nu y elementwise over `count` coefficients
  * (decomposition of mu A + nu B from those of A and B).  out may alias x or y. */
 ptdr_status ptdr_axpby_async(ptdr_c128* out, double mu_re, double mu_im, const ptdr_c128* x,

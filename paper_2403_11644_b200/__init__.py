@@ -76,11 +76,14 @@ def lib():
         L.ptdr_reconstruct_workspace_bytes.argtypes = [i32]
         L.ptdr_reconstruct_workspace_bytes.restype = sz
         L.ptdr_reconstruct_async.argtypes = [vp, i32, vp, vp, sz, vp]
+        L.ptdr_reconstruct_matrix_layout_workspace_bytes.argtypes = [i32]
+        L.ptdr_reconstruct_matrix_layout_workspace_bytes.restype = sz
+        L.ptdr_reconstruct_matrix_layout_async.argtypes = [vp, i32, vp, vp, sz, vp]
         L.ptdr_axpby_async.argtypes = [vp, dbl, dbl, vp, dbl, dbl, vp, sz, vp]
         L.ptdr_block_diag_async.argtypes = [vp, i32, i32, vp, vp]
         L.ptdr_hermitian_augment_async.argtypes = [vp, i32, vp, vp]
-        for name in ("ptdr_reconstruct_async", "ptdr_axpby_async", "ptdr_block_diag_async",
-                     "ptdr_hermitian_augment_async"):
+        for name in ("ptdr_reconstruct_async", "ptdr_reconstruct_matrix_layout_async", "ptdr_axpby_async",
+                     "ptdr_block_diag_async", "ptdr_hermitian_augment_async"):
             getattr(L, name).restype = i32
         L.ptdr_padded_workspace_bytes.argtypes = [u64, i32]
         L.ptdr_padded_workspace_bytes.restype = sz
@@ -678,6 +681,36 @@ def reconstruct(coeffs, out=None, workspace=None, stream=None):
     _check(lib().ptdr_reconstruct_async(ctypes.c_void_p(coeffs.data_ptr()), n, ctypes.c_void_p(out.data_ptr()),
                                         ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
                                         _stream_ptr(stream)), "ptdr_reconstruct_async")
+    return out
+
+
+def reconstruct_matrix_layout(M, out=None, workspace=None, stream=None, inplace=False):
+    """Inverse transform from the matrix layout M[z][z ^ x] = alpha(x, z) (what
+    decompose(..., inplace=True) / decompose_matrix_layout return) to the dense matrix
+    (ptdr_reconstruct_matrix_layout_async).  inplace=True overwrites M with A."""
+    import torch
+
+    _require_cuda_c128(M, "M")
+    n = _n_of_coeffs(M)
+    if inplace:
+        if out is not None:
+            raise ValueError("inplace=True writes into M; out must be None")
+        out = M
+    elif out is None:
+        out = torch.empty((1 << n, 1 << n), dtype=torch.complex128, device=M.device)
+        _keep_for_stream(stream, out)
+    _require_cuda_c128(out, "out", 4 ** n, M.device)
+    nb = int(lib().ptdr_reconstruct_matrix_layout_workspace_bytes(n))
+    if workspace is None:
+        workspace = torch.empty(nb, dtype=torch.uint8, device=M.device)
+        _keep_for_stream(stream, workspace)
+    else:
+        _require_workspace(workspace, nb, M.device)
+    _check(lib().ptdr_reconstruct_matrix_layout_async(ctypes.c_void_p(M.data_ptr()), n,
+                                                      ctypes.c_void_p(out.data_ptr()),
+                                                      ctypes.c_void_p(workspace.data_ptr()),
+                                                      workspace.numel() * workspace.element_size(),
+                                                      _stream_ptr(stream)), "ptdr_reconstruct_matrix_layout_async")
     return out
 
 

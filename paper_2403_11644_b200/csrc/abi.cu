@@ -790,6 +790,72 @@ ptdr_status ptdr_decompose_matrix_layout_async(const ptdr_c128* A, int n, int st
   return r;
 }
 
+// ---- inverse transform from the matrix layout ------------------------
+// v_x = WHT_n(u_x), u_x[z] = (-i)^{popcount(x & z)} alpha(x, z), A[i][i ^ x] = v_x[i]: the
+// forward pipeline with the phase moved from the epilogue into phase A (MODE_INV).  The input
+// M[z][z ^ x] = alpha(x, z) and the output share every XOR-diagonal, so it runs in place.
+// Sizes without the pipeline permute to q order in the workspace and call the q-order inverse.
+static bool inv_pipe(int n) {
+  const DensePlan p = plan_for(MODE_GENERAL, n, 1ull << n);
+  return p.pipe_cfg != kPipeNone && p.kind == 2;
+}
+
+__global__ void matrix_layout_to_q_kernel(const double2* __restrict__ M, int n, double2* __restrict__ Q) {
+  const uint64_t N = 1ull << n;
+  for (uint64_t id = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; id < N * N;
+       id += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t x = id >> n, z = id & (N - 1);
+    Q[q_offset(x, z, n)] = M[(z << n) | (z ^ x)];
+  }
+}
+
+size_t ptdr_reconstruct_matrix_layout_workspace_bytes(int n) {
+  if (n < 1 || n > 16) return (size_t)-1;
+  if (inv_pipe(n)) return plan_ws(n, 1ull << n);
+  return pad_copy_bytes(n) + reconstruct_workspace_bytes(n);
+}
+
+ptdr_status ptdr_reconstruct_matrix_layout_async(const ptdr_c128* M, int n, ptdr_c128* A, void* workspace,
+                                                 size_t ws_bytes, void* stream) {
+  g_last_launches = 0;
+  if (n < 1 || n > 16) return fail(PTDR_EINVAL, "invalid n (1..16)");
+  if (!M || !A || ((uintptr_t)M & 15) || ((uintptr_t)A & 15)) return fail(PTDR_EINVAL, "null or misaligned pointer");
+  const size_t need = ptdr_reconstruct_matrix_layout_workspace_bytes(n);
+  if (!workspace || ((uintptr_t)workspace & 255)) return fail(PTDR_EINVAL, "workspace missing or not 256-byte aligned");
+  if (ws_bytes < need) return fail(PTDR_ENOMEM, "workspace too small");
+  const size_t nb = (size_t)16 << (2 * n);
+  if (M != A && overlaps(M, nb, A, nb)) return fail(PTDR_EUNSUPPORTED, "A partially overlaps M (in place needs A == M)");
+  if (overlaps(workspace, need, A, nb) || overlaps(workspace, need, M, nb))
+    return fail(PTDR_EINVAL, "workspace overlaps M or A");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const double2* m = reinterpret_cast<const double2*>(M);
+  double2* a_out = reinterpret_cast<double2*>(A);
+  int nl = 0;
+  if (inv_pipe(n)) {
+    const DensePlan p = plan_for(MODE_GENERAL, n, 1ull << n);
+    DenseArgs a = base_args(m, a_out, n, workspace);
+    a.scale = 1.0;
+    a.layout_mat = 1;
+    a.nv = n;
+    a.x_base = 0;
+    a.nchunks = p.nchunks;
+    a.scratch = reinterpret_cast<double2*>(reinterpret_cast<char*>(workspace) + p.ctr_bytes);
+    const ptdr_status r = launch_mode(MODE_INV, a, p, st, &nl);
+    g_last_launches = nl;
+    return r;
+  }
+  double2* Q = reinterpret_cast<double2*>(workspace);
+  const uint64_t total = 1ull << (2 * n);
+  uint64_t g = (total + 255) / 256;
+  if (g > (uint64_t)device_sm_count() * 16) g = (uint64_t)device_sm_count() * 16;
+  matrix_layout_to_q_kernel<<<(unsigned)g, 256, 0, st>>>(m, n, Q);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "layout kernel launch");
+  e = launch_reconstruct(Q, n, a_out, reinterpret_cast<char*>(workspace) + pad_copy_bytes(n), st, &nl);
+  g_last_launches = 1 + nl;
+  return e == cudaSuccess ? PTDR_OK : cuda_fail(e, "reconstruct launch");
+}
+
 // ---- selected coefficients (Algorithm 2 per string) ------------------------------------
 ptdr_status ptdr_coefficients_async(const ptdr_c128* A, int n, const uint64_t* qs, uint64_t count,
                                     ptdr_c128* out, void* stream) {

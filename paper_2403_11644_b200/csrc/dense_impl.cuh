@@ -21,7 +21,8 @@ namespace ptdr {
 // triangle), 2 REAL_SYMMETRIC mirrored, 3 HERMITIAN half-length, 4 REAL_SYMMETRIC
 // half-length.  See DESIGN.md "Hermitian / real-symmetric path".
 enum { MODE_GENERAL = 0, MODE_HERM_MIRROR = 1, MODE_SYM_MIRROR = 2, MODE_HERM_HALF = 3, MODE_SYM_HALF = 4,
-       MODE_GEN = 8 /* matrix-free GENERAL (pipeline only): entries generated in phase A */ };
+       MODE_GEN = 8 /* matrix-free GENERAL (pipeline only): entries generated in phase A */,
+       MODE_INV = 9 /* inverse transform from the matrix layout (pipeline only, see dense_pipe.cuh) */ };
 
 struct DenseArgs {
   const double2* A;

@@ -156,7 +156,9 @@ struct EpiUnit {
 template <int MODE>
 __device__ __forceinline__ void emit_one(const DenseArgs& a, uint32_t q, uint32_t p, uint32_t dt,
                                          double2 w) {
-  if constexpr (MODE == MODE_GENERAL || MODE == MODE_GEN) {
+  if constexpr (MODE == MODE_INV) {
+    st_out(a.out + q, w);  // the inverse: A[i][i ^ x] = WHT(u_x)[i], no phase, no scale
+  } else if constexpr (MODE == MODE_GENERAL || MODE == MODE_GEN) {
     const bool sw = (p & 1u) != 0;
     const double s = (p & 2u) ? -a.scale : a.scale;
     const double re = sw ? -w.y : w.x;
@@ -671,6 +673,14 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
             v[kk] = S[r * W + ((r & (W - 1)) ^ u)];
             if (MODE == MODE_SYM_HALF) v[kk].y = 0.0;
           }
+          if constexpr (MODE == MODE_INV) {
+            // inverse: the gathered element M[z][z ^ x] = alpha(x, z) of the
+            // matrix-layout coefficients enters as u_x[z] = (-i)^{popcount(x & z)} alpha(x, z)
+            const uint32_t x = (uint32_t)a.x_base + (m.chunk << XB) + (uint32_t)u;
+            const uint32_t z0 = ((uint32_t)m.tile << R) + (uint32_t)(jh * 16);
+#pragma unroll
+            for (int kk = 0; kk < 16; ++kk) v[kk] = rot_ipow(v[kk], 4 - (__popc(x & (z0 + (uint32_t)kk)) & 3));
+          }
         }
         pwht<4>(v);
         __syncwarp();  // rows of this jh are read and written only by this warp
@@ -853,6 +863,9 @@ static cudaError_t launch_pipe_cfg(int mode, const TmapSet& map, const DenseArgs
     case MODE_GEN:
       // matrix-free: instantiated for the 3-stage in-place configurations only
       if constexpr (NR == 0 && LT == 12) return launch_pipe_m<LT, XB, GW, NG, NS, NR, MODE_GEN>(map, a, M, st);
+      return cudaErrorInvalidValue;
+    case MODE_INV:
+      if constexpr (NR == 0 && LT == 12) return launch_pipe_m<LT, XB, GW, NG, NS, NR, MODE_INV>(map, a, M, st);
       return cudaErrorInvalidValue;
     default: return cudaErrorInvalidValue;
   }

@@ -208,6 +208,44 @@ def inverse(name, n):
     torch.cuda.empty_cache()
 
 
+def inverse_layout(name, n, inplace_call):
+    """Inverse transform from the matrix layout (ptdr_reconstruct_matrix_layout_async, MODE_INV
+    pipeline at n >= 11), out of place or in place; round trip checked."""
+    A = ptdr.generate_dense(n, 4, "general", device="cuda")
+    M = ptdr.decompose_matrix_layout(A)
+    ws = torch.empty(int(ptdr.lib().ptdr_reconstruct_matrix_layout_workspace_bytes(n)), dtype=torch.uint8,
+                     device="cuda")
+    if inplace_call:
+        del A
+        torch.cuda.empty_cache()
+        src = M.clone()
+        times = []
+        for it in range(8):
+            M.copy_(src)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            ptdr.reconstruct_matrix_layout(M, workspace=ws, inplace=True)
+            e1.record()
+            torch.cuda.synchronize()
+            if it >= 2:
+                times.append(e0.elapsed_time(e1))
+        ms = sorted(times)[len(times) // 2]
+        del src
+        A = ptdr.generate_dense(n, 4, "general", device="cuda")
+        B = M
+    else:
+        B = torch.empty_like(A)
+        ms = time_it(lambda: ptdr.reconstruct_matrix_layout(M, out=B, workspace=ws))
+    err = max(torch.max(torch.abs(A[i:i + 1024] - B[i:i + 1024])).item() for i in range(0, A.shape[0], 1024))
+    alg = 32 * 4 ** n
+    print(json.dumps({"config": name, "n": n, "in_place": inplace_call, "ms": ms, "coeffs_per_s": 4 ** n / (ms * 1e-3),
+                      "hbm_gbs": alg / (ms * 1e-3) / 1e9, "frac_of_measured": alg / (ms * 1e-3) / 1e9 / PEAK,
+                      "round_trip_max_err": err, "launches": ptdr.last_launch_count()}), flush=True)
+    del A, B, M, ws
+    torch.cuda.empty_cache()
+
+
 def inplace(name, n, seed):
     """BASELINE configs[4] "n=16 at 1 GPU in-place": ptdr_decompose_inplace_async overwrites A
     with its coefficients (matrix layout); A is regenerated before every timed call (the
@@ -270,6 +308,8 @@ if __name__ == "__main__":
         band_s("n24band_s2", 24, 2)
         band_s("n22band_s5", 22, 5)
         inverse("n15_inverse", 15)
+        inverse_layout("n15_inverse_matrix_layout", 15, False)
+        inverse_layout("n15_inverse_in_place", 15, True)
         batched("n6_batch16384", 6, 16384)
         batched("n10_batch64", 10, 64)
         generated("n15_matrix_free", 15)
@@ -277,6 +317,11 @@ if __name__ == "__main__":
         dense("n15", 15, 4, "general")
         dense("n15_hermitian", 15, 4, "hermitian")
         dense("n16", 16, 4, "general")
+    if "inverse" in which:
+        inverse("n15_inverse", 15)
+        inverse_layout("n15_inverse_matrix_layout", 15, False)
+        inverse_layout("n15_inverse_in_place", 15, True)
+        inverse_layout("n16_inverse_in_place", 16, True)
     if "all" in which or "big" in which or "inplace" in which:
         inplace("n15_inplace", 15, 4)
         inplace("n16_inplace", 16, 4)

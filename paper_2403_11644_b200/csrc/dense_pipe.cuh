@@ -676,10 +676,21 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
           if constexpr (MODE == MODE_INV) {
             // inverse: the gathered element M[z][z ^ x] = alpha(x, z) of the
             // matrix-layout coefficients enters as u_x[z] = (-i)^{popcount(x & z)} alpha(x, z)
+            // (z0 has 4 zero low bits, so popcount(x & z) = popcount(x & z0) + popcount(x & kk);
+            // the lanes' phases differ, so the rotation is branch-free: swap + sign bits)
             const uint32_t x = (uint32_t)a.x_base + (m.chunk << XB) + (uint32_t)u;
             const uint32_t z0 = ((uint32_t)m.tile << R) + (uint32_t)(jh * 16);
+            const uint32_t p0 = 4u - (uint32_t)__popc(x & z0);
 #pragma unroll
-            for (int kk = 0; kk < 16; ++kk) v[kk] = rot_ipow(v[kk], 4 - (__popc(x & (z0 + (uint32_t)kk)) & 3));
+            for (int kk = 0; kk < 16; ++kk) {
+              const uint32_t p = p0 - (uint32_t)__popc(x & (uint32_t)kk);   // (-i)^popc = i^p
+              const bool sw = p & 1u;
+              const unsigned long long sre = (unsigned long long)(((p + 1u) >> 1) & 1u) << 63;
+              const unsigned long long sim = (unsigned long long)((p >> 1) & 1u) << 63;
+              const double re = sw ? v[kk].y : v[kk].x, im = sw ? v[kk].x : v[kk].y;
+              v[kk].x = __longlong_as_double((long long)((unsigned long long)__double_as_longlong(re) ^ sre));
+              v[kk].y = __longlong_as_double((long long)((unsigned long long)__double_as_longlong(im) ^ sim));
+            }
           }
         }
         pwht<4>(v);

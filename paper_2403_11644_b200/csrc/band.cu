@@ -522,7 +522,14 @@ __global__ void __launch_bounds__(kThreads, 2) topk_pass_kernel(const double2* _
 #pragma unroll
       for (int r = 0; r < IPR; ++r)
 #pragma unroll
-        for (int h = 0; h < (1 << TB); ++h) d[r][h] = ld_l2(in + (u64)h * Q + il0 + (u64)(tid + 256 * (m + r)));
+        for (int h = 0; h < (1 << TB); ++h) {
+          // a rank keeping a fraction of the branches (KK < TB) reads the band once and
+          // writes little: evict-first loads keep its output L2-resident for the tail
+          // (n = 24, G = 8: 0.084 -> 0.076 ms); keeping every branch, plain loads are faster
+          // (99 vs 115 us)
+          const double2* p = in + (u64)h * Q + il0 + (u64)(tid + 256 * (m + r));
+          d[r][h] = KK < TB ? ld_stream(p) : ld_l2(p);
+        }
 #pragma unroll
       for (int r = 0; r < IPR; ++r) {
         double2 o[KS];
@@ -853,6 +860,17 @@ cudaError_t launch_band(const double2* A, double2* out, int n, int structure, vo
     if (tail_ok(f)) return launch_tail(f, tail_ctr, st, nl);
     return run_families(&f, 1, st, nl);
   }
+  // Block 0 (x = 0, WHT(main) scaled) first: its passes stream the main diagonal through L2,
+  // so running them before the split keeps the split's P/M output L2-resident for the
+  // segment passes that follow.
+  WhtFamily fam[kMaxSeg];
+  int nf = 0;
+  if ((e = x0_family(A + N, 0ull, fam[nf])) != cudaSuccess) return e;
+  if (tail_ok(fam[nf])) {
+    if ((e = launch_tail(fam[nf], tail_ctr, st, nl)) != cudaSuccess) return e;
+  } else {
+    ++nf;
+  }
   // TRIDIAGONAL: A = [sub | main | sup].  Segments t with lam = n - t - 1 >= kTopMin: fused
   // split + top levels (the rank's branches only); shorter ones: plain split, replicated.
   const int lam_small = n - 1 < kTopMin - 1 ? n - 1 : kTopMin - 1;
@@ -876,15 +894,7 @@ cudaError_t launch_band(const double2* A, double2* out, int n, int structure, vo
     *nl += 1;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  // block 0 (x = 0): WHT(main) scaled; blocks t+1: P_t / M_t
-  WhtFamily fam[kMaxSeg];
-  int nf = 0;
-  if ((e = x0_family(A + N, 0ull, fam[nf])) != cudaSuccess) return e;
-  if (tail_ok(fam[nf])) {
-    if ((e = launch_tail(fam[nf], tail_ctr, st, nl)) != cudaSuccess) return e;
-  } else {
-    ++nf;
-  }
+  // blocks t+1: P_t / M_t
   for (int t = 0; t < n; ++t) {
     const int lam = n - t - 1;
     const u64 seg = N - (N >> t);

@@ -140,13 +140,15 @@ __device__ __forceinline__ SegView seg_view(const double2* PM, int n, int t, int
 }
 
 __global__ void __launch_bounds__(256) tridiag_expand_kernel(const double2* PM, double2* out, int n,
-                                                             double scale, int zshift, u64 zrank, int k_keep) {
+                                                             double scale, int zshift, u64 zrank, int k_keep,
+                                                             int t_first) {
   const u64 N = 1ull << n;
   const u64 NL = 1ull << zshift;              // outputs per block on this rank
   const u64 z0 = zrank << zshift;
   const u64 groups = ((u64)n * NL) >> 8;      // 256 outputs per warp-group of 8 stores
+  const u64 g0 = ((u64)t_first * NL) >> 8;    // blocks 1..t_first come from the fused kernel
   const int lane = threadIdx.x & 31;
-  for (u64 gidx = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; gidx < groups;
+  for (u64 gidx = g0 + (((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5); gidx < groups;
        gidx += ((u64)gridDim.x * blockDim.x) >> 5) {
     const u64 id0 = gidx << 8;
     const int t = (int)(id0 >> zshift);
@@ -373,7 +375,7 @@ cudaError_t run_families(const WhtFamily* fam, int nfam, cudaStream_t st, int* n
       sp.px = 0;
       sp.zoff = 0;
       if (fnfam(w)) {
-        if (p >= 2) continue;
+        if (p >= 2 - w.skip_last) continue;
         const bool last = p == 1;
         sp.in = p == 0 ? w.in : w.out;
         sp.out = last ? fin : w.out;
@@ -411,6 +413,7 @@ cudaError_t run_families(const WhtFamily* fam, int nfam, cudaStream_t st, int* n
         if (b0 < w.first_bit || b0 >= w.lam) continue;
         const int K = (w.lam - b0) < 8 ? (w.lam - b0) : 8;
         const bool last = b0 + K >= w.lam;
+        if (last && w.skip_last) continue;
         sp.in = b0 == w.first_bit ? w.in : w.out;
         sp.out = last ? fin : w.out;
         sp.b0 = b0;
@@ -769,6 +772,177 @@ static cudaError_t launch_tail(const WhtFamily& f, unsigned* ctr, cudaStream_t s
   return cudaGetLastError();
 }
 
+// ---- tridiagonal: last P/M pass fused with the expansion (segments t <= 3) ---------------
+// For a long segment t whose last WHT pass runs over bits [8, 8 + K) of the branch index (the
+// 17-20-bit families after fn_tile, or a 13-16-bit family after its contig8 pass), one tile
+// takes the 2^(12-K) x 2^K fibres of that pass from P_t AND from M_t, transforms both (the same
+// fiber_tile arithmetic, bitwise), and writes the 2^(t+1) outputs of every one of its 4096 zh
+// values straight into block t+1 -- the P/M values never go back to DRAM and the expansion
+// does not read them again (n = 24: 0.96 GiB less traffic).  Blocks t >= 4 keep the separate
+// expansion (a tile's output, 2^(t+1) x 64 KiB, would unbalance the grid).  One CTA per SM
+// (two 64 KiB transform buffers); the next tile's 32 loads per thread are issued before the
+// current tile's output loop, so load latency hides behind the stores.
+constexpr int kFuseMaxT = 3;
+struct FusedSeg {
+  const double2* P;  // P_t branches (KS x 2^lamp), M_t follows at P + KS 2^lamp
+  u64 tiles;         // KS 2^lamp / 4096
+  u64 first_tile;
+  int lamp;          // branch length bits
+  int K;             // bits of the last pass (at bit 8)
+  int t;
+  int parts_log;     // work items per tile = 2^parts_log (each emits 4096 / 2^parts_log slots)
+};
+struct FusedArgs {
+  FusedSeg s[kFuseMaxT + 1];
+  int count;
+  u64 total_tiles;
+  double2* out;  // block 0 of the rank's output (block t+1 at out + (t+1) NL)
+  u64 NL;
+  double scale;
+  unsigned* ticket;
+};
+constexpr int kFusedSmem = 2 * kTileBytes;
+
+template <int K>
+__device__ __forceinline__ void fused_load(const FusedSeg& sg, u64 local, double2 (&vP)[16], double2 (&vM)[16]) {
+  constexpr int F = kTileElems >> K;
+  const int tid = threadIdx.x;
+  const int f = tid % F, jh = tid / F;
+  const u64 rho = local * F + (u64)f;
+  const u64 msk = (1ull << 8) - 1ull;
+  const double2* M = sg.P + ((u64)sg.tiles << 12);
+#pragma unroll
+  for (int kk = 0; kk < 16; ++kk) {
+    const u64 j = (u64)((jh << 4) + kk);
+    const u64 e = ((rho >> 8) << (8 + K)) | (j << 8) | (rho & msk);
+    vP[kk] = ld_l2(sg.P + e);
+    vM[kk] = ld_l2(M + e);
+  }
+}
+
+// fiber_tile<K> stages on registers already loaded (K >= 5: radix 16 then 2^(K-4)); the
+// final values land at S[j F + f] (in place of the exchange slots).
+template <int K>
+__device__ __forceinline__ void fused_transform(double2* S, double2 (&v)[16]) {
+  constexpr int F = kTileElems >> K;
+  const int tid = threadIdx.x;
+  wht_regs<4>(v);
+  {
+    const int f = tid % F, jh = tid / F;
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) S[(jh * 16 + kk) * F + f] = v[kk];
+  }
+  __syncthreads();
+  constexpr int R2 = K - 4;
+  constexpr int U2 = 1 << (8 - K);
+#pragma unroll
+  for (int p = 0; p < U2; ++p) {
+    const int uu = tid + kThreads * p;
+    const int f = uu % F, jl = uu / F;
+    double2 w[1 << R2];
+#pragma unroll
+    for (int jh = 0; jh < (1 << R2); ++jh) w[jh] = S[(jh * 16 + jl) * F + f];
+    wht_regs<R2>(w);
+#pragma unroll
+    for (int jh = 0; jh < (1 << R2); ++jh) S[(jh * 16 + jl) * F + f] = w[jh];
+  }
+}
+
+// Outputs of slots [part S_p, (part + 1) S_p) of the tile (S_p = 4096 / parts).  Thread tid
+// writes o = tid + 256 i: zl = o mod 2^(t+1) is fixed per thread (t <= 3), so the phase and
+// the P/M choice are too; slot = j F + f maps to e = e0 + (j << 8) + f (F <= 256).
+template <int K>
+__device__ __forceinline__ void fused_emit(const FusedArgs& A, const FusedSeg& sg, u64 local, int part,
+                                           const double2* SP, const double2* SM) {
+  constexpr int F = kTileElems >> K;
+  const int t = sg.t;
+  const int tb = t + 1;
+  const int sp_bits = 12 - (sg.parts_log);
+  const u64 per = 1ull << (sp_bits + tb);  // outputs of this work item
+  double2* blk = A.out + (u64)tb * A.NL;
+  const u64 rb = local * (u64)F;
+  const u64 e0 = ((rb >> 8) << (8 + K)) | (rb & 255ull);
+  const int zl = threadIdx.x & ((1 << tb) - 1);
+  const int s1 = __popc(zl & ((1 << t) - 1)) & 1;
+  const int s2 = (zl >> t) & 1;
+  const double2* src = s1 == s2 ? SP : SM;
+  const int ph = __popc(zl) + 2 * s1;
+  const bool sw = (ph & 1) != 0;
+  const double sc = (ph & 2) ? -A.scale : A.scale;
+  double2* base = blk + (e0 << tb) + (u64)zl;
+  const int slot_base = part << sp_bits;
+  for (u64 o = threadIdx.x; o < per; o += kThreads) {
+    const int slot = slot_base + (int)(o >> tb);
+    const int f = slot & (F - 1), j = slot / F;
+    const double2 w = src[slot];
+    const double re = sw ? -w.y : w.x;
+    const double im = sw ? w.x : w.y;
+    st_stream(base + ((((u64)j << 8) + (u64)f) << tb), make_double2(re * sc, im * sc));
+  }
+}
+
+__device__ __forceinline__ int fused_seg_of(const FusedArgs& A, u64 tile) {
+  int i = 0;
+  while (i + 1 < A.count && A.s[i + 1].first_tile <= tile) ++i;
+  return i;
+}
+
+template <int K>
+__device__ __forceinline__ void fused_load_k(const FusedSeg& sg, u64 local, double2 (&vP)[16], double2 (&vM)[16]) {
+  fused_load<K>(sg, local, vP, vM);
+}
+__device__ __forceinline__ void fused_load_any(const FusedSeg& sg, u64 local, double2 (&vP)[16], double2 (&vM)[16]) {
+  switch (sg.K) {
+    case 5: fused_load_k<5>(sg, local, vP, vM); break;
+    case 6: fused_load_k<6>(sg, local, vP, vM); break;
+    case 7: fused_load_k<7>(sg, local, vP, vM); break;
+    default: fused_load_k<8>(sg, local, vP, vM); break;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) tri_fused_expand_kernel(const __grid_constant__ FusedArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* SP = reinterpret_cast<double2*>(smem_raw);
+  double2* SM = SP + kTileElems;
+  __shared__ unsigned long long s_tk;
+  if (threadIdx.x == 0) s_tk = atomicAdd(A.ticket, 1u);
+  __syncthreads();
+  u64 item = s_tk;
+  double2 vP[16], vM[16];
+  if (item < A.total_tiles) {
+    const FusedSeg& sg = A.s[fused_seg_of(A, item)];
+    fused_load_any(sg, (item - sg.first_tile) >> sg.parts_log, vP, vM);
+  }
+  while (item < A.total_tiles) {
+    const FusedSeg& sg = A.s[fused_seg_of(A, item)];
+    const u64 rel = item - sg.first_tile;
+    const u64 local = rel >> sg.parts_log;
+    const int part = (int)(rel & ((1ull << sg.parts_log) - 1ull));
+    switch (sg.K) {
+      case 5: fused_transform<5>(SP, vP); fused_transform<5>(SM, vM); break;
+      case 6: fused_transform<6>(SP, vP); fused_transform<6>(SM, vM); break;
+      case 7: fused_transform<7>(SP, vP); fused_transform<7>(SM, vM); break;
+      default: fused_transform<8>(SP, vP); fused_transform<8>(SM, vM); break;
+    }
+    // next ticket, and its loads issued before this item's output loop
+    if (threadIdx.x == 0) s_tk = atomicAdd(A.ticket, 1u);
+    __syncthreads();
+    const u64 next = s_tk;
+    if (next < A.total_tiles) {
+      const FusedSeg& sn = A.s[fused_seg_of(A, next)];
+      fused_load_any(sn, (next - sn.first_tile) >> sn.parts_log, vP, vM);
+    }
+    switch (sg.K) {
+      case 5: fused_emit<5>(A, sg, local, part, SP, SM); break;
+      case 6: fused_emit<6>(A, sg, local, part, SP, SM); break;
+      case 7: fused_emit<7>(A, sg, local, part, SP, SM); break;
+      default: fused_emit<8>(A, sg, local, part, SP, SM); break;
+    }
+    __syncthreads();  // SP / SM and s_tk are rewritten by the next item
+    item = next;
+  }
+}
+
 // Workspace: [P/M segments: 2 * 2^n] (TRIDIAGONAL) + [x = 0 vector: 2^n] (world > 1: the
 // x = 0 intermediate when it does not fit the rank's output block) + [tail counters].
 constexpr size_t kTailCtrBytes = 256;
@@ -894,27 +1068,68 @@ cudaError_t launch_band(const double2* A, double2* out, int n, int structure, vo
     *nl += 1;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  // blocks t+1: P_t / M_t
+  // blocks t+1: P_t / M_t.  Segments t < tf run their last pass inside the fused expansion.
+  const int zs = world > 1 ? zshift : n;
+  const u64 NL = 1ull << zs;
+  FusedArgs FA{};
+  int tf = 0;
+  if (g <= 3 && NL >= 256) {
+    for (int t = 0; t <= kFuseMaxT && t < n; ++t) {
+      const int lam = n - t - 1, lamp = lam - 3;
+      if (lam < kTopMin || lamp < 13 || lamp > 20) break;
+      FusedSeg& sg = FA.s[tf];
+      sg.P = PM + 2 * (N - (N >> t));
+      sg.tiles = ((u64)1 << (lamp + k_keep)) / (u64)kTileElems;
+      sg.lamp = lamp;
+      sg.K = lamp - 8 < 8 ? lamp - 8 : 8;
+      sg.t = t;
+      sg.parts_log = t > 1 ? t - 1 : 0;  // <= 256 KiB of output per work item
+      ++tf;
+    }
+  }
   for (int t = 0; t < n; ++t) {
     const int lam = n - t - 1;
     const u64 seg = N - (N >> t);
     if (lam >= kTopMin) {
       WhtFamily f{PM + 2 * seg, PM + 2 * seg, lam - 3, 2ull << k_keep, 1.0};  // P then M branches
       f.first_bit = 0;
+      f.skip_last = t < tf ? 1 : 0;
       fam[nf++] = f;
     } else {
       fam[nf++] = WhtFamily{PM + 2 * seg, PM + 2 * seg, lam, 2, 1.0};
     }
   }
   if ((e = run_families(fam, nf, st, nl)) != cudaSuccess) return e;
+  if (tf > 0) {
+    // largest outputs per tile first (t descending) for the dynamic tickets
+    FusedArgs B = FA;
+    u64 first = 0;
+    for (int i = 0; i < tf; ++i) {
+      B.s[i] = FA.s[tf - 1 - i];
+      B.s[i].first_tile = first;
+      first += B.s[i].tiles << B.s[i].parts_log;
+    }
+    B.count = tf;
+    B.total_tiles = first;
+    B.out = out;
+    B.NL = NL;
+    B.scale = scale;
+    B.ticket = tail_ctr + 63;
+    if ((e = cudaMemsetAsync(B.ticket, 0, 4, st)) != cudaSuccess) return e;
+    if ((e = ensure_smem_attr(reinterpret_cast<const void*>(tri_fused_expand_kernel), kFusedSmem)) != cudaSuccess)
+      return e;
+    u64 grid = (u64)sms;
+    if (grid > first) grid = first;
+    tri_fused_expand_kernel<<<(unsigned)grid, kThreads, kFusedSmem, st>>>(B);
+    *nl += 1;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
   {
-    const int zs = world > 1 ? zshift : n;
-    const u64 NL = 1ull << zs;
     const u64 total = (u64)n * NL;
     if (NL >= 256) {
       u64 blocks = (total / 8 + 255) / 256;
       if (blocks > (u64)sms * 16) blocks = (u64)sms * 16;
-      tridiag_expand_kernel<<<(unsigned)blocks, 256, 0, st>>>(PM, out, n, scale, zs, zrank, k_keep);
+      tridiag_expand_kernel<<<(unsigned)blocks, 256, 0, st>>>(PM, out, n, scale, zs, zrank, k_keep, tf);
     } else {
       tridiag_expand_small_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(PM, out, n, scale, zs,
                                                                                  zrank, k_keep);

@@ -22,6 +22,7 @@ struct WhtFamily {
                                  //   the family starts at pass first_bit / 8 and never uses the
                                  //   whole-vector tiles)
   unsigned long long zoff = 0;   // z of element 0 of the last pass's output (the px phase uses z)
+  int skip_last = 0;             // 1: the last pass runs elsewhere (fused into a consumer kernel)
 };
 
 constexpr int kMaxFamilies = 40;  // per run_families call

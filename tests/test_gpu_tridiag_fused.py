@@ -1,0 +1,57 @@
+"""Complex, non-symmetric tridiagonals at the sizes where the last P/M pass runs fused with the
+expansion (band.cu tri_fused_expand_kernel: segments t <= 3 with 13..20-bit branches, n = 17..24).
+
+The BASELINE n = 24 input is real symmetric (sub[i+1] = sup[i]), so M_t = WHT(S_t - U_t) = 0
+there; these inputs make every M_t nonzero and complex.  Checked against the oracle (the
+definition Tr(P A)/2^n entry by entry, Sec. IV-A l.395-465) at sampled strings of every
+output block incl. the fused ones, exact zeros outside the support (Table I, l.513), Parseval,
+and the z-shards at G = 2 / 8 bit for bit against the one-GPU result."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2403_11644_b200 as ptdr
+from paper_2403_11644_b200 import dist as pdist
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+def _band(n, seed):
+    rng = np.random.default_rng(seed)
+    N = 1 << n
+    sub, main, sup = (rng.standard_normal(N) + 1j * rng.standard_normal(N) for _ in range(3))
+    sub[0] = 0.0        # A[0][-1] does not exist
+    sup[N - 1] = 0.0    # A[N-1][N] does not exist
+    return sub, main, sup
+
+
+@pytest.mark.parametrize("n", [17, 19, 21])
+def test_fused_tridiagonal_vs_oracle(gpu, n):
+    import torch
+
+    sub, main, sup = _band(n, 900 + n)
+    B = torch.from_numpy(np.stack([sub, main, sup])).cuda()
+    out = ptdr.decompose(B, "tridiagonal").cpu().numpy()
+    N = 1 << n
+    # Parseval: sum |alpha|^2 = ||A||_F^2 / 2^n
+    fro2 = sum(float(np.sum(np.abs(v) ** 2)) for v in (sub, main, sup))
+    assert abs(float(np.sum(np.abs(out) ** 2)) - fro2 / N) <= 1e-11 * fro2 / N
+    rng = np.random.default_rng(n)
+    blocks = np.concatenate([np.repeat(np.arange(n + 1), 4), rng.integers(0, n + 1, 384)])
+    zs = np.concatenate([np.tile([0, 1, N - 2, N - 1], n + 1), rng.integers(0, N, 384)])
+    qs = np.array([ptdr.q_of((1 << int(b)) - 1, int(z), n) for b, z in zip(blocks, zs)], dtype=np.uint64)
+    want = oracle.coeffs_tridiagonal(sub, main, sup, qs)
+    got = out.reshape(n + 1, N)[blocks, zs]
+    maxabs = max(np.max(np.abs(v)) for v in (sub, main, sup))
+    assert np.max(np.abs(got - want)) <= TOL * maxabs
+    # strings outside the n + 1 X-masks 2^b - 1 are exactly zero
+    inside = {(1 << b) - 1 for b in range(n + 1)}
+    xo = [x for x in rng.integers(0, N, 64) if int(x) not in inside][:32]
+    qo = np.array([ptdr.q_of(int(x), int(z), n) for x, z in zip(xo, rng.integers(0, N, len(xo)))], dtype=np.uint64)
+    assert np.all(oracle.coeffs_tridiagonal(sub, main, sup, qo) == 0)
+    # the z-sharded path (fused for G <= 8) is the same slice bit for bit
+    for world in (2, 8):
+        parts = [ptdr.decompose_zshard(B, "tridiagonal", r, world).cpu().numpy() for r in range(world)]
+        full = pdist.assemble_zshards(parts, n, n + 1)
+        assert np.array_equal(full.view(np.uint64), out.view(np.uint64)), world

@@ -260,8 +260,11 @@ ptdr_status ptdr_decompose_band_async(const ptdr_c128* diags, int n, int s, ptdr
 
 /* Inverse transform A = sum_P alpha_P P (l.116-121): dense row-major A [2^n][2^n] from the
  * 4^n q-ordered coefficients.  Same path as the decomposition run backwards (per X-mask:
- * conjugate phase, WHT over z, XOR scatter into rows).  workspace >= 16 * 4^n bytes
- * (ptdr_reconstruct_workspace_bytes), 256-byte aligned; coeffs, A, workspace disjoint. */
+ * conjugate phase, WHT over z, XOR scatter into rows): n >= 11 is one launch of the dense TMA
+ * pipeline whose phase A reads q-order boxes (W^2 consecutive q each) and whose phase B stores
+ * the XOR-diagonals into A's rows; smaller n a multi-pass kernel.  workspace >=
+ * ptdr_reconstruct_workspace_bytes(n) (the pipeline's scratch, <= 2 GiB + counters, for
+ * n >= 11; 16 * 4^n bytes below), 256-byte aligned; coeffs, A, workspace disjoint. */
 size_t ptdr_reconstruct_workspace_bytes(int n);
 ptdr_status ptdr_reconstruct_async(const ptdr_c128* coeffs, int n, ptdr_c128* A, void* workspace,
                                    size_t ws_bytes, void* stream);

@@ -222,6 +222,26 @@ static ptdr_status run_dense(const double2* A, int n, int s, double2* out, void*
   }
 }
 
+// The inverse transform on the dense pipeline (MODE_INV from the matrix layout, MODE_INVQ from
+// q order): the forward kernel with the phase (-i)^{popcount(x & z)} applied on input, no
+// scale, and the matrix-layout store A[i][i ^ x] (dense_pipe.cuh).  Sizes with the pipeline only.
+static bool inv_pipe(int n) {
+  const DensePlan p = plan_for(MODE_GENERAL, n, 1ull << n);
+  return p.pipe_cfg != kPipeNone && p.kind == 2;
+}
+static ptdr_status run_inverse_pipe(int mode, const double2* src, int n, double2* out, void* ws, cudaStream_t st,
+                                    int* nl) {
+  const DensePlan p = plan_for(MODE_GENERAL, n, 1ull << n);
+  DenseArgs a = base_args(src, out, n, ws);
+  a.scale = 1.0;
+  a.layout_mat = 1;
+  a.nv = n;
+  a.x_base = 0;
+  a.nchunks = p.nchunks;
+  a.scratch = reinterpret_cast<double2*>(reinterpret_cast<char*>(ws) + p.ctr_bytes);
+  return launch_mode(mode, a, p, st, nl);
+}
+
 static bool overlaps(const void* a, size_t abytes, const void* b, size_t bbytes) {
   const uintptr_t a0 = (uintptr_t)a, b0 = (uintptr_t)b;
   return a0 < b0 + bbytes && b0 < a0 + abytes;
@@ -560,6 +580,7 @@ ptdr_status ptdr_decompose_band_async(const ptdr_c128* diags, int n, int s, ptdr
 // ---- algebra and inverse transform (algebra.cu) ---------------------------------------
 size_t ptdr_reconstruct_workspace_bytes(int n) {
   if (n < 1 || n > 16) return (size_t)-1;
+  if (inv_pipe(n)) return plan_ws(n, 1ull << n);
   return reconstruct_workspace_bytes(n);
 }
 
@@ -571,10 +592,18 @@ ptdr_status ptdr_reconstruct_async(const ptdr_c128* coeffs, int n, ptdr_c128* A,
   if (((uintptr_t)coeffs & 15) || ((uintptr_t)A & 15) || ((uintptr_t)workspace & 255))
     return fail(PTDR_EINVAL, "misaligned pointer");
   const size_t nb = (size_t)16 << (2 * n);
-  if (ws_bytes < reconstruct_workspace_bytes(n)) return fail(PTDR_ENOMEM, "workspace too small");
-  if (overlaps(coeffs, nb, A, nb) || overlaps(workspace, nb, A, nb) || overlaps(workspace, nb, coeffs, nb))
+  const size_t need = ptdr_reconstruct_workspace_bytes(n);
+  if (ws_bytes < need) return fail(PTDR_ENOMEM, "workspace too small");
+  if (overlaps(coeffs, nb, A, nb) || overlaps(workspace, need, A, nb) || overlaps(workspace, need, coeffs, nb))
     return fail(PTDR_EUNSUPPORTED, "coeffs, A and workspace must be disjoint");
   int nl = 0;
+  if (inv_pipe(n)) {
+    const ptdr_status r = run_inverse_pipe(MODE_INVQ, reinterpret_cast<const double2*>(coeffs), n,
+                                           reinterpret_cast<double2*>(A), workspace,
+                                           reinterpret_cast<cudaStream_t>(stream), &nl);
+    g_last_launches = nl;
+    return r;
+  }
   cudaError_t e = launch_reconstruct(reinterpret_cast<const double2*>(coeffs), n, reinterpret_cast<double2*>(A),
                                      workspace, reinterpret_cast<cudaStream_t>(stream), &nl);
   g_last_launches = nl;
@@ -795,11 +824,6 @@ ptdr_status ptdr_decompose_matrix_layout_async(const ptdr_c128* A, int n, int st
 // forward pipeline with the phase moved from the epilogue into phase A (MODE_INV).  The input
 // M[z][z ^ x] = alpha(x, z) and the output share every XOR-diagonal, so it runs in place.
 // Sizes without the pipeline permute to q order in the workspace and call the q-order inverse.
-static bool inv_pipe(int n) {
-  const DensePlan p = plan_for(MODE_GENERAL, n, 1ull << n);
-  return p.pipe_cfg != kPipeNone && p.kind == 2;
-}
-
 __global__ void matrix_layout_to_q_kernel(const double2* __restrict__ M, int n, double2* __restrict__ Q) {
   const uint64_t N = 1ull << n;
   for (uint64_t id = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; id < N * N;
@@ -832,15 +856,7 @@ ptdr_status ptdr_reconstruct_matrix_layout_async(const ptdr_c128* M, int n, ptdr
   double2* a_out = reinterpret_cast<double2*>(A);
   int nl = 0;
   if (inv_pipe(n)) {
-    const DensePlan p = plan_for(MODE_GENERAL, n, 1ull << n);
-    DenseArgs a = base_args(m, a_out, n, workspace);
-    a.scale = 1.0;
-    a.layout_mat = 1;
-    a.nv = n;
-    a.x_base = 0;
-    a.nchunks = p.nchunks;
-    a.scratch = reinterpret_cast<double2*>(reinterpret_cast<char*>(workspace) + p.ctr_bytes);
-    const ptdr_status r = launch_mode(MODE_INV, a, p, st, &nl);
+    const ptdr_status r = run_inverse_pipe(MODE_INV, m, n, a_out, workspace, st, &nl);
     g_last_launches = nl;
     return r;
   }

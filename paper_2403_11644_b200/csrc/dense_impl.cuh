@@ -22,7 +22,8 @@ namespace ptdr {
 // half-length.  See DESIGN.md "Hermitian / real-symmetric path".
 enum { MODE_GENERAL = 0, MODE_HERM_MIRROR = 1, MODE_SYM_MIRROR = 2, MODE_HERM_HALF = 3, MODE_SYM_HALF = 4,
        MODE_GEN = 8 /* matrix-free GENERAL (pipeline only): entries generated in phase A */,
-       MODE_INV = 9 /* inverse transform from the matrix layout (pipeline only, see dense_pipe.cuh) */ };
+       MODE_INV = 9 /* inverse transform from the matrix layout (pipeline only, see dense_pipe.cuh) */,
+       MODE_INVQ = 10 /* inverse transform from q order (pipeline only) */ };
 
 struct DenseArgs {
   const double2* A;

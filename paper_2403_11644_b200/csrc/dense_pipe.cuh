@@ -156,7 +156,7 @@ struct EpiUnit {
 template <int MODE>
 __device__ __forceinline__ void emit_one(const DenseArgs& a, uint32_t q, uint32_t p, uint32_t dt,
                                          double2 w) {
-  if constexpr (MODE == MODE_INV) {
+  if constexpr (MODE == MODE_INV || MODE == MODE_INVQ) {
     st_out(a.out + q, w);  // the inverse: A[i][i ^ x] = WHT(u_x)[i], no phase, no scale
   } else if constexpr (MODE == MODE_GENERAL || MODE == MODE_GEN) {
     const bool sw = (p & 1u) != 0;
@@ -464,6 +464,17 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
         meta[s].slot = slot;
         if (phX == 0 && MODE == MODE_GEN) {
           mbar_arrive(fullk);  // matrix-free: the consumers generate the tile's entries
+        } else if (phX == 0 && MODE == MODE_INVQ) {
+          // inverse from q order: the W x W (X-mask low bits, z low bits) combinations of a
+          // box are W^2 consecutive q (the low 2 XB bits of q), one bulk copy per box
+          mbar_arrive_expect_tx(fullk, (uint32_t)Cfg::TB);
+          const uint32_t xh = ((uint32_t)a.x_base + (gch << XB)) >> XB;
+#pragma unroll
+          for (int rb = 0; rb < (1 << (R - XB)); ++rb) {
+            const uint32_t zh = ((tlX << R) + (uint32_t)rb * W) >> XB;
+            const uint64_t qb = (spread_bits((uint64_t)(xh ^ zh)) | (spread_bits((uint64_t)zh) << 1)) << (2 * XB);
+            bulk_load(dst + rb * W * W, a.A + qb, (uint32_t)(W * W * 16), fullk, pol);
+          }
         } else if (phX == 0) {
           mbar_arrive_expect_tx(fullk, (uint32_t)Cfg::TB);
           const uint32_t x0 = (uint32_t)a.x_base + (gch << XB);
@@ -667,13 +678,25 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
             v[kk] = gauss_pair(a.gen_seed, (i << a.n) + (i ^ x), 0u);
           }
         } else {
+          if constexpr (MODE == MODE_INVQ) {
+            // element (z = row r, X-mask u) of a box run sits at spread(r_l ^ u) | spread(r_l) << 1
+            // = spread(u) ^ 3 spread(r_l), r_l = r mod W
+            const uint32_t su = (uint32_t)spread_bits((uint64_t)u);
 #pragma unroll
-          for (int kk = 0; kk < 16; ++kk) {
-            const int r = jh * 16 + kk;
-            v[kk] = S[r * W + ((r & (W - 1)) ^ u)];
-            if (MODE == MODE_SYM_HALF) v[kk].y = 0.0;
+            for (int kk = 0; kk < 16; ++kk) {
+              const int r = jh * 16 + kk;
+              const uint32_t sr = (uint32_t)spread_bits((uint64_t)(r & (W - 1)));
+              v[kk] = S[(r >> XB) * W * W + (int)(su ^ (3u * sr))];
+            }
+          } else {
+#pragma unroll
+            for (int kk = 0; kk < 16; ++kk) {
+              const int r = jh * 16 + kk;
+              v[kk] = S[r * W + ((r & (W - 1)) ^ u)];
+              if (MODE == MODE_SYM_HALF) v[kk].y = 0.0;
+            }
           }
-          if constexpr (MODE == MODE_INV) {
+          if constexpr (MODE == MODE_INV || MODE == MODE_INVQ) {
             // inverse: the gathered element M[z][z ^ x] = alpha(x, z) of the
             // matrix-layout coefficients enters as u_x[z] = (-i)^{popcount(x & z)} alpha(x, z)
             // (z0 has 4 zero low bits, so popcount(x & z) = popcount(x & z0) + popcount(x & kk);
@@ -877,6 +900,9 @@ static cudaError_t launch_pipe_cfg(int mode, const TmapSet& map, const DenseArgs
       return cudaErrorInvalidValue;
     case MODE_INV:
       if constexpr (NR == 0 && LT == 12) return launch_pipe_m<LT, XB, GW, NG, NS, NR, MODE_INV>(map, a, M, st);
+      return cudaErrorInvalidValue;
+    case MODE_INVQ:
+      if constexpr (NR == 0 && LT == 12) return launch_pipe_m<LT, XB, GW, NG, NS, NR, MODE_INVQ>(map, a, M, st);
       return cudaErrorInvalidValue;
     default: return cudaErrorInvalidValue;
   }

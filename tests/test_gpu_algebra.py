@@ -68,6 +68,31 @@ def test_round_trip_large(gpu, n):
     torch.cuda.empty_cache()
 
 
+def test_round_trip_n16_q_order(gpu):
+    """n = 16 (64 GiB of coefficients, 64 GiB out): the q-order inverse runs in the pipeline's
+    2 GiB scratch, so A -> coefficients -> A fits one GPU; compared with the generator's rows
+    regenerated block by block."""
+    torch = _torch()
+    n, seed = 16, 5
+    A = ptdr.generate_dense(n, seed, "general")
+    maxabs = max(torch.max(torch.abs(A[i:i + 1024])).item() for i in range(0, A.shape[0], 1024))
+    c = ptdr.decompose(A)
+    del A
+    torch.cuda.empty_cache()
+    B = ptdr.reconstruct(c)
+    del c
+    torch.cuda.empty_cache()
+    err = 0.0
+    blk = 4096
+    for r0 in range(0, 1 << n, blk):
+        ref = ptdr.generate_dense(n, seed, "general", row0=r0, nrows=blk)
+        err = max(err, torch.max(torch.abs(B[r0:r0 + blk] - ref)).item())
+        del ref
+    del B
+    torch.cuda.empty_cache()
+    assert err <= 1e-12 * maxabs * n, err
+
+
 def test_axpby_is_linear_combination(gpu):
     # l.570-577: c(mu A + nu B) = mu c(A) + nu c(B)
     rng = np.random.default_rng(71)

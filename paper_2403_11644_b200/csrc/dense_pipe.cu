@@ -92,7 +92,19 @@ cudaError_t launch_dense_pipe(int mode, const DenseArgs& a_in, const DensePlan& 
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   };
   CUresult r = CUDA_SUCCESS;
-  if (a.peer_shift) {
+  if (mode == MODE_INVQ) {
+    // q-ordered coefficients viewed as [4^n / 8 rows][8 complex128 = 128 B]: a box of W^2
+    // consecutive q is W^2 / 8 rows; the 128-byte swizzle spreads a phase-A read (16 lanes
+    // along the X-mask, fixed z) over all eight 16-byte slots of a bank row
+    if (W * W % 8 != 0) return cudaErrorInvalidValue;
+    const cuuint64_t rows = (1ull << (2 * a.n)) / 8ull;
+    cuuint64_t gdim[2] = {16, rows};
+    cuuint64_t gstride[1] = {128};
+    cuuint32_t qbox[2] = {16, W * W / 8};
+    r = enc(&map.m[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double2*>(a.A), gdim, gstride, qbox, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else if (a.peer_shift) {
     // peer-pull: one map per rank's row-block shard [R rows][2^n columns] (row pitch a.ld)
     if (a.npeers < 1 || a.npeers > kMaxPeers) return cudaErrorInvalidValue;
     for (int g = 0; g < a.npeers && r == CUDA_SUCCESS; ++g)

@@ -466,14 +466,15 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
           mbar_arrive(fullk);  // matrix-free: the consumers generate the tile's entries
         } else if (phX == 0 && MODE == MODE_INVQ) {
           // inverse from q order: the W x W (X-mask low bits, z low bits) combinations of a
-          // box are W^2 consecutive q (the low 2 XB bits of q), one bulk copy per box
+          // box are W^2 consecutive q (the low 2 XB bits of q): one TMA box of W^2 / 8 rows of
+          // the [4^n / 8][8] view, 128-byte swizzled (launch_dense_pipe)
           mbar_arrive_expect_tx(fullk, (uint32_t)Cfg::TB);
           const uint32_t xh = ((uint32_t)a.x_base + (gch << XB)) >> XB;
 #pragma unroll
           for (int rb = 0; rb < (1 << (R - XB)); ++rb) {
             const uint32_t zh = ((tlX << R) + (uint32_t)rb * W) >> XB;
             const uint64_t qb = (spread_bits((uint64_t)(xh ^ zh)) | (spread_bits((uint64_t)zh) << 1)) << (2 * XB);
-            bulk_load(dst + rb * W * W, a.A + qb, (uint32_t)(W * W * 16), fullk, pol);
+            tma_load_2d(dst + rb * W * W, &maps.m[0], 0, (int)(qb >> 3), fullk, pol);
           }
         } else if (phX == 0) {
           mbar_arrive_expect_tx(fullk, (uint32_t)Cfg::TB);
@@ -679,14 +680,17 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
           }
         } else {
           if constexpr (MODE == MODE_INVQ) {
-            // element (z = row r, X-mask u) of a box run sits at spread(r_l ^ u) | spread(r_l) << 1
-            // = spread(u) ^ 3 spread(r_l), r_l = r mod W
+            // element (z = row r, X-mask u) is q8 = spread(r_l ^ u) | spread(r_l) << 1 =
+            // spread(u) ^ 3 spread(r_l) of its box (r_l = r mod W); the swizzled box holds
+            // 128-byte row q8 >> 3 with its 16-byte chunk q8 & 7 at chunk (q8 & 7) ^ (row & 7)
             const uint32_t su = (uint32_t)spread_bits((uint64_t)u);
 #pragma unroll
             for (int kk = 0; kk < 16; ++kk) {
               const int r = jh * 16 + kk;
               const uint32_t sr = (uint32_t)spread_bits((uint64_t)(r & (W - 1)));
-              v[kk] = S[(r >> XB) * W * W + (int)(su ^ (3u * sr))];
+              const uint32_t q8 = su ^ (3u * sr);
+              const uint32_t row = q8 >> 3;
+              v[kk] = S[(r >> XB) * W * W + (int)((row << 3) | ((q8 ^ row) & 7u))];
             }
           } else {
 #pragma unroll

@@ -64,6 +64,15 @@ typedef struct {
  *  ANTI_DIAGONAL  A = a[2^n] with a[i] = A[i][2^n - 1 - i] (the anti-diagonal remark,
  *                 l.391-392: swap I,Z <-> X,Y); output = the 2^n {X,Y}^n coefficients
  *                 (X-mask 2^n - 1), ascending z.
+ *  HERMITIAN_TRIDIAGONAL  A = band array [2][2^n]: main[i]=A[i][i], sup[i]=A[i][i+1]
+ *                 (sup[2^n-1] ignored); the sub-diagonal is A[i+1][i] = conj(sup[i]) and not
+ *                 stored (a real symmetric tridiagonal is the real case; the main diagonal is
+ *                 used as given, real for a Hermitian A).  Output exactly as TRIDIAGONAL.
+ *                 With S_t the sup samples of segment t and W_t = WHT(S_t), the TRIDIAGONAL
+ *                 path's P_t = WHT(S_t + conj S_t) = (2 Re W_t, 0) and M_t = (0, 2 Im W_t):
+ *                 one WHT per segment instead of two (Theorem 2, l.123-136: Hermitian
+ *                 matrices have real coefficients; l.395-465 for the tridiagonal structure),
+ *                 bitwise equal to TRIDIAGONAL on the same matrix.
  * X-mask / Z-mask of a string: bit l of x is set iff sigma_l in {X,Y}; bit l of z
  * is set iff sigma_l in {Y,Z}. */
 typedef enum {
@@ -72,7 +81,8 @@ typedef enum {
   PTDR_REAL_SYMMETRIC = 2,
   PTDR_DIAGONAL = 3,
   PTDR_TRIDIAGONAL = 4,
-  PTDR_ANTI_DIAGONAL = 5
+  PTDR_ANTI_DIAGONAL = 5,
+  PTDR_HERMITIAN_TRIDIAGONAL = 6
 } ptdr_structure;
 
 typedef enum {
@@ -314,7 +324,9 @@ ptdr_status ptdr_generate_dense_async(int n, uint64_t seed, int variant, uint64_
 
 /* Same generator for the band inputs: variant 3 (DIAGONAL) writes d[2^n] into
  * band; variant 4 (TRIDIAGONAL) writes the [3][2^n] sub/main/sup array (sub[0] and
- * sup[2^n-1] written as 0).  fro2_partials: as above, over the band's entries. */
+ * sup[2^n-1] written as 0); variant 6 (HERMITIAN_TRIDIAGONAL) writes [main | sup] of the
+ * same real symmetric matrix.  fro2_partials: as above, over the matrix's entries (variant 6
+ * counts the implied sub-diagonal). */
 ptdr_status ptdr_generate_band_async(int n, uint64_t seed, int variant, ptdr_c128* band,
                                      double* fro2_partials, void* stream);
 

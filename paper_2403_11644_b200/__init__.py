@@ -20,6 +20,7 @@ STRUCTURES = {
     "diagonal": 3,
     "tridiagonal": 4,
     "anti_diagonal": 5,
+    "hermitian_tridiagonal": 6,
 }
 PTDR_OK, PTDR_EINVAL, PTDR_EUNSUPPORTED, PTDR_ENOMEM, PTDR_ECUDA = 0, 1, 2, 3, 4
 
@@ -223,7 +224,8 @@ def _pow2_exponent(N: int, what: str) -> int:
 
 def n_of(A, structure="general") -> int:
     """n of an input array: dense [2^n, 2^n]; DIAGONAL / ANTI_DIAGONAL [2^n];
-    TRIDIAGONAL [3, 2^n] (or 3 * 2^n elements).  Torch tensors or numpy arrays."""
+    TRIDIAGONAL [3, 2^n] (or 3 * 2^n elements); HERMITIAN_TRIDIAGONAL [2, 2^n] (main, sup).
+    Torch tensors or numpy arrays."""
     s = _structure(structure)
     ndim = len(A.shape)
     numel = 1
@@ -242,6 +244,10 @@ def n_of(A, structure="general") -> int:
         if numel % 3 != 0 or (ndim == 2 and A.shape[0] != 3) or ndim > 2:
             raise ValueError("TRIDIAGONAL input is [3, 2^n] (sub, main, sup)")
         return _pow2_exponent(numel // 3, "the band length")
+    if s == 6:
+        if numel % 2 != 0 or (ndim == 2 and A.shape[0] != 2) or ndim > 2:
+            raise ValueError("HERMITIAN_TRIDIAGONAL input is [2, 2^n] (main, sup)")
+        return _pow2_exponent(numel // 2, "the band length")
     raise ValueError(f"unknown structure {structure!r}")
 
 
@@ -825,11 +831,11 @@ def generate_band(n: int, seed: int, variant="tridiagonal", out=None, device=Non
     import torch
 
     v = _structure(variant)
-    shape = (1 << n,) if v == 3 else (3, 1 << n)
+    shape = (1 << n,) if v == 3 else (2, 1 << n) if v == 6 else (3, 1 << n)
     if out is None:
         out = torch.empty(shape, dtype=torch.complex128, device=device or "cuda")
         _keep_for_stream(stream, out)
-    _require_cuda_c128(out, "out", shape[0] if v == 3 else 3 << n)
+    _require_cuda_c128(out, "out", shape[0] if v == 3 else shape[0] << n)
     st = lib().ptdr_generate_band_async(n, seed, v, ctypes.c_void_p(out.data_ptr()), _fro2_ptr(fro2),
                                         _stream_ptr(stream))
     _check(st, "ptdr_generate_band_async")

@@ -66,7 +66,10 @@ ptdr_status plan_fail(ptdr_status s, const char* msg) { return fail(s, msg); }
 ptdr_status plan_cuda_fail(cudaError_t e, const char* where) { return cuda_fail(e, where); }
 
 static bool is_dense(int s) { return s >= PTDR_GENERAL && s <= PTDR_REAL_SYMMETRIC; }
-static bool is_band(int s) { return s == PTDR_DIAGONAL || s == PTDR_TRIDIAGONAL || s == PTDR_ANTI_DIAGONAL; }
+static bool is_band(int s) {
+  return s == PTDR_DIAGONAL || s == PTDR_TRIDIAGONAL || s == PTDR_ANTI_DIAGONAL || s == PTDR_HERMITIAN_TRIDIAGONAL;
+}
+static bool is_tri(int s) { return s == PTDR_TRIDIAGONAL || s == PTDR_HERMITIAN_TRIDIAGONAL; }
 static bool valid_n(int n, int s) {
   if (is_dense(s)) return n >= 1 && n <= 16;
   if (is_band(s)) return n >= 1 && n <= 28;
@@ -267,14 +270,14 @@ size_t ptdr_input_count(int n, int s) {
   if (!valid_n(n, s)) return 0;
   const size_t N = (size_t)1 << n;
   if (is_dense(s)) return N * N;
-  return s == PTDR_TRIDIAGONAL ? 3 * N : N;
+  return s == PTDR_TRIDIAGONAL ? 3 * N : s == PTDR_HERMITIAN_TRIDIAGONAL ? 2 * N : N;
 }
 
 size_t ptdr_output_count(int n, int s) {
   if (!valid_n(n, s)) return 0;
   const size_t N = (size_t)1 << n;
   if (is_dense(s)) return N * N;
-  return s == PTDR_TRIDIAGONAL ? (size_t)(n + 1) * N : N;
+  return is_tri(s) ? (size_t)(n + 1) * N : N;
 }
 
 size_t ptdr_workspace_bytes(int n, int s, int world) {
@@ -524,7 +527,8 @@ ptdr_status ptdr_decompose_zshard_async(const ptdr_c128* band, int n, int struct
                                         ptdr_c128* out_local, void* workspace, size_t ws_bytes,
                                         void* stream) {
   g_last_launches = 0;
-  if (!is_band(structure)) return fail(PTDR_EINVAL, "z-sharding is for DIAGONAL / TRIDIAGONAL / ANTI_DIAGONAL");
+  if (!is_band(structure))
+    return fail(PTDR_EINVAL, "z-sharding is for DIAGONAL / TRIDIAGONAL / ANTI_DIAGONAL / HERMITIAN_TRIDIAGONAL");
   if (!valid_n(n, structure)) return fail(PTDR_EINVAL, "invalid n");
   if (world < 1 || (world & (world - 1))) return fail(PTDR_EINVAL, "world must be a power of two");
   if ((uint64_t)world > (1ull << n)) return fail(PTDR_EINVAL, "world > 2^n");
@@ -1018,7 +1022,7 @@ ptdr_status ptdr_generate_dense_async(int n, uint64_t seed, int variant, uint64_
 ptdr_status ptdr_generate_band_async(int n, uint64_t seed, int variant, ptdr_c128* band,
                                      double* fro2_partials, void* stream) {
   g_last_launches = 0;
-  if (n < 1 || n > 28 || (variant != 3 && variant != 4)) return fail(PTDR_EINVAL, "invalid n or variant");
+  if (n < 1 || n > 28 || (variant != 3 && variant != 4 && variant != 6)) return fail(PTDR_EINVAL, "invalid n or variant");
   if (!band || ((uintptr_t)band & 15)) return fail(PTDR_EINVAL, "null or misaligned band");
   if (!fro2_ok(fro2_partials)) return fail(PTDR_EINVAL, "misaligned fro2_partials");
   cudaError_t e = launch_generate_band(n, seed, variant, reinterpret_cast<double2*>(band), fro2_partials,

@@ -139,6 +139,29 @@ __device__ __forceinline__ SegView seg_view(const double2* PM, int n, int t, int
   return SegView{Pt, Pt + (1ull << lam), ~0ull};
 }
 
+// HERMITIAN_TRIDIAGONAL (sub[i + 1] = conj(sup[i])): U_t = conj(S_t), so with W_t = WHT(S_t)
+// P_t = W_t + conj(W_t) = (2 Re W_t, 0) and M_t = (0, 2 Im W_t) -- one WHT per segment instead
+// of two, stored as S_t at PM + (2^n - 2^(n-t)) (KS branches of 2^(lam-3) for long segments).
+// For an input that satisfies the relation exactly, these are bitwise the P_t / M_t of the
+// general path: 2x is exact, and S + conj(S), S - conj(S) have exact +0 parts.
+__device__ __forceinline__ SegView herm_seg_view(const double2* W, int n, int t, int k_keep) {
+  const u64 N = 1ull << n;
+  const int lam = n - t - 1;
+  const double2* St = W + (N - (N >> t));
+  if (lam >= kTopMin) return SegView{St, St, (1ull << (lam - 3 + k_keep)) - 1ull};
+  return SegView{St, St, ~0ull};
+}
+template <bool HERM>
+__device__ __forceinline__ double2 pm_value(const SegView& sv, bool use_p, u64 idx) {
+  if constexpr (HERM) {
+    const double2 w = __ldg(sv.P + idx);
+    return use_p ? make_double2(2.0 * w.x, 0.0) : make_double2(0.0, 2.0 * w.y);
+  } else {
+    return __ldg((use_p ? sv.P : sv.M) + idx);
+  }
+}
+
+template <bool HERM>
 __global__ void __launch_bounds__(256) tridiag_expand_kernel(const double2* PM, double2* out, int n,
                                                              double scale, int zshift, u64 zrank, int k_keep,
                                                              int t_first) {
@@ -152,7 +175,7 @@ __global__ void __launch_bounds__(256) tridiag_expand_kernel(const double2* PM, 
        gidx += ((u64)gridDim.x * blockDim.x) >> 5) {
     const u64 id0 = gidx << 8;
     const int t = (int)(id0 >> zshift);
-    const SegView sv = seg_view(PM, n, t, k_keep);
+    const SegView sv = HERM ? herm_seg_view(PM, n, t, k_keep) : seg_view(PM, n, t, k_keep);
     double2 w[8];
     int ph[8];
 #pragma unroll
@@ -162,7 +185,7 @@ __global__ void __launch_bounds__(256) tridiag_expand_kernel(const double2* PM, 
       const u64 zh = z >> (t + 1);
       const int s1 = __popcll(z & ((1ull << t) - 1ull)) & 1;
       const int s2 = (int)((z >> t) & 1ull);
-      w[k] = __ldg(((s1 == s2) ? sv.P : sv.M) + (zh & sv.mask));
+      w[k] = pm_value<HERM>(sv, s1 == s2, zh & sv.mask);
       ph[k] = __popcll(zl) + 2 * s1;  // i^{popcount(zl)} * (-1)^{s1}
     }
 #pragma unroll
@@ -177,6 +200,7 @@ __global__ void __launch_bounds__(256) tridiag_expand_kernel(const double2* PM, 
 }
 
 // Small slices (2^zshift < 256): one output per thread.
+template <bool HERM>
 __global__ void tridiag_expand_small_kernel(const double2* PM, double2* out, int n, double scale,
                                             int zshift, u64 zrank, int k_keep) {
   const u64 N = 1ull << n;
@@ -185,11 +209,11 @@ __global__ void tridiag_expand_small_kernel(const double2* PM, double2* out, int
   if (id >= (u64)n * NL) return;
   const int t = (int)(id >> zshift);
   const u64 z = (zrank << zshift) + (id & (NL - 1));
-  const SegView sv = seg_view(PM, n, t, k_keep);
+  const SegView sv = HERM ? herm_seg_view(PM, n, t, k_keep) : seg_view(PM, n, t, k_keep);
   const u64 zl = z & ((2ull << t) - 1ull);
   const int s1 = __popcll(z & ((1ull << t) - 1ull)) & 1;
   const int s2 = (int)((z >> t) & 1ull);
-  const double2 w = ((s1 == s2) ? sv.P : sv.M)[(z >> (t + 1)) & sv.mask];
+  const double2 w = pm_value<HERM>(sv, s1 == s2, (z >> (t + 1)) & sv.mask);
   const int ph = __popcll(zl) + 2 * s1;
   const double2 c = rot_ipow(w, ph);
   out[NL + id] = make_double2(c.x * scale, c.y * scale);
@@ -628,6 +652,42 @@ __global__ void __launch_bounds__(256) tri_split_top3_kernel(const double2* __re
   }
 }
 
+// HERMITIAN_TRIDIAGONAL split: S_t only (sup; the sub-diagonal is conj(sup) and not stored).
+template <int KK>
+__global__ void __launch_bounds__(256) htri_split_top3_kernel(const double2* __restrict__ sup, double2* W, int n,
+                                                              unsigned rsel) {
+  const u64 N = 1ull << n;
+  const u64 Q = N >> 3;
+  constexpr int KS = 1 << KK;
+  for (u64 il = (u64)blockIdx.x * blockDim.x + threadIdx.x; il < Q - 1; il += (u64)gridDim.x * blockDim.x) {
+    const int t = __ffsll((long long)~il) - 1;
+    const int lam = n - t - 1;
+    if (lam < kTopMin) continue;
+    double2 S[8];
+#pragma unroll
+    for (int h = 0; h < 8; ++h) S[h] = ld_stream(sup + (u64)h * Q + il);
+    const u64 seg = N - (N >> t);
+    const int Lb = lam - 3;
+    double2* St = W + seg;
+    const u64 hl = il >> (t + 1);
+    double2 o[KS];
+    topk_kept<3, KK>(S, rsel, o);
+#pragma unroll
+    for (int kt = 0; kt < KS; ++kt) st_l2(St + ((u64)kt << Lb) + hl, o[kt]);
+  }
+}
+__global__ void htri_split_small_kernel(const double2* __restrict__ sup, double2* W, int n, int lam_max) {
+  const u64 N = 1ull << n;
+  const u64 total = (2ull << lam_max) - 1ull;
+  for (u64 id = (u64)blockIdx.x * blockDim.x + threadIdx.x; id < total; id += (u64)gridDim.x * blockDim.x) {
+    const int lam = 63 - __clzll((long long)(id + 1));
+    const u64 h = id + 1 - (1ull << lam);
+    const int t = n - 1 - lam;
+    const u64 i = (h << (t + 1)) + (1ull << t) - 1ull;
+    W[(N - (N >> t)) + h] = ld_stream(sup + i);
+  }
+}
+
 // Split of the short segments (lam < kTopMin, replicated on every rank): one thread per
 // (lam, h), id = 2^lam - 1 + h; full P_t (2^lam) then M_t (2^lam).
 __global__ void tri_split_small_kernel(const double2* __restrict__ band, double2* PM, int n, int lam_max) {
@@ -803,7 +863,7 @@ struct FusedArgs {
 };
 constexpr int kFusedSmem = 2 * kTileBytes;
 
-template <int K>
+template <int K, bool HERM>
 __device__ __forceinline__ void fused_load(const FusedSeg& sg, u64 local, double2 (&vP)[16], double2 (&vM)[16]) {
   constexpr int F = kTileElems >> K;
   const int tid = threadIdx.x;
@@ -816,7 +876,7 @@ __device__ __forceinline__ void fused_load(const FusedSeg& sg, u64 local, double
     const u64 j = (u64)((jh << 4) + kk);
     const u64 e = ((rho >> 8) << (8 + K)) | (j << 8) | (rho & msk);
     vP[kk] = ld_l2(sg.P + e);
-    vM[kk] = ld_l2(M + e);
+    if constexpr (!HERM) vM[kk] = ld_l2(M + e);
   }
 }
 
@@ -851,7 +911,7 @@ __device__ __forceinline__ void fused_transform(double2* S, double2 (&v)[16]) {
 // Outputs of slots [part S_p, (part + 1) S_p) of the tile (S_p = 4096 / parts).  Thread tid
 // writes o = tid + 256 i: zl = o mod 2^(t+1) is fixed per thread (t <= 3), so the phase and
 // the P/M choice are too; slot = j F + f maps to e = e0 + (j << 8) + f (F <= 256).
-template <int K>
+template <int K, bool HERM>
 __device__ __forceinline__ void fused_emit(const FusedArgs& A, const FusedSeg& sg, u64 local, int part,
                                            const double2* SP, const double2* SM) {
   constexpr int F = kTileElems >> K;
@@ -865,7 +925,7 @@ __device__ __forceinline__ void fused_emit(const FusedArgs& A, const FusedSeg& s
   const int zl = threadIdx.x & ((1 << tb) - 1);
   const int s1 = __popc(zl & ((1 << t) - 1)) & 1;
   const int s2 = (zl >> t) & 1;
-  const double2* src = s1 == s2 ? SP : SM;
+  const double2* src = (HERM || s1 == s2) ? SP : SM;
   const int ph = __popc(zl) + 2 * s1;
   const bool sw = (ph & 1) != 0;
   const double sc = (ph & 2) ? -A.scale : A.scale;
@@ -874,7 +934,8 @@ __device__ __forceinline__ void fused_emit(const FusedArgs& A, const FusedSeg& s
   for (u64 o = threadIdx.x; o < per; o += kThreads) {
     const int slot = slot_base + (int)(o >> tb);
     const int f = slot & (F - 1), j = slot / F;
-    const double2 w = src[slot];
+    double2 w = src[slot];
+    if constexpr (HERM) w = s1 == s2 ? make_double2(2.0 * w.x, 0.0) : make_double2(0.0, 2.0 * w.y);
     const double re = sw ? -w.y : w.x;
     const double im = sw ? w.x : w.y;
     st_stream(base + ((((u64)j << 8) + (u64)f) << tb), make_double2(re * sc, im * sc));
@@ -887,19 +948,22 @@ __device__ __forceinline__ int fused_seg_of(const FusedArgs& A, u64 tile) {
   return i;
 }
 
-template <int K>
-__device__ __forceinline__ void fused_load_k(const FusedSeg& sg, u64 local, double2 (&vP)[16], double2 (&vM)[16]) {
-  fused_load<K>(sg, local, vP, vM);
-}
+template <bool HERM>
 __device__ __forceinline__ void fused_load_any(const FusedSeg& sg, u64 local, double2 (&vP)[16], double2 (&vM)[16]) {
   switch (sg.K) {
-    case 5: fused_load_k<5>(sg, local, vP, vM); break;
-    case 6: fused_load_k<6>(sg, local, vP, vM); break;
-    case 7: fused_load_k<7>(sg, local, vP, vM); break;
-    default: fused_load_k<8>(sg, local, vP, vM); break;
+    case 5: fused_load<5, HERM>(sg, local, vP, vM); break;
+    case 6: fused_load<6, HERM>(sg, local, vP, vM); break;
+    case 7: fused_load<7, HERM>(sg, local, vP, vM); break;
+    default: fused_load<8, HERM>(sg, local, vP, vM); break;
   }
 }
+template <int K, bool HERM>
+__device__ __forceinline__ void fused_transform2(double2* SP, double2* SM, double2 (&vP)[16], double2 (&vM)[16]) {
+  fused_transform<K>(SP, vP);
+  if constexpr (!HERM) fused_transform<K>(SM, vM);
+}
 
+template <bool HERM>
 __global__ void __launch_bounds__(kThreads, 1) tri_fused_expand_kernel(const __grid_constant__ FusedArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* SP = reinterpret_cast<double2*>(smem_raw);
@@ -911,7 +975,7 @@ __global__ void __launch_bounds__(kThreads, 1) tri_fused_expand_kernel(const __g
   double2 vP[16], vM[16];
   if (item < A.total_tiles) {
     const FusedSeg& sg = A.s[fused_seg_of(A, item)];
-    fused_load_any(sg, (item - sg.first_tile) >> sg.parts_log, vP, vM);
+    fused_load_any<HERM>(sg, (item - sg.first_tile) >> sg.parts_log, vP, vM);
   }
   while (item < A.total_tiles) {
     const FusedSeg& sg = A.s[fused_seg_of(A, item)];
@@ -919,10 +983,10 @@ __global__ void __launch_bounds__(kThreads, 1) tri_fused_expand_kernel(const __g
     const u64 local = rel >> sg.parts_log;
     const int part = (int)(rel & ((1ull << sg.parts_log) - 1ull));
     switch (sg.K) {
-      case 5: fused_transform<5>(SP, vP); fused_transform<5>(SM, vM); break;
-      case 6: fused_transform<6>(SP, vP); fused_transform<6>(SM, vM); break;
-      case 7: fused_transform<7>(SP, vP); fused_transform<7>(SM, vM); break;
-      default: fused_transform<8>(SP, vP); fused_transform<8>(SM, vM); break;
+      case 5: fused_transform2<5, HERM>(SP, SM, vP, vM); break;
+      case 6: fused_transform2<6, HERM>(SP, SM, vP, vM); break;
+      case 7: fused_transform2<7, HERM>(SP, SM, vP, vM); break;
+      default: fused_transform2<8, HERM>(SP, SM, vP, vM); break;
     }
     // next ticket, and its loads issued before this item's output loop
     if (threadIdx.x == 0) s_tk = atomicAdd(A.ticket, 1u);
@@ -930,25 +994,30 @@ __global__ void __launch_bounds__(kThreads, 1) tri_fused_expand_kernel(const __g
     const u64 next = s_tk;
     if (next < A.total_tiles) {
       const FusedSeg& sn = A.s[fused_seg_of(A, next)];
-      fused_load_any(sn, (next - sn.first_tile) >> sn.parts_log, vP, vM);
+      fused_load_any<HERM>(sn, (next - sn.first_tile) >> sn.parts_log, vP, vM);
     }
     switch (sg.K) {
-      case 5: fused_emit<5>(A, sg, local, part, SP, SM); break;
-      case 6: fused_emit<6>(A, sg, local, part, SP, SM); break;
-      case 7: fused_emit<7>(A, sg, local, part, SP, SM); break;
-      default: fused_emit<8>(A, sg, local, part, SP, SM); break;
+      case 5: fused_emit<5, HERM>(A, sg, local, part, SP, SM); break;
+      case 6: fused_emit<6, HERM>(A, sg, local, part, SP, SM); break;
+      case 7: fused_emit<7, HERM>(A, sg, local, part, SP, SM); break;
+      default: fused_emit<8, HERM>(A, sg, local, part, SP, SM); break;
     }
     __syncthreads();  // SP / SM and s_tk are rewritten by the next item
     item = next;
   }
 }
 
-// Workspace: [P/M segments: 2 * 2^n] (TRIDIAGONAL) + [x = 0 vector: 2^n] (world > 1: the
-// x = 0 intermediate when it does not fit the rank's output block) + [tail counters].
+// Workspace: [P/M segments: 2 * 2^n] (TRIDIAGONAL; S segments: 2^n for
+// HERMITIAN_TRIDIAGONAL) + [x = 0 vector: 2^n] (world > 1: the x = 0 intermediate when it
+// does not fit the rank's output block) + [tail counters].
 constexpr size_t kTailCtrBytes = 256;
+static size_t seg_ws_elems(int n, int structure) {
+  const size_t N = (size_t)1 << n;
+  return structure == 4 ? 2 * N : structure == 6 ? N : 0;
+}
 size_t band_workspace_bytes(int n, int structure, int world) {
   const size_t N = (size_t)1 << n;
-  size_t b = structure == 4 ? 2 * N * 16 : 0;
+  size_t b = seg_ws_elems(n, structure) * 16;
   if (world > 1 && n > 12) b += N * 16;
   return b + kTailCtrBytes;
 }
@@ -961,7 +1030,7 @@ cudaError_t launch_band(const double2* A, double2* out, int n, int structure, vo
   const int zshift = world > 1 ? n - g : 63;
   const u64 zrank = world > 1 ? (u64)rank : 0ull;
   double2* PM = reinterpret_cast<double2*>(ws);
-  double2* X0 = world > 1 ? PM + (structure == 4 ? 2 * N : 0) : nullptr;  // x = 0 scratch
+  double2* X0 = world > 1 ? PM + seg_ws_elems(n, structure) : nullptr;  // x = 0 scratch
   unsigned* tail_ctr = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(ws) + band_workspace_bytes(n, structure, world) -
                                                    kTailCtrBytes);
   // the x = 0 family after topk_pass_kernel: its two remaining passes as the L2-resident tail
@@ -1034,41 +1103,59 @@ cudaError_t launch_band(const double2* A, double2* out, int n, int structure, vo
     if (tail_ok(f)) return launch_tail(f, tail_ctr, st, nl);
     return run_families(&f, 1, st, nl);
   }
+  // TRIDIAGONAL: A = [sub | main | sup]; HERMITIAN_TRIDIAGONAL: A = [main | sup], the
+  // sub-diagonal conj(sup) implied (one WHT per segment, see herm_seg_view).
+  const bool herm = structure == 6;
+  const double2* mainv = herm ? A : A + N;
+  const double2* supv = herm ? A + N : A + 2 * N;
+  const u64 segmul = herm ? 1 : 2;  // P_t and M_t, or S_t
   // Block 0 (x = 0, WHT(main) scaled) first: its passes stream the main diagonal through L2,
-  // so running them before the split keeps the split's P/M output L2-resident for the
-  // segment passes that follow.
+  // so running them before the split keeps the split's output L2-resident for the segment
+  // passes that follow.
   WhtFamily fam[kMaxSeg];
   int nf = 0;
-  if ((e = x0_family(A + N, 0ull, fam[nf])) != cudaSuccess) return e;
+  if ((e = x0_family(mainv, 0ull, fam[nf])) != cudaSuccess) return e;
   if (tail_ok(fam[nf])) {
     if ((e = launch_tail(fam[nf], tail_ctr, st, nl)) != cudaSuccess) return e;
   } else {
     ++nf;
   }
-  // TRIDIAGONAL: A = [sub | main | sup].  Segments t with lam = n - t - 1 >= kTopMin: fused
-  // split + top levels (the rank's branches only); shorter ones: plain split, replicated.
+  // Segments t with lam = n - t - 1 >= kTopMin: fused split + top levels (the rank's branches
+  // only); shorter ones: plain split, replicated.
   const int lam_small = n - 1 < kTopMin - 1 ? n - 1 : kTopMin - 1;
   {
     u64 total = (2ull << lam_small) - 1ull;
     u64 blocks = (total + 255) / 256;
     if (blocks > (u64)sms * 32) blocks = (u64)sms * 32;
-    tri_split_small_kernel<<<(unsigned)blocks, 256, 0, st>>>(A, PM, n, lam_small);
+    if (herm) htri_split_small_kernel<<<(unsigned)blocks, 256, 0, st>>>(supv, PM, n, lam_small);
+    else tri_split_small_kernel<<<(unsigned)blocks, 256, 0, st>>>(A, PM, n, lam_small);
     *nl += 1;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   if (n - 1 >= kTopMin) {
     u64 blocks = ((N >> 3) + 255) / 256;
     if (blocks > (u64)sms * 16) blocks = (u64)sms * 16;
-    switch (k_keep) {
-      case 3: tri_split_top3_kernel<3><<<(unsigned)blocks, 256, 0, st>>>(A, PM, n, rsel); break;
-      case 2: tri_split_top3_kernel<2><<<(unsigned)blocks, 256, 0, st>>>(A, PM, n, rsel); break;
-      case 1: tri_split_top3_kernel<1><<<(unsigned)blocks, 256, 0, st>>>(A, PM, n, rsel); break;
-      default: tri_split_top3_kernel<0><<<(unsigned)blocks, 256, 0, st>>>(A, PM, n, rsel); break;
+    const unsigned b = (unsigned)blocks;
+    if (herm) {
+      switch (k_keep) {
+        case 3: htri_split_top3_kernel<3><<<b, 256, 0, st>>>(supv, PM, n, rsel); break;
+        case 2: htri_split_top3_kernel<2><<<b, 256, 0, st>>>(supv, PM, n, rsel); break;
+        case 1: htri_split_top3_kernel<1><<<b, 256, 0, st>>>(supv, PM, n, rsel); break;
+        default: htri_split_top3_kernel<0><<<b, 256, 0, st>>>(supv, PM, n, rsel); break;
+      }
+    } else {
+      switch (k_keep) {
+        case 3: tri_split_top3_kernel<3><<<b, 256, 0, st>>>(A, PM, n, rsel); break;
+        case 2: tri_split_top3_kernel<2><<<b, 256, 0, st>>>(A, PM, n, rsel); break;
+        case 1: tri_split_top3_kernel<1><<<b, 256, 0, st>>>(A, PM, n, rsel); break;
+        default: tri_split_top3_kernel<0><<<b, 256, 0, st>>>(A, PM, n, rsel); break;
+      }
     }
     *nl += 1;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  // blocks t+1: P_t / M_t.  Segments t < tf run their last pass inside the fused expansion.
+  // blocks t+1: P_t / M_t (or S_t).  Segments t < tf run their last pass inside the fused
+  // expansion.
   const int zs = world > 1 ? zshift : n;
   const u64 NL = 1ull << zs;
   FusedArgs FA{};
@@ -1078,7 +1165,7 @@ cudaError_t launch_band(const double2* A, double2* out, int n, int structure, vo
       const int lam = n - t - 1, lamp = lam - 3;
       if (lam < kTopMin || lamp < 13 || lamp > 20) break;
       FusedSeg& sg = FA.s[tf];
-      sg.P = PM + 2 * (N - (N >> t));
+      sg.P = PM + segmul * (N - (N >> t));
       sg.tiles = ((u64)1 << (lamp + k_keep)) / (u64)kTileElems;
       sg.lamp = lamp;
       sg.K = lamp - 8 < 8 ? lamp - 8 : 8;
@@ -1089,14 +1176,14 @@ cudaError_t launch_band(const double2* A, double2* out, int n, int structure, vo
   }
   for (int t = 0; t < n; ++t) {
     const int lam = n - t - 1;
-    const u64 seg = N - (N >> t);
+    double2* base = PM + segmul * (N - (N >> t));
     if (lam >= kTopMin) {
-      WhtFamily f{PM + 2 * seg, PM + 2 * seg, lam - 3, 2ull << k_keep, 1.0};  // P then M branches
+      WhtFamily f{base, base, lam - 3, segmul << k_keep, 1.0};  // [P then M] or S branches
       f.first_bit = 0;
       f.skip_last = t < tf ? 1 : 0;
       fam[nf++] = f;
     } else {
-      fam[nf++] = WhtFamily{PM + 2 * seg, PM + 2 * seg, lam, 2, 1.0};
+      fam[nf++] = WhtFamily{base, base, lam, segmul, 1.0};
     }
   }
   if ((e = run_families(fam, nf, st, nl)) != cudaSuccess) return e;
@@ -1116,11 +1203,13 @@ cudaError_t launch_band(const double2* A, double2* out, int n, int structure, vo
     B.scale = scale;
     B.ticket = tail_ctr + 63;
     if ((e = cudaMemsetAsync(B.ticket, 0, 4, st)) != cudaSuccess) return e;
-    if ((e = ensure_smem_attr(reinterpret_cast<const void*>(tri_fused_expand_kernel), kFusedSmem)) != cudaSuccess)
-      return e;
+    const void* kf = herm ? reinterpret_cast<const void*>(tri_fused_expand_kernel<true>)
+                          : reinterpret_cast<const void*>(tri_fused_expand_kernel<false>);
+    if ((e = ensure_smem_attr(kf, kFusedSmem)) != cudaSuccess) return e;
     u64 grid = (u64)sms;
     if (grid > first) grid = first;
-    tri_fused_expand_kernel<<<(unsigned)grid, kThreads, kFusedSmem, st>>>(B);
+    if (herm) tri_fused_expand_kernel<true><<<(unsigned)grid, kThreads, kFusedSmem, st>>>(B);
+    else tri_fused_expand_kernel<false><<<(unsigned)grid, kThreads, kFusedSmem, st>>>(B);
     *nl += 1;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
@@ -1129,10 +1218,12 @@ cudaError_t launch_band(const double2* A, double2* out, int n, int structure, vo
     if (NL >= 256) {
       u64 blocks = (total / 8 + 255) / 256;
       if (blocks > (u64)sms * 16) blocks = (u64)sms * 16;
-      tridiag_expand_kernel<<<(unsigned)blocks, 256, 0, st>>>(PM, out, n, scale, zs, zrank, k_keep, tf);
+      if (herm) tridiag_expand_kernel<true><<<(unsigned)blocks, 256, 0, st>>>(PM, out, n, scale, zs, zrank, k_keep, tf);
+      else tridiag_expand_kernel<false><<<(unsigned)blocks, 256, 0, st>>>(PM, out, n, scale, zs, zrank, k_keep, tf);
     } else {
-      tridiag_expand_small_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(PM, out, n, scale, zs,
-                                                                                 zrank, k_keep);
+      const unsigned b = (unsigned)((total + 255) / 256);
+      if (herm) tridiag_expand_small_kernel<true><<<b, 256, 0, st>>>(PM, out, n, scale, zs, zrank, k_keep);
+      else tridiag_expand_small_kernel<false><<<b, 256, 0, st>>>(PM, out, n, scale, zs, zrank, k_keep);
     }
     *nl += 1;
     e = cudaGetLastError();

@@ -100,6 +100,13 @@ __global__ void __launch_bounds__(256) gen_band_kernel(int n, u64 seed, int vari
     }
     const double2 m = make_double2(gauss_pair(seed, i, 1u).x, 0.0);
     const double2 up = (i + 1 < N) ? make_double2(gauss_pair(seed, i, 2u).x, 0.0) : make_double2(0.0, 0.0);
+    if (variant == 6) {
+      // HERMITIAN_TRIDIAGONAL storage [main | sup] of the same matrix (sub = conj(sup) implied)
+      band[i] = m;
+      band[N + i] = up;
+      acc += abs2(m) + 2.0 * abs2(up);
+      continue;
+    }
     const double2 lo = (i > 0) ? make_double2(gauss_pair(seed, i - 1, 2u).x, 0.0) : make_double2(0.0, 0.0);
     band[N + i] = m;
     band[2 * N + i] = up;

@@ -5,6 +5,7 @@ import ctypes
 import os
 import re
 
+import numpy as np
 import pytest
 
 import paper_2403_11644_b200 as ptdr
@@ -46,6 +47,13 @@ def test_counts(L):
     assert ptdr.input_count(24, "diagonal") == 1 << 24
     assert ptdr.input_count(24, "tridiagonal") == 3 << 24
     assert ptdr.output_count(24, "tridiagonal") == 25 << 24
+    # HERMITIAN_TRIDIAGONAL: [main, sup] in, the same n + 1 blocks out, half the segment storage
+    assert ptdr.input_count(24, "hermitian_tridiagonal") == 2 << 24
+    assert ptdr.output_count(24, "hermitian_tridiagonal") == 25 << 24
+    assert ptdr.workspace_bytes(24, "hermitian_tridiagonal") == (1 << 24) * 16 + 256
+    assert ptdr.n_of(np.zeros((2, 1 << 5), dtype=np.complex128), "hermitian_tridiagonal") == 5
+    with pytest.raises(ValueError):
+        ptdr.n_of(np.zeros((3, 1 << 5), dtype=np.complex128), "hermitian_tridiagonal")
     assert ptdr.output_count(0) == 0 and ptdr.output_count(17) == 0
     assert L.ptdr_max_n(0) == 16 and L.ptdr_max_n(4) == 28
 

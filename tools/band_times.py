@@ -15,9 +15,9 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from tools_bench_configs import PEAK, time_it  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 24
-for structure in ("diagonal", "anti_diagonal", "tridiagonal"):
+for structure in ("diagonal", "anti_diagonal", "tridiagonal", "hermitian_tridiagonal"):
     B = ptdr.generate_band(n, 3, "diagonal" if structure == "anti_diagonal" else structure)
-    blocks = n + 1 if structure == "tridiagonal" else 1
+    blocks = n + 1 if "tridiagonal" in structure else 1
     for world in (1, 2, 4, 8):
         NL = (1 << n) // world
         outl = torch.empty(blocks * NL, dtype=torch.complex128, device="cuda")

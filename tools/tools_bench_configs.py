@@ -102,7 +102,7 @@ def band(name, n, seed, variant):
     import ptdr_inputs
     from paper_2403_11644_b200 import q_of
 
-    if variant == "tridiagonal":
+    if variant in ("tridiagonal", "hermitian_tridiagonal"):
         sub, main, sup = ptdr_inputs.band(n, seed, "tridiagonal")
 
         def orc_fn(idx):
@@ -303,6 +303,7 @@ if __name__ == "__main__":
     if "all" in which or "band" in which:
         band("n24tri", 24, 3, "tridiagonal")
         band("n24diag", 24, 3, "diagonal")
+        band("n24tri_hermitian", 24, 3, "hermitian_tridiagonal")
     if "all" in which or "next" in which:
         anti("n24anti", 24)
         band_s("n24band_s2", 24, 2)

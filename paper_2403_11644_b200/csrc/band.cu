@@ -26,7 +26,11 @@ namespace ptdr {
 
 // Vectors of at least 2^kTopMin elements run their three top butterfly levels first (the
 // z-sharded paths read them once and transform only the rank's part; see topk_pass_kernel).
-constexpr int kTopMin = 15;
+// Tridiagonal segments from 2^13 on (their split is per element, and 2^10-2^11-element
+// branches are whole-vector tiles: one pass); the x = 0 vector from 2^15 on (a
+// topk_pass_kernel tile needs 4096 / 2^KK <= 2^(n - TB) consecutive elements per branch).
+constexpr int kTopMin = 13;
+constexpr int kTopMinX0 = 15;
 
 // ---- flat WHT pass over bits [b0, b0+K) of a contiguous array ---------------------
 template <int K>
@@ -842,7 +846,7 @@ static cudaError_t launch_tail(const WhtFamily& f, unsigned* ctr, cudaStream_t s
 // expansion (a tile's output, 2^(t+1) x 64 KiB, would unbalance the grid).  One CTA per SM
 // (two 64 KiB transform buffers); the next tile's 32 loads per thread are issued before the
 // current tile's output loop, so load latency hides behind the stores.
-constexpr int kFuseMaxT = 3;
+constexpr int kFuseMaxT = 7;
 struct FusedSeg {
   const double2* P;  // P_t branches (KS x 2^lamp), M_t follows at P + KS 2^lamp
   u64 tiles;         // KS 2^lamp / 4096
@@ -1045,7 +1049,7 @@ cudaError_t launch_band(const double2* A, double2* out, int n, int structure, vo
   // The x = 0 family (diagonal, anti-diagonal, tridiagonal main diagonal): vector `src`,
   // output block 0 of `out` (2^n / world elements), px = X-mask phase.
   auto x0_family = [&](const double2* src, u64 px, WhtFamily& f) -> cudaError_t {
-    if (n >= kTopMin) {
+    if (n >= kTopMinX0) {
       // top levels + bits 0-7 in one pass into the rank's kept branches (the top 4 bits from
       // n = 16 on: 16 branches of 2^(n-4), short enough for the L2-resident tail; 3 at
       // n = 15), then bits 8.. of the branches; ranks beyond the top TB bits filter their

@@ -614,6 +614,35 @@ static cudaError_t launch_topk(const double2* in, double2* out, int lam, unsigne
   return cudaGetLastError();
 }
 
+// Split of the short segments (lam < kTopMin, replicated on every rank): element id =
+// 2^lam - 1 + h of segment lam (t = n - 1 - lam); TRIDIAGONAL stores full P_t (2^lam) then
+// M_t (2^lam), HERMITIAN_TRIDIAGONAL S_t.  Run by the tail loop of the split kernels below
+// (and alone when no segment is long).
+__device__ __forceinline__ void split_small_one(const double2* __restrict__ band, double2* PM, int n, u64 id,
+                                                bool herm) {
+  const u64 N = 1ull << n;
+  const int lam = 63 - __clzll((long long)(id + 1));
+  const u64 h = id + 1 - (1ull << lam);
+  const int t = n - 1 - lam;
+  const u64 i = (h << (t + 1)) + (1ull << t) - 1ull;
+  const u64 seg = N - (N >> t);
+  if (herm) {
+    PM[seg + h] = ld_stream(band + N + i);  // [main | sup]
+    return;
+  }
+  const double2 sv = ld_stream(band + 2 * N + i), uv = ld_stream(band + i + 1);
+  PM[2 * seg + h] = cadd(sv, uv);
+  PM[2 * seg + (1ull << lam) + h] = csub(sv, uv);
+}
+__device__ __forceinline__ void split_small_loop(const double2* band, double2* PM, int n, int lam_max, bool herm) {
+  const u64 total = (2ull << lam_max) - 1ull;  // lam = 0 .. lam_max
+  for (u64 id = (u64)blockIdx.x * blockDim.x + threadIdx.x; id < total; id += (u64)gridDim.x * blockDim.x)
+    split_small_one(band, PM, n, id, herm);
+}
+__global__ void split_small_kernel(const double2* __restrict__ band, double2* PM, int n, int lam_max, int herm) {
+  split_small_loop(band, PM, n, lam_max, herm != 0);
+}
+
 // Tridiagonal split of the long segments (lam = n - t - 1 >= kTopMin) fused with their top
 // levels: for i = h 2^(n-3) + i_low with t trailing ones (t < n - 3, the same for all eight
 // top blocks h), S_t[.] = sup[i] and U_t[.] = sub[i + 1] sit at segment index
@@ -622,7 +651,7 @@ static cudaError_t launch_topk(const double2* in, double2* out, int lam, unsigne
 // segment: P_t at PM + 2 seg, KS branches of 2^(lam-3) (kt major), M_t right after.
 template <int KK>
 __global__ void __launch_bounds__(256) tri_split_top3_kernel(const double2* __restrict__ band, double2* PM, int n,
-                                                             unsigned rsel) {
+                                                             unsigned rsel, int lam_small) {
   const u64 N = 1ull << n;
   const u64 Q = N >> 3;
   const double2* sub = band;
@@ -654,12 +683,14 @@ __global__ void __launch_bounds__(256) tri_split_top3_kernel(const double2* __re
       st_l2(Mt + ((u64)kt << Lb) + hl, oM[kt]);
     }
   }
+  split_small_loop(band, PM, n, lam_small, false);
 }
 
 // HERMITIAN_TRIDIAGONAL split: S_t only (sup; the sub-diagonal is conj(sup) and not stored).
 template <int KK>
-__global__ void __launch_bounds__(256) htri_split_top3_kernel(const double2* __restrict__ sup, double2* W, int n,
-                                                              unsigned rsel) {
+__global__ void __launch_bounds__(256) htri_split_top3_kernel(const double2* __restrict__ band, double2* W, int n,
+                                                              unsigned rsel, int lam_small) {
+  const double2* sup = band + (1ull << n);
   const u64 N = 1ull << n;
   const u64 Q = N >> 3;
   constexpr int KS = 1 << KK;
@@ -679,36 +710,7 @@ __global__ void __launch_bounds__(256) htri_split_top3_kernel(const double2* __r
 #pragma unroll
     for (int kt = 0; kt < KS; ++kt) st_l2(St + ((u64)kt << Lb) + hl, o[kt]);
   }
-}
-__global__ void htri_split_small_kernel(const double2* __restrict__ sup, double2* W, int n, int lam_max) {
-  const u64 N = 1ull << n;
-  const u64 total = (2ull << lam_max) - 1ull;
-  for (u64 id = (u64)blockIdx.x * blockDim.x + threadIdx.x; id < total; id += (u64)gridDim.x * blockDim.x) {
-    const int lam = 63 - __clzll((long long)(id + 1));
-    const u64 h = id + 1 - (1ull << lam);
-    const int t = n - 1 - lam;
-    const u64 i = (h << (t + 1)) + (1ull << t) - 1ull;
-    W[(N - (N >> t)) + h] = ld_stream(sup + i);
-  }
-}
-
-// Split of the short segments (lam < kTopMin, replicated on every rank): one thread per
-// (lam, h), id = 2^lam - 1 + h; full P_t (2^lam) then M_t (2^lam).
-__global__ void tri_split_small_kernel(const double2* __restrict__ band, double2* PM, int n, int lam_max) {
-  const u64 N = 1ull << n;
-  const double2* sub = band;
-  const double2* sup = band + 2 * N;
-  const u64 total = (2ull << lam_max) - 1ull;  // lam = 0 .. lam_max
-  for (u64 id = (u64)blockIdx.x * blockDim.x + threadIdx.x; id < total; id += (u64)gridDim.x * blockDim.x) {
-    const int lam = 63 - __clzll((long long)(id + 1));
-    const u64 h = id + 1 - (1ull << lam);
-    const int t = n - 1 - lam;
-    const u64 i = (h << (t + 1)) + (1ull << t) - 1ull;
-    const double2 sv = ld_stream(sup + i), uv = ld_stream(sub + i + 1);
-    const u64 seg = N - (N >> t);
-    PM[2 * seg + h] = cadd(sv, uv);
-    PM[2 * seg + (1ull << lam) + h] = csub(sv, uv);
-  }
+  split_small_loop(band, W, n, lam_small, true);
 }
 
 // ---- L2-resident tail of a long vector family (top-bits-first x = 0 vectors) ------------
@@ -1111,7 +1113,6 @@ cudaError_t launch_band(const double2* A, double2* out, int n, int structure, vo
   // sub-diagonal conj(sup) implied (one WHT per segment, see herm_seg_view).
   const bool herm = structure == 6;
   const double2* mainv = herm ? A : A + N;
-  const double2* supv = herm ? A + N : A + 2 * N;
   const u64 segmul = herm ? 1 : 2;  // P_t and M_t, or S_t
   // Block 0 (x = 0, WHT(main) scaled) first: its passes stream the main diagonal through L2,
   // so running them before the split keeps the split's output L2-resident for the segment
@@ -1127,37 +1128,34 @@ cudaError_t launch_band(const double2* A, double2* out, int n, int structure, vo
   // Segments t with lam = n - t - 1 >= kTopMin: fused split + top levels (the rank's branches
   // only); shorter ones: plain split, replicated.
   const int lam_small = n - 1 < kTopMin - 1 ? n - 1 : kTopMin - 1;
-  {
-    u64 total = (2ull << lam_small) - 1ull;
-    u64 blocks = (total + 255) / 256;
-    if (blocks > (u64)sms * 32) blocks = (u64)sms * 32;
-    if (herm) htri_split_small_kernel<<<(unsigned)blocks, 256, 0, st>>>(supv, PM, n, lam_small);
-    else tri_split_small_kernel<<<(unsigned)blocks, 256, 0, st>>>(A, PM, n, lam_small);
-    *nl += 1;
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  }
   if (n - 1 >= kTopMin) {
+    // long segments + (tail loop) the short ones, one launch
     u64 blocks = ((N >> 3) + 255) / 256;
     if (blocks > (u64)sms * 16) blocks = (u64)sms * 16;
     const unsigned b = (unsigned)blocks;
     if (herm) {
       switch (k_keep) {
-        case 3: htri_split_top3_kernel<3><<<b, 256, 0, st>>>(supv, PM, n, rsel); break;
-        case 2: htri_split_top3_kernel<2><<<b, 256, 0, st>>>(supv, PM, n, rsel); break;
-        case 1: htri_split_top3_kernel<1><<<b, 256, 0, st>>>(supv, PM, n, rsel); break;
-        default: htri_split_top3_kernel<0><<<b, 256, 0, st>>>(supv, PM, n, rsel); break;
+        case 3: htri_split_top3_kernel<3><<<b, 256, 0, st>>>(A, PM, n, rsel, lam_small); break;
+        case 2: htri_split_top3_kernel<2><<<b, 256, 0, st>>>(A, PM, n, rsel, lam_small); break;
+        case 1: htri_split_top3_kernel<1><<<b, 256, 0, st>>>(A, PM, n, rsel, lam_small); break;
+        default: htri_split_top3_kernel<0><<<b, 256, 0, st>>>(A, PM, n, rsel, lam_small); break;
       }
     } else {
       switch (k_keep) {
-        case 3: tri_split_top3_kernel<3><<<b, 256, 0, st>>>(A, PM, n, rsel); break;
-        case 2: tri_split_top3_kernel<2><<<b, 256, 0, st>>>(A, PM, n, rsel); break;
-        case 1: tri_split_top3_kernel<1><<<b, 256, 0, st>>>(A, PM, n, rsel); break;
-        default: tri_split_top3_kernel<0><<<b, 256, 0, st>>>(A, PM, n, rsel); break;
+        case 3: tri_split_top3_kernel<3><<<b, 256, 0, st>>>(A, PM, n, rsel, lam_small); break;
+        case 2: tri_split_top3_kernel<2><<<b, 256, 0, st>>>(A, PM, n, rsel, lam_small); break;
+        case 1: tri_split_top3_kernel<1><<<b, 256, 0, st>>>(A, PM, n, rsel, lam_small); break;
+        default: tri_split_top3_kernel<0><<<b, 256, 0, st>>>(A, PM, n, rsel, lam_small); break;
       }
     }
-    *nl += 1;
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  } else {
+    u64 total = (2ull << lam_small) - 1ull;
+    u64 blocks = (total + 255) / 256;
+    if (blocks > (u64)sms * 32) blocks = (u64)sms * 32;
+    split_small_kernel<<<(unsigned)blocks, 256, 0, st>>>(A, PM, n, lam_small, herm ? 1 : 0);
   }
+  *nl += 1;
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
   // blocks t+1: P_t / M_t (or S_t).  Segments t < tf run their last pass inside the fused
   // expansion.
   const int zs = world > 1 ? zshift : n;

@@ -753,16 +753,18 @@ __device__ __forceinline__ void decode_tail(u64 t, u64 TP, u64 C, u64 look, int&
 __global__ void __launch_bounds__(kThreads, 2) tail_pipe_kernel(const __grid_constant__ TailArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* S = reinterpret_cast<double2*>(smem_raw);
-  __shared__ unsigned long long s_tk;
   const u64 TP = (1ull << A.L) / (u64)kTileElems;  // tiles per pass per branch
   const u64 total = 2ull * (u64)A.nvec * TP;
   unsigned* doneP1 = A.ctr + 1;
-  for (;;) {
-    __syncthreads();
-    if (threadIdx.x == 0) s_tk = atomicAdd(A.ctr, 1u);
-    __syncthreads();
-    const u64 tk = s_tk;
-    if (tk >= total) break;
+  // The next ticket is claimed while the current tile runs (its atomic's latency is hidden).
+  // Tickets still rise per CTA and a tile only waits for smaller tickets, so the smallest
+  // unfinished ticket is always some CTA's current tile: progress is guaranteed.
+  __shared__ unsigned long long s_next[2];
+  if (threadIdx.x == 0) s_next[0] = atomicAdd(A.ctr, 1u);
+  __syncthreads();
+  u64 tk = s_next[0];
+  for (int par = 0; tk < total; par ^= 1) {
+    if (threadIdx.x == 0) s_next[par ^ 1] = atomicAdd(A.ctr, 1u);
     int phase;
     u64 v, tile;
     decode_tail(tk, TP, (u64)A.nvec, (u64)A.look, phase, v, tile);
@@ -802,6 +804,8 @@ __global__ void __launch_bounds__(kThreads, 2) tail_pipe_kernel(const __grid_con
         default: flat_tile<8>(S, sp, v * TP + tile); break;
       }
     }
+    __syncthreads();  // S is reused by the next tile; s_next[par ^ 1] is visible
+    tk = s_next[par ^ 1];
   }
 }
 

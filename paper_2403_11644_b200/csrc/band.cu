@@ -1419,6 +1419,86 @@ __global__ void band_gather_diag_kernel(const double2* diags, int n, int s, cons
   }
 }
 
+// Gather with the top three butterfly levels first (n >= kTopMin + 1): thread (d, il) reads the
+// eight rows i_h = h 2^(n-3) + il of diagonal d (coalesced along il).  When il + d stays inside
+// [0, 2^(n-3)) the eight elements share x = il ^ (il + d) and l, and sit at segment indices
+// h 2^(lam-3) + (il >> (t+1)): for a long segment (lam >= kTopMin) they are combined by the
+// top three levels of its WHT right here (topk_kept, as the tridiagonal split) and stored as
+// eight branches of 2^(lam-3) -- the branch-major result of the remaining passes is the natural
+// output order, so the expansion is unchanged -- and a long family needs one pass less (n = 24,
+// s = 2: two passes instead of three).  Short segments and boundary rows are scattered as
+// band_gather_diag_kernel does.
+__device__ __forceinline__ const BandSegRef* band_find_ref(const BandBlockDev& B, const BandSegRef* refs, u64 l) {
+  for (int k = 0; k < B.nL; ++k)
+    if (refs[B.first + k].l == l) return &refs[B.first + k];
+  return nullptr;
+}
+__global__ void __launch_bounds__(256) band_gather_top3_kernel(const double2* diags, int n, int s,
+                                                               const BandBlockDev* blocks, const BandSegRef* refs,
+                                                               const int* xblock, double2* segs) {
+  const u64 N = 1ull << n;
+  const u64 Q = N >> 3;
+  const u64 Q4 = N >> 4;
+  // ids [0, 2s Q): the off-diagonals (d = -s..-1, 1..s); [2s Q, 2s Q + Q4): the main diagonal
+  // (x = 0: one segment of 2^n, its top FOUR levels here -> 16 branches of 2^(n-4), so it
+  // needs two passes like the rest)
+  const u64 total = (u64)(2 * s) * Q + Q4;
+  for (u64 id = (u64)blockIdx.x * blockDim.x + threadIdx.x; id < total; id += (u64)gridDim.x * blockDim.x) {
+    if (id >= (u64)(2 * s) * Q) {
+      const u64 il = id - (u64)(2 * s) * Q;
+      const double2* D = diags + (u64)s * N;
+      double2 w[16];
+#pragma unroll
+      for (int h = 0; h < 16; ++h) w[h] = ld_stream(D + (u64)h * Q4 + il);
+      const BandSegRef r = refs[blocks[0].first];
+      double2 o[16];
+      topk_kept<4, 4>(w, 0u, o);
+#pragma unroll
+      for (int kt = 0; kt < 16; ++kt) segs[r.off + ((u64)kt << (n - 4)) + il] = o[kt];
+      continue;
+    }
+    const int di = (int)(id / Q);
+    const int d = di < s ? di - s : di - s + 1;
+    const u64 il = id - (u64)di * Q;
+    const double2* D = diags + (u64)(d + s) * N;
+    double2 v[8];
+#pragma unroll
+    for (int h = 0; h < 8; ++h) v[h] = ld_stream(D + (u64)h * Q + il);
+    const long long jl = (long long)il + d;
+    if (jl >= 0 && jl < (long long)Q) {
+      const u64 x = il ^ (u64)jl;
+      const int t = 63 - __clzll(x);
+      const int lam = n - t - 1;
+      if (lam >= kTopMin) {
+        const u64 e = ((2ull << t) - 1ull) - x;
+        const BandBlockDev B = blocks[xblock[t * s + (int)e]];
+        const BandSegRef* r = band_find_ref(B, refs, il & ((2ull << t) - 1ull));
+        if (r) {
+          double2 o[8];
+          topk_kept<3, 3>(v, 0u, o);
+          const u64 hl = il >> (t + 1);
+#pragma unroll
+          for (int kt = 0; kt < 8; ++kt) segs[r->off + ((u64)kt << (lam - 3)) + hl] = o[kt];
+        }
+        continue;
+      }
+    }
+    // short segments / rows whose + d crosses a top-block boundary: one element each
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+      const u64 i = (u64)h * Q + il;
+      const long long j = (long long)i + d;
+      if (j < 0 || j >= (long long)N) continue;
+      const u64 x = i ^ (u64)j;
+      const int t = 63 - __clzll(x);
+      const u64 e = ((2ull << t) - 1ull) - x;
+      const BandBlockDev B = blocks[xblock[t * s + (int)e]];
+      const BandSegRef* r = band_find_ref(B, refs, i & ((2ull << t) - 1ull));
+      if (r) segs[r->off + (i >> (t + 1))] = v[h];
+    }
+  }
+}
+
 // One segment's contribution to a lane's 8 outputs z = z0 + 32 j (z0 = base + lane, base a
 // multiple of 256, so bits 5-7 of z0 are zero).  Wg = W + (base >> SH): the sample of output z
 // is Wg[(lane + 32 j) >> SH], which for SH >= 5 does not depend on the lane, so only 256 >> SH
@@ -1682,7 +1762,15 @@ cudaError_t launch_band_s(const double2* diags, int n, int s, double2* out, void
   e = cudaMemcpyAsync(base, T->pinned, p.table_bytes, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return e;
   const int sms = device_sm_count();
-  if (s >= 1) {
+  const bool top3 = s >= 1 && n - 1 >= kTopMin;
+  if (top3) {
+    const u64 total = ((u64)(2 * s) << (n - 3)) + (1ull << (n - 4));
+    u64 g = (total + 255) / 256;
+    if (g > (u64)sms * 16) g = (u64)sms * 16;
+    band_gather_top3_kernel<<<(unsigned)g, 256, 0, st>>>(diags, n, s, dblocks, drefs, dxb, segs);
+    *nl += 1;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  } else if (s >= 1) {
     const u64 total = (u64)(2 * s + 1) << n;
     u64 g = (total + 255) / 256;
     if (g > (u64)sms * 16) g = (u64)sms * 16;
@@ -1697,8 +1785,13 @@ cudaError_t launch_band_s(const double2* diags, int n, int s, double2* out, void
   }
   // WHT of every segment, in place (one family per length)
   std::vector<WhtFamily> fam;
-  for (size_t f = 0; f < p.fam_lam.size(); ++f)
-    fam.push_back(WhtFamily{segs + p.fam_off[f], segs + p.fam_off[f], p.fam_lam[f], (u64)p.fam_count[f], 1.0});
+  for (size_t f = 0; f < p.fam_lam.size(); ++f) {
+    // long segments after the top-levels gather: 8 branches of 2^(lam-3) each (x = 0, the only
+    // segment of 2^n elements: 16 branches of 2^(n-4))
+    const int tb = !(top3 && p.fam_lam[f] >= kTopMin) ? 0 : p.fam_lam[f] == n ? 4 : 3;
+    fam.push_back(WhtFamily{segs + p.fam_off[f], segs + p.fam_off[f], p.fam_lam[f] - tb,
+                            (u64)p.fam_count[f] << tb, 1.0});
+  }
   for (size_t f0 = 0; f0 < fam.size(); f0 += kMaxSeg) {
     const int cnt = (int)(fam.size() - f0 < (size_t)kMaxSeg ? fam.size() - f0 : kMaxSeg);
     if ((e = run_families(fam.data() + f0, cnt, st, nl)) != cudaSuccess) return e;

@@ -542,10 +542,12 @@ def main_multi(a):
     if rank == 0:
         roof = combined_roofline(n, world, ms_per_step, peak, busbw) if busbw else None
         kernel_gbs = 32 * coeffs_rank / (kernel_ms * 1e-3) / 1e9
-        if roof is None:   # peer pull: the NVLink transfer is inside the kernel
+        if roof is None:   # peer pull (the NVLink transfer is inside the kernel), or world 1
+            note = ("fused peer-pull: exchange inside the kernel; HBM-only roofline" if world > 1 else
+                    "world 1: the all-to-all moves no inter-GPU bytes (a local copy); HBM-only roofline")
             roof = {"bound": "hbm", "unit": "GB/s", "achieved": 32 * coeffs_rank / (ms_per_step * 1e-3) / 1e9,
                     "peak": peak, "frac": 32 * coeffs_rank / (ms_per_step * 1e-3) / 1e9 / peak,
-                    "note": "fused peer-pull: exchange inside the kernel; HBM-only roofline"}
+                    "note": note}
         roof.update({"peak_kind": peak_kind, "traffic": None,
                      "kernel": "dense_pipe_kernel (per-rank shard)", "kernel_ms": kernel_ms,
                      "kernel_hbm_gbs": kernel_gbs, "kernel_hbm_frac": kernel_gbs / peak})

@@ -326,6 +326,8 @@ def main_single(a):
                      "peak_kind": peak_kind, "kernel": "dense_pipe_kernel",
                      "kernel_ms": kmean, "algorithmic_bytes_per_launch": alg_bytes,
                      "hbm_passes": 1, "l2_round_trips": 1,
+                     # also against the ~8 TB/s nominal HBM3e figure
+                     "frac_nominal_8000gbs": achieved / 8000.0,
                      "note": "32 B/coefficient (16 B read of A + 16 B write); the partial "
                              "transforms make one round trip through an L2-resident scratch "
                              "(DESIGN.md section 7)"},

@@ -469,11 +469,14 @@ __global__ void __launch_bounds__(PipeCfg<LT, XB, GW, NG, NS, NR>::THREADS, 1)
           // box are W^2 consecutive q (the low 2 XB bits of q): one TMA box of W^2 / 8 rows of
           // the [4^n / 8][8] view, 128-byte swizzled (launch_dense_pipe)
           mbar_arrive_expect_tx(fullk, (uint32_t)Cfg::TB);
+          // zh = (tlX << (R - XB)) + rb: spread() is linear over XOR and the low R - XB bits of
+          // zh are rb, so the producer spreads once per tile and adds a constant per box
           const uint32_t xh = ((uint32_t)a.x_base + (gch << XB)) >> XB;
+          const uint32_t zh0 = tlX << (R - XB);
+          const uint64_t b0 = spread_bits((uint64_t)(xh ^ zh0)) | (spread_bits((uint64_t)zh0) << 1);
 #pragma unroll
           for (int rb = 0; rb < (1 << (R - XB)); ++rb) {
-            const uint32_t zh = ((tlX << R) + (uint32_t)rb * W) >> XB;
-            const uint64_t qb = (spread_bits((uint64_t)(xh ^ zh)) | (spread_bits((uint64_t)zh) << 1)) << (2 * XB);
+            const uint64_t qb = (b0 ^ (3ull * spread_bits((uint64_t)rb))) << (2 * XB);
             tma_load_2d(dst + rb * W * W, &maps.m[0], 0, (int)(qb >> 3), fullk, pol);
           }
         } else if (phX == 0) {

@@ -108,12 +108,12 @@ def test_dense_guarded(gpu, n, variant):
     _same(out, want)
 
 
-@pytest.mark.parametrize("structure", ["diagonal", "tridiagonal", "anti_diagonal"])
-@pytest.mark.parametrize("n", [1, 2, 4, 8, 9, 12, 17])
+@pytest.mark.parametrize("structure", ["diagonal", "tridiagonal", "anti_diagonal", "hermitian_tridiagonal"])
+@pytest.mark.parametrize("n", [1, 2, 4, 8, 9, 12, 14, 17])
 def test_band_structures_guarded(gpu, structure, n):
     torch = _torch()
     N = 1 << n
-    rows = 3 if structure == "tridiagonal" else 1
+    rows = {"tridiagonal": 3, "hermitian_tridiagonal": 2}.get(structure, 1)
     rng = np.random.default_rng(n)
     b0 = torch.from_numpy(rng.standard_normal((rows, N)) + 1j * rng.standard_normal((rows, N))).cuda()
     if rows == 1:
@@ -265,6 +265,28 @@ def test_reconstruct_guarded(gpu, n):
     ptdr.reconstruct(c, out=out, workspace=ws)
     ar.check()
     _same(out, want)
+
+
+@pytest.mark.parametrize("n", [3, 8, 11, 12])
+def test_reconstruct_matrix_layout_guarded(gpu, n):
+    """The inverse from the matrix layout (MODE_INV pipeline from n = 11), out of place and in
+    place, writes nothing outside its buffers."""
+    N = 1 << n
+    M0 = ptdr.decompose_matrix_layout(ptdr.generate_dense(n, 3, "general"))
+    want = ptdr.reconstruct_matrix_layout(M0)
+    ar = Arena()
+    M = ar.c128(N * N, M0).view(N, N)
+    out = ar.c128(N * N).view(N, N)
+    ws = ar.ws(ptdr.lib().ptdr_reconstruct_matrix_layout_workspace_bytes(n))
+    ptdr.reconstruct_matrix_layout(M, out=out, workspace=ws)
+    ar.check()
+    _same(out, want)
+    ar = Arena()
+    M = ar.c128(N * N, M0).view(N, N)
+    ws = ar.ws(ptdr.lib().ptdr_reconstruct_matrix_layout_workspace_bytes(n))
+    ptdr.reconstruct_matrix_layout(M, workspace=ws, inplace=True)
+    ar.check()
+    _same(M, want)
 
 
 def test_algebra_guarded(gpu):

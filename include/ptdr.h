@@ -14,12 +14,9 @@
  * Memory: every pointer argument is a DEVICE pointer (cudaMalloc / torch CUDA
  * tensor memory) unless the function name ends in _host.  The caller owns all
  * memory; the library keeps no global mutable state except a thread-local error
- * string and a per-device cache of launch parameters (SM count, the SM -> die map of the
- * dense pipeline, band(s) index tables in pinned host memory), allocates no persistent
- * device memory, and is reentrant given distinct workspaces.  The first dense call on a
- * device with n >= 11 runs a one-time probe (~1 ms, its own stream and temporary
- * buffers) that maps SMs to the B200's two dies; it is skipped while the caller's stream
- * is being captured into a CUDA graph (that call then runs without the die split).  Element type: ptdr_c128 =
+ * string and a per-device cache of launch parameters (SM count, band(s) index tables in
+ * pinned host memory), allocates no persistent device memory, and is reentrant given
+ * distinct workspaces.  Element type: ptdr_c128 =
  * interleaved (re, im) binary64 (== cuDoubleComplex == torch.complex128), 16-byte
  * aligned.  Streams are passed as `void*` holding a cudaStream_t (NULL = legacy
  * default stream).

@@ -57,8 +57,6 @@ struct DenseArgs {
   double scale;        // 2^-n
   int layout_mat;      // output layout: 0 = q order at q_offset(x, z, gshift); 1 = matrix
                        //   layout out[z 2^n + (z ^ x)] (the in-place decomposition)
-  // die-aware pipeline (dense_pipe.cuh): bit s of die_mask = die of SM s; die 0 runs chunks
-  // [0, die_chunks0), die 1 the rest, each with its own ticket counter and half the slots
   int max_ctas;        // pipeline grid cap (0: one CTA per SM)
   int acq_fence;       // pipeline dependency waits: 2 ld.acquire.gpu (default); developer
                        //   variants 0 relaxed read, 1 relaxed + fence.acq_rel.gpu

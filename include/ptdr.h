@@ -90,21 +90,22 @@ typedef enum {
   PTDR_ECUDA = 4
 } ptdr_status;
 
-/* Supported n: dense structures 1 <= n <= 16; DIAGONAL / TRIDIAGONAL / ANTI_DIAGONAL
- * 1 <= n <= 28. */
+/* Supported n: dense structures 1 <= n <= 16; DIAGONAL / TRIDIAGONAL / ANTI_DIAGONAL /
+ * HERMITIAN_TRIDIAGONAL 1 <= n <= 28. */
 int ptdr_max_n(int structure);
 
 /* Number of ptdr_c128 elements of the input A: 4^n (dense), 2^n (DIAGONAL,
- * ANTI_DIAGONAL), 3*2^n (TRIDIAGONAL).  0 if (n, structure) is invalid. */
+ * ANTI_DIAGONAL), 3*2^n (TRIDIAGONAL), 2*2^n (HERMITIAN_TRIDIAGONAL).  0 if (n, structure)
+ * is invalid. */
 size_t ptdr_input_count(int n, int structure);
 
 /* Number of ptdr_c128 output coefficients: 4^n, 2^n (DIAGONAL, ANTI_DIAGONAL),
- * (n+1)*2^n (TRIDIAGONAL).  0 if invalid. */
+ * (n+1)*2^n (TRIDIAGONAL, HERMITIAN_TRIDIAGONAL).  0 if invalid. */
 size_t ptdr_output_count(int n, int structure);
 
 /* Device workspace bytes needed by ptdr_decompose_async for (n, structure) on one
  * GPU (world = 1), or per rank of ptdr_decompose_xshard_async (GENERAL, world > 1) or
- * ptdr_decompose_zshard_async (DIAGONAL / TRIDIAGONAL, world > 1).
+ * ptdr_decompose_zshard_async (the band structures, world > 1).
  * Deterministic in its arguments.  (size_t)-1 if invalid. */
 size_t ptdr_workspace_bytes(int n, int structure, int world);
 
@@ -233,7 +234,8 @@ ptdr_status ptdr_ipc_get_handle(const void* dev_ptr, void* handle, uint64_t* off
 ptdr_status ptdr_ipc_open(const void* handle, void** dev_ptr);
 ptdr_status ptdr_ipc_close(void* dev_ptr);
 
-/* Multi-GPU, per rank, DIAGONAL / TRIDIAGONAL (replicated band,
+/* Multi-GPU, per rank, the band structures DIAGONAL / TRIDIAGONAL / ANTI_DIAGONAL /
+ * HERMITIAN_TRIDIAGONAL (replicated band,
  * z-sharded output, no communication).  Every rank holds the whole band (input layout as
  * for ptdr_decompose_async) and writes the z-slice z in [rank 2^(n-g), (rank+1) 2^(n-g))
  * of every output block, world = 2^g <= 2^n: out_local has ptdr_output_count(n, s) / world

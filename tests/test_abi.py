@@ -172,3 +172,10 @@ def test_padded_workspace_rules(L):
     assert L.ptdr_padded_workspace_bytes(3000, 0) == ptdr.workspace_bytes(12, "general")
     assert L.ptdr_padded_workspace_bytes(1000, 0) >= 16 * 4 ** 10
     assert L.ptdr_padded_workspace_bytes(3000, 1) >= 16 * 4 ** 12 + ptdr.workspace_bytes(12, "hermitian")
+
+
+def test_structure_enum_matches_binding():
+    """The binding's structure names map to the values include/ptdr.h declares."""
+    hdr = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "ptdr.h")).read()
+    enum = dict((name.lower(), int(v)) for name, v in re.findall(r"PTDR_([A-Z_]+)\s*=\s*(\d+)", hdr.split("} ptdr_structure;")[0].split("typedef enum {")[-1]))
+    assert enum == ptdr.STRUCTURES

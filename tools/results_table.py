@@ -10,6 +10,8 @@ for line in open(sys.argv[1]):
     if "config" not in d:
         continue
     ms = d.get("ms", d.get("ms_per_rank"))
+    if ms is None:
+        continue
     cps = d.get("coeffs_per_s", d.get("coeffs_per_s_total"))
     frac = d.get("frac_of_measured", d.get("frac_of_measured_16B"))
     orc = d.get("oracle_coeffs_per_s")

@@ -295,6 +295,13 @@ if __name__ == "__main__":
     if "all" in which or "small" in which:
         dense("n6", 6, 0, "general")
         dense("n10a", 10, 1, "general")
+        # the oracle's per-core rate: one thread, n = 10
+        import subprocess
+        r = subprocess.run([sys.executable, os.path.join(os.path.dirname(os.path.abspath(__file__)), "oracle_percore.py"),
+                            "10"], env=dict(os.environ, OMP_NUM_THREADS="1"), capture_output=True, text=True)
+        if r.returncode == 0:
+            print(json.dumps({"config": "n10a_oracle_one_core", **json.loads(r.stdout.strip().splitlines()[-1])}),
+                  flush=True)
         dense("n10b", 10, 1, "hermitian")
     if "all" in which or "n13" in which:
         dense("n13a", 13, 2, "hermitian")

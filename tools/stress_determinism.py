@@ -26,6 +26,32 @@ for n, variant, reps in [(11, "general", reps_small), (12, "general", reps_small
     res[f"n{n}_{variant}"] = {"reps": reps, "mismatches": bad}
     del A, ws, ref, out
     torch.cuda.empty_cache()
+# the inverse on the pipeline (q order and matrix layout), the tail pipeline (n = 24 diagonal)
+# and the fused tridiagonal expansion (both tridiagonal structures)
+for n, reps in [(12, reps_small), (15, reps_large)]:
+    c = ptdr.decompose(ptdr.generate_dense(n, 4, "general"))
+    ref = ptdr.reconstruct(c).clone()
+    out = torch.empty_like(ref)
+    bad = 0
+    for _ in range(reps):
+        out.fill_(float("nan"))
+        ptdr.reconstruct(c, out=out)
+        bad += 0 if torch.equal(torch.view_as_real(out).view(torch.int64), torch.view_as_real(ref).view(torch.int64)) else 1
+    res[f"n{n}_inverse_q"] = {"reps": reps, "mismatches": bad}
+    del c, ref, out
+    torch.cuda.empty_cache()
+for structure in ("diagonal", "tridiagonal", "hermitian_tridiagonal"):
+    B = ptdr.generate_band(24, 3, structure)
+    ref = ptdr.decompose(B, structure).clone()
+    out = torch.empty_like(ref)
+    bad = 0
+    for _ in range(reps_large):
+        out.fill_(float("nan"))
+        ptdr.decompose(B, structure, out=out)
+        bad += 0 if torch.equal(torch.view_as_real(out).view(torch.int64), torch.view_as_real(ref).view(torch.int64)) else 1
+    res[f"n24_{structure}"] = {"reps": reps_large, "mismatches": bad}
+    del B, ref, out
+    torch.cuda.empty_cache()
 res["seconds"] = round(time.time() - t0, 1)
 print(json.dumps(res))
 assert all(v["mismatches"] == 0 for k, v in res.items() if k != "seconds"), res

@@ -121,6 +121,29 @@ def test_band_n20_sampled(gpu):
     assert np.max(np.abs(got - want)) <= TOL * np.max(np.abs(diags))
 
 
+@pytest.mark.parametrize("n,s", [(14, 1), (15, 3), (16, 17), (17, 64)])
+def test_band_top_levels_gather(gpu, n, s):
+    """n >= 14: the gather runs the top butterfly levels of every long segment (three, four for
+    x = 0) and scatters the short segments and the rows whose + d crosses a top-block boundary
+    one by one (band.cu band_gather_top3_kernel); sampled against the oracle in every block,
+    with the strings of the last rows of each top block included."""
+    torch = _torch()
+    rng = np.random.default_rng(4000 + n + s)
+    diags = _cplx(rng, (2 * s + 1, 1 << n))
+    out = ptdr.decompose_band(torch.from_numpy(diags).cuda(), s).cpu().numpy().reshape(-1, 1 << n)
+    xs = ptdr.band_xmasks(n, s)
+    N = 1 << n
+    bs = np.concatenate([np.arange(len(xs)), rng.integers(0, len(xs), 1500)])
+    zs = np.concatenate([np.full(len(xs), N - 1), rng.integers(0, N, 1500)])
+    qs = np.array([q_of(int(xs[b]), int(z), n) for b, z in zip(bs, zs)], dtype=np.uint64)
+    want = oracle.coeffs_band(diags, s, qs)
+    err = np.max(np.abs(out[bs, zs] - want))
+    assert err <= TOL * np.max(np.abs(diags)), err
+    # Parseval over all blocks: sum |alpha|^2 = ||A||_F^2 / 2^n (entries inside the matrix only)
+    fro2 = sum(float(np.sum(np.abs(diags[d + s, max(0, -d):N - max(0, d)]) ** 2)) for d in range(-s, s + 1))
+    assert abs(float(np.sum(np.abs(out) ** 2)) - fro2 / N) <= 1e-11 * fro2 / N
+
+
 @pytest.mark.parametrize("n,s,full", [(9, 17, True), (10, 33, False), (12, 64, False)])
 def test_band_wide(gpu, n, s, full):
     """Wide bands: blocks with more than 8 segments (|L_x| = #m * 2^popcount(e), e = 2^{t+1}-1-x

@@ -246,6 +246,30 @@ def inverse_layout(name, n, inplace_call):
     torch.cuda.empty_cache()
 
 
+def xshard(name, n, world):
+    """BASELINE configs[4] at G GPUs, per rank, kernel side: the X-mask shard decomposition
+    one rank runs after its all-to-all (ranks 0 and G-1 emulated on this GPU; the exchange
+    itself is timed in bench.py's N > 1 line)."""
+    R = (1 << n) // world
+    A = ptdr.generate_dense(n, 4, "general", device="cuda")
+    V = A.view(world, R, world, R)
+    ws = ptdr.alloc_workspace(n, "general", world, "cuda")
+    out = torch.empty(4 ** n // world, dtype=torch.complex128, device="cuda")
+    ms = 0.0
+    for h in (0, world - 1):
+        recv = torch.stack([V[g, :, g ^ h, :] for g in range(world)]).contiguous().view(1 << n, R)
+        ms = max(ms, time_it(lambda: ptdr.decompose_xshard(recv, n, h, world, out=out, workspace=ws)))
+        del recv
+    coeffs = 4 ** n // world
+    gbs = 32 * coeffs / (ms * 1e-3) / 1e9
+    a2a = 16 * coeffs * (world - 1) // world
+    print(json.dumps({"config": name, "n": n, "world": world, "ms_per_rank": ms, "coeffs_per_s_total": 4 ** n / (ms * 1e-3),
+                      "hbm_gbs_per_rank": gbs, "frac_of_measured": gbs / PEAK, "a2a_bytes_sent_per_rank": a2a}),
+          flush=True)
+    del A, V, ws, out
+    torch.cuda.empty_cache()
+
+
 def inplace(name, n, seed):
     """BASELINE configs[4] "n=16 at 1 GPU in-place": ptdr_decompose_inplace_async overwrites A
     with its coefficients (matrix layout); A is regenerated before every timed call (the
@@ -325,6 +349,11 @@ if __name__ == "__main__":
         dense("n15", 15, 4, "general")
         dense("n15_hermitian", 15, 4, "hermitian")
         dense("n16", 16, 4, "general")
+    if "all" in which or "xshard" in which:
+        xshard("n15_2gpu_xshard_kernel", 15, 2)
+        xshard("n15_4gpu_xshard_kernel", 15, 4)
+        xshard("n15_8gpu_xshard_kernel", 15, 8)
+        xshard("n16_8gpu_xshard_kernel", 16, 8)
     if "inverse" in which:
         inverse("n15_inverse", 15)
         inverse_layout("n15_inverse_matrix_layout", 15, False)

@@ -9,6 +9,9 @@
 //   zl = z mod 2^{t+1}, zh = z >> (t+1), s1 = (-1)^{popcount(z mod 2^t)}, s2 = (-1)^{z_t}:
 //   alpha(x_b, z) = 2^-n i^{popcount(zl)} s1 (s1 == s2 ? P_t[zh] : M_t[zh]).
 //   DESIGN.md derives this from the per-x WHT identity.
+// HERMITIAN_TRIDIAGONAL: U_t = conj(S_t), so one W_t = WHT(S_t) per segment gives
+//   P_t = (2 Re W_t, 0) and M_t = (0, 2 Im W_t) (herm_seg_view).
+// ANTI_DIAGONAL and BAND(s) (the (2s+1)-band planner) follow further down.
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>

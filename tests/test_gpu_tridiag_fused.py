@@ -137,3 +137,21 @@ def test_hermitian_tridiagonal_generator_and_n24(gpu):
         b = ptdr.decompose_zshard(G, "tridiagonal", r, 8)
         assert torch.equal(torch.view_as_real(a), torch.view_as_real(b)), r
     torch.cuda.empty_cache()
+
+
+def test_hermitian_tridiagonal_host_entry_points(gpu):
+    """ptdr_decompose_host and the streaming host plan accept the new structure ([2, 2^n]
+    input) and return the device result."""
+    import torch
+
+    n = 17
+    sub, main, sup = _herm_band(n, 901)
+    H = np.ascontiguousarray(np.stack([main, sup]))
+    want = ptdr.decompose(torch.from_numpy(H).cuda(), "hermitian_tridiagonal").cpu().numpy()
+    got = ptdr.decompose_host(H, "hermitian_tridiagonal")
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+    out = np.empty_like(want)
+    with ptdr.HostPlan(n, "hermitian_tridiagonal", depth=2) as plan:
+        plan.decompose_async(H, out)
+        plan.wait()
+    assert np.array_equal(out.view(np.uint64), want.view(np.uint64))
